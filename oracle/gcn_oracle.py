@@ -1,0 +1,398 @@
+"""Plain FP64 definition of one GCN training epoch (Morphling hot path).
+
+TEST INFRASTRUCTURE ONLY — see oracle/__init__.py.  Nothing here is blocked,
+fused or reordered beyond what the cited definition states; numpy / scipy
+primitives (matmul, sort, sparse matmul) serve as single steps.
+
+Notation: A symmetric 0/1 adjacency without self loops,
+Ã = A + I, d̃ = Ã·1, Â = D̃^{-1/2} Ã D̃^{-1/2}; layer ℓ maps F_{ℓ-1} -> F_ℓ.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+import scipy.sparse as sp
+
+__all__ = [
+    "OracleError", "Graph", "graph_build", "a_hat_values", "a_hat_dense_from_csr",
+    "aggregate", "aggregate_rows", "analyze_features", "FeatureAnalysis",
+    "splitmix64_stream", "xavier_init", "philox4x32_10", "dropout_keep",
+    "dropout_threshold", "forward", "softmax_ce", "backward", "adam_step", "train",
+    "partition_1d", "localize", "LocalPlan", "GOLDEN",
+]
+
+GOLDEN = 0x9E3779B97F4A7C15
+_M64 = (1 << 64) - 1
+
+
+class OracleError(ValueError):
+    """Error with the C-ABI class name (SURVEY §8(b) error table)."""
+
+    def __init__(self, code: str, msg: str):
+        super().__init__(f"{code}: {msg}")
+        self.code = code
+
+
+# ---------------------------------------------------------------------------
+# a0 — graph build.  SURVEY c.2 G1-G6; PAPER P:222 ("CSR ... once during
+# initialization").  Readings Q2-Q4 (symmetrise, dedup, drop
+# input self loops, add I).
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class Graph:
+    num_nodes: int
+    row_ptr: np.ndarray   # int64[N+1]
+    col_idx: np.ndarray   # int32[nnz], ascending per row, diagonal included
+    deg: np.ndarray       # int32[N] = d̃
+    dinv: np.ndarray      # float32[N] = (float)(1/sqrt((double)d̃))  (G6 bit recipe)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    @property
+    def rows(self) -> np.ndarray:
+        return np.repeat(np.arange(self.num_nodes, dtype=np.int64), np.diff(self.row_ptr))
+
+
+def graph_build(src, dst, num_nodes: int) -> Graph:
+    n = int(num_nodes)
+    if n <= 0:
+        raise OracleError("EDEGENERATE", "N = 0")                        # G1
+    src = np.asarray(src, dtype=np.int64)
+    dst = np.asarray(dst, dtype=np.int64)
+    if src.shape != dst.shape:
+        raise OracleError("EINVAL", "src/dst length mismatch")
+    if src.size and (src.min() < 0 or dst.min() < 0 or src.max() >= n or dst.max() >= n):
+        raise OracleError("ERANGE", "node id outside [0, N)")            # G1
+    off = src != dst                                                     # G2: drop self loops
+    u = np.concatenate([src[off], dst[off]])                             # G2: symmetrise
+    v = np.concatenate([dst[off], src[off]])
+    diag = np.arange(n, dtype=np.int64)
+    keys = np.concatenate([u * n + v, diag * n + diag])                  # G3: S ∪ I
+    keys = np.unique(keys)                                               # G2 dedup, G4 (u,v) order
+    rows = keys // n
+    cols = keys % n
+    counts = np.bincount(rows, minlength=n).astype(np.int64)
+    row_ptr = np.zeros(n + 1, dtype=np.int64)                            # G4
+    np.cumsum(counts, out=row_ptr[1:])
+    deg = counts.astype(np.int32)                                        # G5
+    dinv = (1.0 / np.sqrt(deg.astype(np.float64))).astype(np.float32)   # G6
+    return Graph(n, row_ptr, cols.astype(np.int32), deg, dinv)
+
+
+def a_hat_values(g: Graph) -> np.ndarray:
+    """â_e = 1/sqrt(d̃_u d̃_v) in FP64 for every CSR entry (G6; Q1)."""
+    d = g.deg.astype(np.float64)
+    return 1.0 / np.sqrt(d[g.rows] * d[g.col_idx.astype(np.int64)])
+
+
+def _a_hat_csr(g: Graph) -> sp.csr_matrix:
+    return sp.csr_matrix((a_hat_values(g), g.col_idx.astype(np.int64), g.row_ptr),
+                         shape=(g.num_nodes, g.num_nodes))
+
+
+def a_hat_dense_from_csr(g: Graph) -> np.ndarray:
+    return _a_hat_csr(g).toarray()
+
+
+def aggregate(g: Graph, P: np.ndarray) -> np.ndarray:
+    """Y = Â·P in FP64 (F2 / B2).  Alg. 3 P:373-384 computes the same sum
+    Y[u,f] = Σ_{ei∈row u} val[ei]·X[col[ei], f]; here val = â (Q1)."""
+    P = np.asarray(P, dtype=np.float64)
+    return np.asarray(_a_hat_csr(g) @ P)
+
+
+def aggregate_rows(g: Graph, P: np.ndarray, rows) -> np.ndarray:
+    """Â·P for a subset of output rows, one row at a time (full-size sampling)."""
+    d = g.deg.astype(np.float64)
+    out = np.zeros((len(rows), P.shape[1]), dtype=np.float64)
+    for i, u in enumerate(rows):
+        s, e = int(g.row_ptr[u]), int(g.row_ptr[u + 1])
+        cols = g.col_idx[s:e].astype(np.int64)
+        w = 1.0 / np.sqrt(d[u] * d[cols])
+        out[i] = w @ np.asarray(P[cols], dtype=np.float64)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# a1 — feature analysis and the dense/sparse switch.  Alg. 1 Initialize
+# P:256-266; Eq. 1; τ≈0.80 P:216; readings Q11, Q12, Q28.
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class FeatureAnalysis:
+    nnz: int
+    mode: int              # 0 Dense, 1 Sparse
+    is_binary: bool
+    sparsity: float        # s = 1 - nnz/(N*F)
+    csr: tuple | None      # (ptr int64[N+1], idx int32[nnz], val f32[nnz])
+    csc: tuple | None      # (ptr int64[F+1], idx int32[nnz] rows ascending, val f32[nnz])
+
+
+def analyze_features(X: np.ndarray, tau_bp: int = 8000, force_mode: int = -1) -> FeatureAnalysis:
+    X = np.asarray(X, dtype=np.float32)
+    n, f = X.shape
+    if n * f == 0:
+        raise OracleError("EDEGENERATE", "N*F = 0")
+    nz = X != np.float32(0.0)                                   # S1 (IEEE compare, Q12)
+    nnz = int(nz.sum())
+    sparse = 10000 * nnz <= (10000 - int(tau_bp)) * n * f       # S2: s >= τ, integer-decided
+    mode = int(sparse) if force_mode < 0 else int(force_mode)
+    s = 1.0 - nnz / (n * f)
+    is_binary = bool(np.all(X[nz] == np.float32(1.0)))
+    csr = csc = None
+    if mode == 1:                                               # S3
+        r, c = np.nonzero(nz)                                   # row-major order
+        ptr = np.zeros(n + 1, np.int64)
+        np.cumsum(np.bincount(r, minlength=n), out=ptr[1:])
+        csr = (ptr, c.astype(np.int32), X[r, c].astype(np.float32))
+        ct, rt = np.nonzero(nz.T)                               # column-major, rows ascending
+        cptr = np.zeros(f + 1, np.int64)
+        np.cumsum(np.bincount(ct, minlength=f), out=cptr[1:])
+        csc = (cptr, rt.astype(np.int32), X[rt, ct].astype(np.float32))
+    return FeatureAnalysis(nnz, mode, is_binary, s, csr, csc)
+
+
+# ---------------------------------------------------------------------------
+# Xavier initialisation ("xaviers", Listing 1; bound S:322; stream Q16)
+# ---------------------------------------------------------------------------
+def splitmix64_stream(seed: int, count: int) -> np.ndarray:
+    """The splitmix64 sequence, written out sequentially (Q16)."""
+    out = np.empty(count, dtype=np.uint64)
+    state = seed & _M64
+    for i in range(count):
+        state = (state + GOLDEN) & _M64
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+        out[i] = z ^ (z >> 31)
+    return out
+
+
+def xavier_init(dims, seed: int):
+    """W_ℓ ~ U(-a, a), a = sqrt(6/(f_in+f_out)) on unpadded fans; b_ℓ = 0 (Q6, Q16).
+
+    Stream for layer ℓ (1-based): splitmix64 seeded seed ^ (ℓ·GOLDEN mod 2^64),
+    row-major fill of [f_in, f_out]; value a·(2·(x>>40)/2^24 − 1) in double,
+    rounded once to f32.
+    """
+    Ws, bs = [], []
+    for l in range(1, len(dims)):
+        fi, fo = int(dims[l - 1]), int(dims[l])
+        a = math.sqrt(6.0 / (fi + fo))
+        x = splitmix64_stream(seed ^ ((l * GOLDEN) & _M64), fi * fo)
+        u24 = (x >> np.uint64(40)).astype(np.float64)
+        w = a * (2.0 * u24 / float(1 << 24) - 1.0)
+        Ws.append(w.astype(np.float32).reshape(fi, fo))
+        bs.append(np.zeros(fo, dtype=np.float32))
+    return Ws, bs
+
+
+# ---------------------------------------------------------------------------
+# Dropout mask (Q10): Philox4x32-10, key=(seed lo, seed hi),
+# counter=(row, col/4, layer, epoch), lane col%4; keep iff u32 >= floor(p·2^32).
+# ---------------------------------------------------------------------------
+_PM0, _PM1 = 0xD2511F53, 0xCD9E8D57
+_PW0, _PW1 = 0x9E3779B9, 0xBB67AE85
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32 with 10 rounds (Salmon et al. 2011, Random123); vectorised over
+    leading axes: ctr uint64-able [...,4], key [...,2]; returns uint32 [...,4]."""
+    c = [np.asarray(ctr[..., i], dtype=np.uint64) & np.uint64(0xFFFFFFFF) for i in range(4)]
+    k0 = np.asarray(key[..., 0], dtype=np.uint64) & np.uint64(0xFFFFFFFF)
+    k1 = np.asarray(key[..., 1], dtype=np.uint64) & np.uint64(0xFFFFFFFF)
+    mask = np.uint64(0xFFFFFFFF)
+    for r in range(10):
+        if r > 0:
+            k0 = (k0 + np.uint64(_PW0)) & mask
+            k1 = (k1 + np.uint64(_PW1)) & mask
+        p0 = np.uint64(_PM0) * c[0]
+        p1 = np.uint64(_PM1) * c[2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & mask
+        hi1, lo1 = p1 >> np.uint64(32), p1 & mask
+        c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
+    return np.stack([x.astype(np.uint32) for x in c], axis=-1)
+
+
+def dropout_threshold(p: float) -> int:
+    return int(math.floor(float(np.float32(p)) * 4294967296.0))
+
+
+def dropout_keep(n_rows: int, n_cols: int, p: float, seed: int, layer: int, epoch: int,
+                 row0: int = 0) -> np.ndarray:
+    """Boolean keep mask [n_rows, n_cols] for hidden layer `layer` at `epoch` (Q10)."""
+    rows = np.arange(row0, row0 + n_rows, dtype=np.uint64)
+    cols = np.arange(n_cols, dtype=np.uint64)
+    ctr = np.zeros((n_rows, n_cols, 4), dtype=np.uint64)
+    ctr[..., 0] = rows[:, None]
+    ctr[..., 1] = (cols // np.uint64(4))[None, :]
+    ctr[..., 2] = np.uint64(layer)
+    ctr[..., 3] = np.uint64(epoch)
+    key = np.zeros((n_rows, n_cols, 2), dtype=np.uint64)
+    key[..., 0] = np.uint64(seed & 0xFFFFFFFF)
+    key[..., 1] = np.uint64((seed >> 32) & 0xFFFFFFFF)
+    out = philox4x32_10(ctr, key)
+    lane = (cols % np.uint64(4)).astype(np.int64)
+    u32 = np.take_along_axis(out, np.broadcast_to(lane[None, :, None], (n_rows, n_cols, 1)), axis=2)[..., 0]
+    return u32.astype(np.uint64) >= np.uint64(dropout_threshold(p))
+
+
+# ---------------------------------------------------------------------------
+# Forward (c.2 F1-F4): layer update of P:92 with Q1 (Â), Q6 (bias),
+# Q8 (ReLU hidden, identity output), Q10 (dropout after ReLU).
+# ---------------------------------------------------------------------------
+def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1):
+    H = np.asarray(X, dtype=np.float64)
+    hs, zs = [H], []
+    L = len(Ws)
+    for l in range(1, L + 1):
+        P = H @ np.asarray(Ws[l - 1], dtype=np.float64)                 # F1
+        Z = aggregate(g, P) + np.asarray(bs[l - 1], dtype=np.float64)   # F2
+        zs.append(Z)
+        if l < L:
+            H = np.maximum(Z, 0.0)                                       # F3
+            if dropout_p > 0.0:
+                keep = dropout_keep(Z.shape[0], Z.shape[1], dropout_p, seed, l, epoch)
+                H = H * keep / (1.0 - float(np.float32(dropout_p)))
+            hs.append(H)
+    return zs[-1], {"H": hs, "Z": zs, "dropout_p": dropout_p, "seed": seed, "epoch": epoch}
+
+
+def softmax_ce(Z, labels, mask=None, n_lab: int | None = None):
+    """L1-L3 (Q9, Q17, Q25): mean softmax cross-entropy over labelled rows."""
+    Z = np.asarray(Z, dtype=np.float64)
+    labels = np.asarray(labels, dtype=np.int64)
+    lab = np.ones(Z.shape[0], bool) if mask is None else np.asarray(mask, bool)
+    nl = int(lab.sum()) if n_lab is None else int(n_lab)
+    m = Z.max(axis=1)
+    lse = m + np.log(np.exp(Z - m[:, None]).sum(axis=1))               # L1
+    rows = np.nonzero(lab)[0]
+    loss = float((lse[rows] - Z[rows, labels[rows]]).sum() / nl)        # L2
+    dZ = np.exp(Z - lse[:, None])
+    dZ[np.arange(Z.shape[0]), labels] -= 1.0
+    dZ /= nl                                                             # L3
+    dZ[~lab] = 0.0
+    return loss, dZ
+
+
+def backward(g: Graph, cache, Ws, dZ):
+    """B1-B4: returns (dWs, dbs)."""
+    L = len(Ws)
+    dWs, dbs = [None] * L, [None] * L
+    for l in range(L, 0, -1):
+        dbs[l - 1] = dZ.sum(axis=0)                                     # B1
+        G = aggregate(g, dZ)                                             # B2 (Âᵀ = Â)
+        dWs[l - 1] = cache["H"][l - 1].T @ G                             # B3
+        if l > 1:
+            dH = G @ np.asarray(Ws[l - 1], dtype=np.float64).T           # B4
+            dZ = dH * (cache["Z"][l - 2] > 0.0)                          # ReLU'(0) := 0 (Q8)
+            if cache["dropout_p"] > 0.0:
+                keep = dropout_keep(dZ.shape[0], dZ.shape[1], cache["dropout_p"], cache["seed"],
+                                    l - 1, cache["epoch"])
+                dZ = dZ * keep / (1.0 - float(np.float32(cache["dropout_p"])))
+    return dWs, dbs
+
+
+def adam_step(params, grads, m, v, t: int, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8):
+    """A1 (P:170 lr/β1/β2, Q15 ε outside sqrt, bias-corrected, t from 1). In place."""
+    for p, gr, mm, vv in zip(params, grads, m, v):
+        mm *= beta1
+        mm += (1.0 - beta1) * gr
+        vv *= beta2
+        vv += (1.0 - beta2) * gr * gr
+        mhat = mm / (1.0 - beta1 ** t)
+        vhat = vv / (1.0 - beta2 ** t)
+        p -= lr * mhat / (np.sqrt(vhat) + eps)
+
+
+def train(g: Graph, X, labels, dims, epochs: int, seed: int = 42, lr=0.01, beta1=0.9,
+          beta2=0.999, eps=1e-8, mask=None, dropout_p: float = 0.0, dropout_seed: int = 0,
+          init=None):
+    """Epoch loop (Listing 1): loss_t at θ_{t-1}, backward, Adam -> θ_t."""
+    if init is None:
+        Ws, bs = xavier_init(dims, seed)
+    else:
+        Ws, bs = init
+    params = [np.asarray(w, np.float64).copy() for w in Ws] + [np.asarray(b, np.float64).copy() for b in bs]
+    L = len(Ws)
+    m = [np.zeros_like(p) for p in params]
+    v = [np.zeros_like(p) for p in params]
+    losses = []
+    for t in range(1, epochs + 1):
+        Z, cache = forward(g, X, params[:L], params[L:], dropout_p, dropout_seed, t)
+        loss, dZ = softmax_ce(Z, labels, mask)
+        losses.append(loss)
+        dWs, dbs = backward(g, cache, params[:L], dZ)
+        adam_step(params, dWs + dbs, m, v, t, lr, beta1, beta2, eps)
+    return losses, params
+
+
+# ---------------------------------------------------------------------------
+# Distributed plans (c.2 D1-D5): 1D contiguous partition balanced by Σ d̃
+# (Phase III weight deg+1, Alg. 4; Q20), G2L local-then-ghost layout
+# (P:514-515), halo lists (Q21).
+# ---------------------------------------------------------------------------
+def partition_1d(row_ptr, world: int) -> np.ndarray:
+    """bounds[r] = min{u in [0,N] : world·row_ptr[u] >= r·nnz} (D1)."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    nnz = int(row_ptr[-1])
+    bounds = np.empty(world + 1, dtype=np.int64)
+    u = 0
+    for r in range(world + 1):
+        while world * int(row_ptr[u]) < r * nnz:
+            u += 1
+        bounds[r] = u
+    return bounds
+
+
+@dataclasses.dataclass
+class LocalPlan:
+    rank: int
+    n_own: int
+    row0: int
+    ghosts: np.ndarray        # int64 global ids, ascending (D2)
+    row_ptr: np.ndarray       # int64[n_own+1] local CSR
+    col_idx: np.ndarray       # int32 local ids, [owned | ghosts] per row (D3)
+    split: np.ndarray         # int64[n_own]: index in the row where ghost columns start
+    recv_offset: np.ndarray   # int64[world]: offset of peer q's slice inside the ghost region
+    n_recv: np.ndarray        # int64[world]
+    send_ids: list            # per peer: ascending owned LOCAL ids to send (D4)
+
+
+def localize(g: Graph, bounds, rank: int) -> LocalPlan:
+    bounds = np.asarray(bounds, dtype=np.int64)
+    world = len(bounds) - 1
+    b0, b1 = int(bounds[rank]), int(bounds[rank + 1])
+    n_own = b1 - b0
+    s, e = int(g.row_ptr[b0]), int(g.row_ptr[b1])
+    cols = g.col_idx[s:e].astype(np.int64)
+    is_ghost = (cols < b0) | (cols >= b1)
+    ghosts = np.unique(cols[is_ghost])                                   # D2
+    lid = np.where(is_ghost, n_own + np.searchsorted(ghosts, cols), cols - b0)   # D3
+    local_rp = g.row_ptr[b0:b1 + 1] - s
+    new_cols = np.empty_like(lid)
+    split = np.empty(n_own, dtype=np.int64)
+    for i in range(n_own):
+        a, b = int(local_rp[i]), int(local_rp[i + 1])
+        row = np.sort(lid[a:b])
+        new_cols[a:b] = row
+        split[i] = int((row < n_own).sum())
+    owner = np.searchsorted(bounds, ghosts, side="right") - 1
+    n_recv = np.bincount(owner, minlength=world).astype(np.int64)
+    recv_offset = np.zeros(world, dtype=np.int64)
+    np.cumsum(n_recv[:-1], out=recv_offset[1:])
+    send_ids = []
+    for q in range(world):
+        if q == rank:
+            send_ids.append(np.zeros(0, dtype=np.int64))
+            continue
+        q0, q1 = int(bounds[q]), int(bounds[q + 1])
+        qs, qe = int(g.row_ptr[q0]), int(g.row_ptr[q1])
+        qc = g.col_idx[qs:qe].astype(np.int64)
+        need = np.unique(qc[(qc >= b0) & (qc < b1)])                    # D4
+        send_ids.append(need - b0)
+    return LocalPlan(rank, n_own, b0, ghosts, local_rp.astype(np.int64), new_cols.astype(np.int32),
+                     split, recv_offset, n_recv, send_ids)
