@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark: GCN ms/epoch (fwd+bwd+Adam) on B200, with SpMM roofline and CPU-oracle baseline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit] [--impl ours|reference]
+
+One JSON line on rank 0 (BASELINE.json metric).  An epoch is SURVEY §8(d)'s step a2..a11:
+forward, softmax-CE, backward, (halo + gradient all-reduce when N > 1) and Adam, on a
+synthetic graph shaped like the named config (synth/, seeded).  For N > 1 launch with
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N
+(one rank per GPU, NCCL; the graph is 1D row-partitioned, so total work is fixed: strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "GCN ms/epoch (fwd+bwd+Adam) at 1/2/4/8 B200; SpMM HBM GB/s vs peak"
+UNIT = "ms/epoch"
+FALLBACK_HBM_GBS = 6650.0
+# CPU-oracle sample: the same generator recipe at 1/k scale (same mean degree, widths, classes)
+SAMPLE_SCALE = {"cora": 1, "pubmed": 1, "arxiv": 4, "reddit": 16, "products": 32}
+PROF_KINDS = {0: "spmm", 1: "gemm_nt", 2: "gemm_tn", 3: "softmax_ce", 4: "adam", 5: "sparse_feat", 6: "halo"}
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", FALLBACK_HBM_GBS)), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------- oracle sample
+def _oracle_sample(name: str, seed_offset: int = 0):
+    """The same workload recipe at 1/k scale, for the CPU oracle (bounded sample)."""
+    from synth.generate import CONFIGS, make_features, make_graph, make_labels
+    cfg = CONFIGS[name]
+    k = SAMPLE_SCALE[name]
+    n = max(64, cfg.num_nodes // k)
+    nnz = cfg.nnz_a // k
+    y = make_labels(n, cfg.num_classes)
+    src, dst = make_graph(n, nnz, cfg.num_classes, cfg.alpha, cfg.mu, cfg.seed + seed_offset)
+    X = make_features(n, cfg.num_features, y, cfg.num_classes, cfg.feature_kind, cfg.density, cfg.seed)
+    return {"src": src, "dst": dst, "X": X, "y": y, "n": n, "nnz_a": nnz, "k": k, "cfg": cfg}
+
+
+def _oracle_epoch_ms(sample, epochs: int):
+    """Time `epochs` epochs of the oracle (as it stands) on the sample; return per-epoch ms scaled to
+    the full workload (x k: every step is linear in N at fixed mean degree)."""
+    import oracle
+    g = oracle.graph_build(sample["src"], sample["dst"], sample["n"])
+    times = []
+    for e in range(epochs):
+        t0 = time.perf_counter()
+        oracle.train(g, sample["X"], sample["y"], sample["cfg"].dims, epochs=1, seed=42)
+        times.append(time.perf_counter() - t0)
+    return [t * 1e3 * sample["k"] for t in times]
+
+
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+        return int(n)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _sample_desc(sample):
+    c = sample["cfg"]
+    return (f"oracle (FP64 numpy/scipy) full epoch on a {c.name}-shaped graph at 1/{sample['k']} scale "
+            f"(N={sample['n']}, nnz(A)={sample['nnz_a']}, dims={list(c.dims)}), time x{sample['k']}")
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    sample = _oracle_sample(args.config)
+    for _ in range(args.warmup):
+        _oracle_epoch_ms(sample, 1)
+    ms = _oracle_epoch_ms(sample, args.steps)
+    v = statistics.median(ms)
+    cores = _cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "oracle_scale": f"1/{sample['k']}"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": _sample_desc(sample)},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------- our arm
+def _build_model(P, torch, w, world, rank, comm):
+    cfg = w["cfg"]
+    n = cfg.num_nodes
+    X = w["X"]
+    if world == 1:
+        g = P.Graph(w["src"], w["dst"], n)
+        f = P.Features(torch.from_numpy(X).cuda())
+        m = P.GCN(g, f, cfg.dims)
+        y = torch.from_numpy(w["y"]).cuda()
+        own = (0, n)
+        extra = {}
+    else:
+        gfull = P.Graph(w["src"], w["dst"], n)
+        rp, ci = gfull.csr()[0].cpu().numpy(), gfull.csr()[1].cpu().numpy()
+        del gfull
+        bounds = P.partition_1d(rp, world)
+        plan = P.Plan(rp, ci, n, bounds, rank)
+        del rp, ci
+        g = P.Graph.from_plan(plan)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        f = P.Features(torch.from_numpy(np.ascontiguousarray(X[r0:r1])).cuda())
+        m = P.GCN(g, f, cfg.dims, comm=comm)
+        y = torch.from_numpy(np.ascontiguousarray(w["y"][r0:r1])).cuda()
+        own = (r0, r1)
+        extra = {"n_ghost": plan.n_ghost, "halo_rows_sent": plan.n_send}
+    m.init_xavier(42)
+    m.set_labels(y, n_lab_global=n)
+    return g, f, m, y, own, extra
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2512_01678_b200 as P
+    from paper_2512_01678_b200 import _lib as L
+    from synth.generate import make_workload
+
+    import ctypes as C
+    L.mph_device_check(C.byref(C.c_int32()))
+    t_setup = time.perf_counter()
+    w = make_workload(args.config)
+    t_gen = time.perf_counter() - t_setup
+    comm = P.Comm(world, rank) if world > 1 else None
+    t0 = time.perf_counter()
+    g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    cfg = w["cfg"]
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for t in range(1, args.warmup + 1):
+        m.train_epoch(t)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---------------- device-timed region: K epochs, inputs resident in HBM
+    clocks = ClockSampler(local)
+    L.mph_profile_enable(1)
+    launches0 = L.launch_count()
+    clocks.start()
+    time.sleep(0.15)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for t in range(args.warmup + 1, args.warmup + args.steps + 1):
+        m.train_epoch(t)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = L.launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    kernels = {}
+    for kind, name in PROF_KINDS.items():
+        cnt, tms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        L.mph_profile_read(kind, C.byref(cnt), C.byref(tms), C.byref(by), C.byref(fl))
+        if cnt.value:
+            kernels[name] = {"launches_per_epoch": cnt.value / args.steps, "ms_per_epoch": tms.value / args.steps,
+                             "avg_launch_ms": tms.value / cnt.value, "algorithmic_GBps": by.value / tms.value / 1e6,
+                             "bytes_per_launch": by.value / cnt.value, "TFLOPs": fl.value / tms.value / 1e9}
+    L.mph_profile_enable(0)
+    loss_last = m.loss_buf.item()
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = tt.item()
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        X = w["X"][own[0]:own[1]]
+        Xh = torch.from_numpy(np.ascontiguousarray(X)).pin_memory()
+        yh = torch.from_numpy(np.ascontiguousarray(w["y"][own[0]:own[1]])).pin_memory()
+        lh = torch.zeros(1, dtype=torch.float64).pin_memory()
+        ysrc = y  # device label buffer the model reads
+        steps_e2e = max(3, args.steps // 2)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        base = args.warmup + args.steps
+        for t in range(base + 1, base + steps_e2e + 1):
+            L.mph_gcn_upload_features(m.h, Xh.data_ptr(), X.shape[1], stream.cuda_stream)
+            ysrc.copy_(yh, non_blocking=True)
+            m.train_epoch(t)
+            lh.copy_(m.loss_buf, non_blocking=True)
+            stream.synchronize()  # the step's result is on the host
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / steps_e2e
+        if world > 1:
+            tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = tt.item()
+        e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 4 + yh.numel() * 4),
+               "d2h_bytes_per_step": 8, "steps": steps_e2e}
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_kind = _peaks()
+    dom = max((k for k in ("spmm", "gemm_nt", "gemm_tn") if k in kernels), key=lambda k: kernels[k]["ms_per_epoch"],
+              default=None)
+    roofline = None
+    if dom is not None:
+        kd = kernels[dom]
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+        if os.path.exists(tp):
+            with open(tp) as fh:
+                traffic = json.load(fh).get(dom, {}).get("dram_bytes_per_launch")
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": peak, "unit": "GB/s",
+                    "frac": kd["algorithmic_GBps"] / peak, "traffic": traffic,
+                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                    "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_ms": kd["avg_launch_ms"],
+                    "share_of_epoch": kd["ms_per_epoch"] / ms}
+
+    # ---------------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        sample = _oracle_sample(args.config)
+        ms_cpu = _oracle_epoch_ms(sample, 1)
+        cpu = {"value": statistics.median(ms_cpu), "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
+               "sample": _sample_desc(sample)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": False, "scaling": "strong" if world > 1 else "strong",
+            "vs_baseline": None, "dtype": "f32 (SpMM, loss, Adam) + tf32 tensor-core GEMMs", "data": "synthetic",
+            "config": {"workload": args.config, "nodes": cfg.num_nodes, "nnz_A": cfg.nnz_a, "dims": list(cfg.dims),
+                       "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
+                       "parallelism": f"1d-row-partition x{world}" if world > 1 else "single-gpu",
+                       "layer_order": ["AF" if o else "TF" for o in m.order],
+                       "l2": "inputs larger than L2 (X and col_idx each > 126 MB); no flush",
+                       **extra},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "kernels": kernels, "final_loss": loss_last,
+            "setup_s": {"generate": round(t_gen, 2), "graph_build_and_init": round(t_build, 2)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        del m, f, g
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="reddit", choices=["cora", "pubmed", "arxiv", "reddit", "products"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

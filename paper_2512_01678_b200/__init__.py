@@ -1,0 +1,12 @@
+"""B200-native GCN training hot path of Morphling (arXiv 2512.01678).
+
+The compute lives in `lib/libmorphling.so` (CUDA, sm_100a) behind the C-ABI of
+include/morphling.h; `_lib` is its ctypes binding and `api` a thin object layer.
+Importing this package fails if the shared library has not been built — there is
+no CPU fallback.
+"""
+from . import _lib  # noqa: F401  (raises ImportError when the library is missing)
+from .api import (Comm, Features, GCN, Graph, Plan, device_view, pad_width,  # noqa: F401
+                  partition_1d, stream_ptr)
+
+__all__ = ["Comm", "Features", "GCN", "Graph", "Plan", "device_view", "pad_width", "partition_1d", "stream_ptr"]

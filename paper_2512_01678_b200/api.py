@@ -1,0 +1,319 @@
+"""Python API over the C-ABI (marshalling only; every step runs in libmorphling.so kernels).
+
+    g = Graph(src, dst, num_nodes)                         # a0, mph_graph_build
+    f = Features(X_cuda, tau_bp=8000)                      # a1, mph_features_create
+    m = GCN(g, f, dims=(602, 128, 41))                     # mph_gcn_create
+    m.init_xavier(42); m.set_labels(y_cuda)
+    loss = m.train_epoch(t=1)                              # a2..a11 + Adam, loss in a device double
+
+torch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import AdamCfg, Epilogue, GcnDesc, MorphlingError  # noqa: F401
+
+DEFAULT_ADAM = (0.01, 0.9, 0.999, 1e-8)  # Listing 1; eps reading Q15
+
+
+def pad_width(w: int) -> int:
+    return 4 if w <= 4 else (w + 7) // 8 * 8
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class _CAI:
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+_TYPESTR = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8", torch.uint8: "|u1"}
+
+
+def device_view(ptr: int, shape, dtype) -> torch.Tensor:
+    """Zero-copy torch view of library-owned device memory (borrowed: valid until the handle dies)."""
+    if int(np.prod(shape)) == 0 or not ptr:
+        return torch.empty(shape, dtype=dtype, device="cuda")
+    return torch.as_tensor(_CAI(ptr, shape, _TYPESTR[dtype]), device="cuda")
+
+
+def _out_ptr():
+    return C.c_void_p()
+
+
+class Graph:
+    """a0 — CSR of Â's pattern (symmetrised, deduplicated, self loops added) + deg + dinv."""
+
+    def __init__(self, src=None, dst=None, num_nodes: int = 0, stream=None, _handle=None):
+        if _handle is not None:
+            self.h = _handle
+        else:
+            src = np.ascontiguousarray(np.asarray(src, dtype=np.int32))
+            dst = np.ascontiguousarray(np.asarray(dst, dtype=np.int32))
+            h = _out_ptr()
+            L.mph_graph_build(src.ctypes.data, dst.ctypes.data, int(src.size), int(num_nodes), stream_ptr(stream),
+                              C.byref(h))
+            self.h = h
+        nr, nc, nnz, md = C.c_int32(), C.c_int32(), C.c_int64(), C.c_int32()
+        L.mph_graph_info(self.h, C.byref(nr), C.byref(nc), C.byref(nnz), C.byref(md))
+        self.n_rows, self.n_cols, self.nnz, self.max_deg = nr.value, nc.value, nnz.value, md.value
+
+    @classmethod
+    def from_plan(cls, plan: "Plan", stream=None) -> "Graph":
+        h = _out_ptr()
+        L.mph_graph_from_plan(plan.h, stream_ptr(stream), C.byref(h))
+        return cls(_handle=h)
+
+    def csr(self):
+        rp, ci, dg, di = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        L.mph_graph_csr(self.h, C.byref(rp), C.byref(ci), C.byref(dg), C.byref(di))
+        return (device_view(rp.value, (self.n_rows + 1,), torch.int64),
+                device_view(ci.value, (self.nnz,), torch.int32),
+                device_view(dg.value, (self.n_cols,), torch.int32),
+                device_view(di.value, (self.n_cols,), torch.float32))
+
+    @property
+    def dinv(self) -> torch.Tensor:
+        return self.csr()[3]
+
+    def spmm(self, inp: torch.Tensor, out: torch.Tensor, w: int | None = None, epi: Epilogue | None = None,
+             part: int = -1, stream=None):
+        w = inp.shape[1] if w is None else w
+        e = C.byref(epi) if epi is not None else None
+        L.mph_spmm_part(self.h, part, inp.data_ptr(), w, inp.stride(0), out.data_ptr(), out.stride(0), e,
+                        stream_ptr(stream))
+        return out
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            L.mph_graph_destroy(h)
+            self.h = None
+
+
+class Features:
+    """a1 — feature analysis + dense/sparse switch (Alg. 1 Initialize)."""
+
+    def __init__(self, X: torch.Tensor, tau_bp: int = 8000, force_mode: int = -1, stream=None):
+        assert X.is_cuda and X.dtype == torch.float32 and X.dim() == 2 and X.stride(1) == 1
+        h = _out_ptr()
+        L.mph_features_create(X.data_ptr(), X.shape[0], X.shape[1], X.stride(0), tau_bp, force_mode,
+                              stream_ptr(stream), C.byref(h))
+        self.h = h
+        self.N, self.F = X.shape
+        nnz, mode, binary = C.c_int64(), C.c_int32(), C.c_int32()
+        L.mph_features_info(h, C.byref(nnz), C.byref(mode), C.byref(binary))
+        self.nnz, self.mode, self.is_binary = nnz.value, mode.value, bool(binary.value)
+
+    def csr(self):
+        p, i, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        L.mph_features_csr(self.h, C.byref(p), C.byref(i), C.byref(v))
+        return (device_view(p.value, (self.N + 1,), torch.int64), device_view(i.value, (self.nnz,), torch.int32),
+                device_view(v.value, (self.nnz,), torch.float32))
+
+    def csc(self):
+        p, i, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        L.mph_features_csc(self.h, C.byref(p), C.byref(i), C.byref(v))
+        return (device_view(p.value, (self.F + 1,), torch.int64), device_view(i.value, (self.nnz,), torch.int32),
+                device_view(v.value, (self.nnz,), torch.float32))
+
+    def dense(self) -> torch.Tensor:
+        x, ld = C.c_void_p(), C.c_int32()
+        L.mph_features_dense(self.h, C.byref(x), C.byref(ld))
+        return device_view(x.value, (self.N, ld.value), torch.float32)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            L.mph_features_destroy(h)
+            self.h = None
+
+
+class Plan:
+    """D1-D4 host plan of one rank (mph_plan_create)."""
+
+    def __init__(self, row_ptr: np.ndarray, col_idx: np.ndarray, num_nodes: int, bounds: np.ndarray, rank: int):
+        self._rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self._ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        self._b = np.ascontiguousarray(bounds, dtype=np.int64)
+        self.world = len(self._b) - 1
+        self.rank = rank
+        h = _out_ptr()
+        L.mph_plan_create(self._rp.ctypes.data, self._ci.ctypes.data, int(num_nodes), self._b.ctypes.data,
+                          self.world, rank, C.byref(h))
+        self.h = h
+        n_own, row0, ng, nnz, ns = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        L.mph_plan_info(h, C.byref(n_own), C.byref(row0), C.byref(ng), C.byref(nnz), C.byref(ns))
+        self.n_own, self.row0, self.n_ghost, self.nnz, self.n_send = n_own.value, row0.value, ng.value, nnz.value, ns.value
+
+    def arrays(self) -> dict:
+        ptrs = [C.c_void_p() for _ in range(9)]
+        L.mph_plan_arrays(self.h, *[C.byref(p) for p in ptrs])
+        w = self.world
+
+        def arr(p, n, ct, dt):
+            if n == 0:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(C.cast(p, C.POINTER(ct)), shape=(n,)).copy()
+
+        return {
+            "ghosts": arr(ptrs[0].value, self.n_ghost, C.c_int64, np.int64),
+            "row_ptr": arr(ptrs[1].value, self.n_own + 1, C.c_int64, np.int64),
+            "col_idx": arr(ptrs[2].value, self.nnz, C.c_int32, np.int32),
+            "split": arr(ptrs[3].value, self.n_own, C.c_int64, np.int64),
+            "deg_local": arr(ptrs[4].value, self.n_own + self.n_ghost, C.c_int32, np.int32),
+            "recv_offset": arr(ptrs[5].value, w, C.c_int64, np.int64),
+            "n_recv": arr(ptrs[6].value, w, C.c_int64, np.int64),
+            "send_offset": arr(ptrs[7].value, w + 1, C.c_int64, np.int64),
+            "send_ids": arr(ptrs[8].value, self.n_send, C.c_int32, np.int32),
+        }
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            L.mph_plan_destroy(h)
+            self.h = None
+
+
+def partition_1d(row_ptr: np.ndarray, world: int) -> np.ndarray:
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    out = np.zeros(world + 1, dtype=np.int64)
+    L.mph_partition_1d(rp.ctypes.data, int(rp.size - 1), int(world), out.ctypes.data)
+    return out
+
+
+class Comm:
+    """NCCL communicator; the unique id travels over torch.distributed (plumbing only)."""
+
+    def __init__(self, world: int, rank: int, pg=None):
+        import torch.distributed as dist
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            L.mph_comm_unique_id(C.cast(buf, C.c_void_p))
+        t = torch.tensor(list(bytes(buf)), dtype=torch.uint8)
+        if dist.get_backend(pg) == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=0, group=pg)
+        ids = bytes(t.cpu().tolist())
+        C.memmove(buf, ids, 128)
+        h = _out_ptr()
+        L.mph_comm_create(C.cast(buf, C.c_void_p), world, rank, C.byref(h))
+        self.h = h
+        self.world, self.rank = world, rank
+
+    def allreduce_(self, t: torch.Tensor, stream=None):
+        L.mph_allreduce_sum(self.h, t.data_ptr(), t.numel(), int(t.dtype == torch.float64), stream_ptr(stream))
+        return t
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            L.mph_comm_destroy(h)
+            self.h = None
+
+
+class GCN:
+    """The L-layer GCN training step (initializeLayers / forwardPass / backPropagation / optimizer)."""
+
+    def __init__(self, graph: Graph, features: Features, dims, dropout_p: float = 0.0, dropout_seed: int = 0,
+                 order_policy: int = 0, comm: Comm | None = None, stream=None):
+        self.graph, self.features, self.comm = graph, features, comm
+        self.dims = tuple(int(d) for d in dims)
+        self.L = len(self.dims) - 1
+        arr = (C.c_int32 * len(self.dims))(*self.dims)
+        desc = GcnDesc(self.L, arr, float(dropout_p), int(dropout_seed), int(order_policy))
+        h = _out_ptr()
+        L.mph_gcn_create(graph.h, features.h, C.byref(desc), comm.h if comm is not None else None,
+                         stream_ptr(stream), C.byref(h))
+        self.h = h
+        n = C.c_int64()
+        offs = (C.c_int64 * (2 * self.L))()
+        lds = (C.c_int32 * self.L)()
+        L.mph_gcn_param_layout(h, C.byref(n), C.cast(offs, C.c_void_p), C.cast(lds, C.c_void_p))
+        self.num_params = n.value
+        self.offsets = list(offs)
+        self.ld_w = list(lds)
+        ptrs = [C.c_void_p() for _ in range(4)]
+        L.mph_gcn_buffers(h, *[C.byref(p) for p in ptrs])
+        self.params_flat, self.grads_flat, self.adam_m, self.adam_v = (
+            device_view(p.value, (self.num_params,), torch.float32) for p in ptrs)
+        order = (C.c_int32 * self.L)()
+        mode = C.c_int32()
+        L.mph_gcn_info(h, C.cast(order, C.c_void_p), C.byref(mode))
+        self.order = list(order)
+        self.loss_buf = torch.zeros(1, dtype=torch.float64, device="cuda")
+        self._labels = None
+
+    # -- parameter views ([F_in][F_out] weights, [F_out] biases; padding excluded)
+    def _views(self, flat):
+        out = []
+        for l in range(self.L):
+            fin, fout = self.dims[l], self.dims[l + 1]
+            ld = self.ld_w[l]
+            W = flat[self.offsets[2 * l]:self.offsets[2 * l] + fin * ld].view(fin, ld)[:, :fout]
+            b = flat[self.offsets[2 * l + 1]:self.offsets[2 * l + 1] + fout]
+            out.append((W, b))
+        return out
+
+    def params(self):
+        return self._views(self.params_flat)
+
+    def grads(self):
+        return self._views(self.grads_flat)
+
+    def init_xavier(self, seed: int = 42, stream=None):
+        L.mph_gcn_init_xavier(self.h, int(seed), stream_ptr(stream))
+
+    def params_updated(self, stream=None):
+        L.mph_gcn_params_updated(self.h, stream_ptr(stream))
+
+    def set_labels(self, labels: torch.Tensor, mask: torch.Tensor | None = None, n_lab_global: int | None = None):
+        assert labels.is_cuda and labels.dtype == torch.int32
+        if mask is not None:
+            assert mask.is_cuda and mask.dtype == torch.uint8
+        if n_lab_global is None:
+            n_lab_global = int(mask.sum().item()) if mask is not None else labels.numel()
+        self._labels = (labels, mask)  # keep alive
+        L.mph_gcn_set_labels(self.h, labels.data_ptr(), mask.data_ptr() if mask is not None else None,
+                             int(n_lab_global))
+
+    def forward(self, epoch: int = 1, stream=None):
+        L.mph_gcn_forward(self.h, int(epoch), stream_ptr(stream))
+
+    def loss(self, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        out = self.loss_buf if out is None else out
+        L.mph_gcn_loss(self.h, out.data_ptr(), stream_ptr(stream))
+        return out
+
+    def backward(self, stream=None):
+        L.mph_gcn_backward(self.h, stream_ptr(stream))
+
+    def adam(self, t: int, cfg=DEFAULT_ADAM, stream=None):
+        L.mph_gcn_adam(self.h, C.byref(AdamCfg(*cfg)), int(t), stream_ptr(stream))
+
+    def train_epoch(self, t: int, cfg=DEFAULT_ADAM, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        out = self.loss_buf if out is None else out
+        L.mph_gcn_train_epoch(self.h, int(t), C.byref(AdamCfg(*cfg)), out.data_ptr(), stream_ptr(stream))
+        return out
+
+    def tensor(self, kind: int, layer: int) -> torch.Tensor:
+        p, rows, width, ld = C.c_void_p(), C.c_int32(), C.c_int32(), C.c_int32()
+        L.mph_gcn_tensor(self.h, kind, layer, C.byref(p), C.byref(rows), C.byref(width), C.byref(ld))
+        if not p.value:
+            return None
+        return device_view(p.value, (rows.value, ld.value), torch.float32)[:, :width.value]
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            L.mph_gcn_destroy(h)
+            self.h = None

@@ -1,0 +1,123 @@
+// Shared device/host helpers for the Morphling B200 kernels (sm_100a only).
+// Nothing here is used by oracle/ (and nothing from oracle/ is used here).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/morphling.h"
+
+namespace mph {
+
+// ------------------------------------------------------------------ errors
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+
+#define MPH_CUDA_TRY(expr)                                                            \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess)                                                            \
+      return ::mph::fail(MPH_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,        \
+                         cudaGetErrorString(_e));                                     \
+  } while (0)
+
+#define MPH_TRY(expr)             \
+  do {                            \
+    int _rc = (expr);             \
+    if (_rc != MPH_OK) return _rc; \
+  } while (0)
+
+#define MPH_CHECK_ARG(cond, msg)                                 \
+  do {                                                           \
+    if (!(cond)) return ::mph::fail(MPH_EINVAL, "%s", (msg));    \
+  } while (0)
+
+inline int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MPH_ECUDA, "launch %s: %s", what, cudaGetErrorString(e));
+  return MPH_OK;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
+
+// Feature rows are padded to a multiple of 8 floats (one 32 B sector), or 4 when w <= 4
+// (SURVEY §8 "Per-config shapes"; padded columns are exactly zero, Q26).
+inline int pad_width(int w) { return w <= 4 ? 4 : round_up(w, 8); }
+
+// Device memory: plain cudaMalloc; the library owns what it allocates (include/morphling.h).
+template <class T>
+int dev_alloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return MPH_OK;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? MPH_ENOMEM : MPH_ECUDA, "cudaMalloc(%zu B): %s", count * sizeof(T),
+                cudaGetErrorString(e));
+  return MPH_OK;
+}
+inline void dev_free(void* p) {
+  if (p) cudaFree(p);
+}
+
+// Kernel launch counter (bench.py reports gpu_launches from it).
+void count_launch(int n = 1);
+
+// ------------------------------------------------------------------ device helpers
+#ifdef __CUDACC__
+__device__ __forceinline__ float4 ldg_f4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int ldg_stream_i32(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4_zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+// Philox4x32-10 (Salmon et al., SC'11) — the dropout mask of reading Q10.
+struct PhiloxOut {
+  uint32_t v[4];
+};
+__device__ __forceinline__ PhiloxOut philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                   uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  PhiloxOut o;
+  o.v[0] = c0;
+  o.v[1] = c1;
+  o.v[2] = c2;
+  o.v[3] = c3;
+  return o;
+}
+#endif
+
+// Dropout parameters carried into fused epilogues (Q10).
+struct Dropout {
+  uint32_t threshold;  // keep iff u32 >= threshold; 0 disables
+  float scale;         // 1/(1-p) in f32
+  uint32_t key0, key1;
+  uint32_t layer, epoch;
+};
+
+}  // namespace mph

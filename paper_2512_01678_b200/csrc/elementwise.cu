@@ -1,0 +1,346 @@
+// a5 loss, a9 Adam, Xavier init, weight transposes, and the sparse-feature kernels of the
+// density switch (a2 sparse X_csr·W, a7 sparse X_csc^T·G).
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace mph {
+
+// ------------------------------------------------------------------ a5 softmax cross-entropy
+// Reading Q9: max-subtracted log-sum-exp over the first C columns, mean over the
+// labelled rows (global count n_lab), dZ = (softmax - onehot)/n_lab.  Warp per row;
+// each block accumulates its rows' loss (double) and column sums of dZ in a fixed order and
+// writes one partial; a single-block pass reduces the partials in block order.
+constexpr int kCeThreads = 256;
+constexpr int kCeMaxC = 256;
+
+static int ce_grid(int N) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, 64), 592)); }
+
+__global__ void __launch_bounds__(kCeThreads) k_softmax_ce(const float* Z, int N, int C, int ld, const int32_t* labels,
+                                                           const uint8_t* mask, float inv_nlab, const float* row_scale,
+                                                           float* dZ, int ld_dz, double* part_loss, float* part_db) {
+  __shared__ double s_loss[kCeThreads / 32];
+  __shared__ float s_db[kCeThreads / 32][kCeMaxC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nj = (C + 31) / 32;
+  float dbacc[kCeMaxC / 32];
+#pragma unroll
+  for (int j = 0; j < kCeMaxC / 32; ++j) dbacc[j] = 0.0f;
+  double lacc = 0.0;
+  const int wpb = kCeThreads / 32;
+  for (int i = blockIdx.x * wpb + warp; i < N; i += gridDim.x * wpb) {
+    const float* z = Z + (int64_t)i * ld;
+    float* dz = dZ + (int64_t)i * ld_dz;
+    const bool lab = mask ? (mask[i] != 0) : true;
+    if (!lab) {
+      for (int c = lane; c < C; c += 32) dz[c] = 0.0f;
+      continue;
+    }
+    float zv[kCeMaxC / 32];
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kCeMaxC / 32; ++j) {
+      const int c = lane + 32 * j;
+      zv[j] = (j < nj && c < C) ? z[c] : -INFINITY;
+      m = fmaxf(m, zv[j]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float se = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kCeMaxC / 32; ++j)
+      if (j < nj && lane + 32 * j < C) se += expf(zv[j] - m);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const float lse = m + logf(se);
+    const int y = labels[i];
+    const float rs = row_scale ? row_scale[i] : 1.0f;
+    float zy = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kCeMaxC / 32; ++j) {
+      const int c = lane + 32 * j;
+      if (j < nj && c < C) {
+        if (c == y) zy = zv[j];
+        const float g = (expf(zv[j] - lse) - (c == y ? 1.0f : 0.0f)) * inv_nlab;
+        dbacc[j] += g;
+        dz[c] = g * rs;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) zy += __shfl_xor_sync(0xffffffffu, zy, o);
+    lacc += (double)lse - (double)zy;
+  }
+  if (lane == 0) s_loss[warp] = lacc;
+#pragma unroll
+  for (int j = 0; j < kCeMaxC / 32; ++j)
+    if (j < nj && lane + 32 * j < C) s_db[warp][lane + 32 * j] = dbacc[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < wpb; ++w) t += s_loss[w];
+    part_loss[blockIdx.x] = t;
+  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float t = 0.0f;
+    for (int w = 0; w < wpb; ++w) t += s_db[w][c];
+    part_db[(int64_t)blockIdx.x * C + c] = t;
+  }
+}
+
+__global__ void k_ce_finish(const double* part_loss, const float* part_db, int parts, int C, double inv_nlab,
+                            double* loss, float* db) {
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int b = 0; b < parts; ++b) t += part_loss[b];
+    *loss = t * inv_nlab;
+  }
+  if (db)
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      float t = 0.0f;
+      for (int b = 0; b < parts; ++b) t += part_db[(int64_t)b * C + c];
+      db[c] = t;
+    }
+}
+
+size_t softmax_ce_ws_bytes(int N, int C) {
+  const int g = ce_grid(std::max(N, 1));
+  return (size_t)g * sizeof(double) + (size_t)g * std::max(C, 1) * sizeof(float) + 16;
+}
+
+int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* labels, const uint8_t* mask, int64_t n_lab,
+                      const float* row_scale, float* dZ, int ld_dz, float* db, double* loss, void* ws, size_t ws_bytes,
+                      cudaStream_t s) {
+  if (!Z || !labels || !dZ || !loss || N < 0 || C <= 0 || ld < C || ld_dz < C || n_lab <= 0)
+    return fail(MPH_EINVAL, "softmax_ce: bad arguments");
+  if (C > kCeMaxC) return fail(MPH_ENOTSUP, "softmax_ce: C=%d > %d", C, kCeMaxC);
+  if (!ws || ws_bytes < softmax_ce_ws_bytes(N, C)) return fail(MPH_EINVAL, "softmax_ce: workspace too small");
+  const int g = ce_grid(std::max(N, 1));
+  double* part_loss = reinterpret_cast<double*>(ws);
+  float* part_db = reinterpret_cast<float*>(part_loss + g);
+  k_softmax_ce<<<g, kCeThreads, 0, s>>>(Z, N, C, ld, labels, mask, (float)(1.0 / (double)n_lab), row_scale, dZ, ld_dz,
+                                        part_loss, part_db);
+  k_ce_finish<<<1, 256, 0, s>>>(part_loss, part_db, g, C, 1.0 / (double)n_lab, loss, db);
+  count_launch(2);
+  return launch_check("softmax_ce");
+}
+
+// ------------------------------------------------------------------ a9 Adam
+__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
+                       int64_t n, float lr, float b1, float b2, float eps, float bc1, float bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+  }
+}
+
+int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s) {
+  if (!p || !g || !m || !v || !cfg || n < 0 || t < 1) return fail(MPH_EINVAL, "adam: bad arguments");
+  if (n == 0) return MPH_OK;
+  const float bc1 = (float)(1.0 - pow((double)cfg->beta1, (double)t));
+  const float bc2 = (float)(1.0 - pow((double)cfg->beta2, (double)t));
+  k_adam<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(p, g, m, v, n, cfg->lr, cfg->beta1,
+                                                                                 cfg->beta2, cfg->eps, bc1, bc2);
+  count_launch();
+  return launch_check("adam");
+}
+
+// ------------------------------------------------------------------ Xavier (Q16)
+__global__ void k_xavier(float* W, int f_in, int f_out, int ld, uint64_t seed_l, double a) {
+  const int64_t total = (int64_t)f_in * f_out;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed_l + (uint64_t)(k + 1) * 0x9E3779B97F4A7C15ull;  // k-th splitmix64 state
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    const double u24 = (double)(z >> 40);
+    const double t = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, u24), 16777216.0), -1.0);
+    const int64_t i = k / f_out, j = k - i * f_out;
+    W[i * ld + j] = __double2float_rn(__dmul_rn(a, t));
+  }
+}
+
+int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int layer, cudaStream_t s) {
+  if (!W || f_in <= 0 || f_out <= 0 || ld < f_out || layer < 1) return fail(MPH_EINVAL, "xavier: bad arguments");
+  const uint64_t seed_l = seed ^ ((uint64_t)layer * 0x9E3779B97F4A7C15ull);
+  const double a = std::sqrt(6.0 / (double)(f_in + f_out));
+  const int64_t total = (int64_t)f_in * f_out;
+  k_xavier<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0, s>>>(W, f_in, f_out, ld, seed_l, a);
+  count_launch();
+  return launch_check("xavier");
+}
+
+// ------------------------------------------------------------------ transposes / row scale
+__global__ void k_transpose(const float* src, int rows, int cols, int ld_src, float* dst, int ld_dst) {
+  __shared__ float tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[(int64_t)r * ld_src + c] : 0.0f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) dst[(int64_t)c * ld_dst + r] = tile[threadIdx.x][i];
+  }
+}
+
+int transpose_launch(const float* src, int rows, int cols, int ld_src, float* dst, int ld_dst, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return MPH_OK;
+  dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+  k_transpose<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld_src, dst, ld_dst);
+  count_launch();
+  return launch_check("transpose");
+}
+
+__global__ void k_rowscale(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out) {
+  const int64_t total = (int64_t)rows * w;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / w;
+    const int c = (int)(t - i * w);
+    out[i * ld_out + c] = in[i * ld_in + c] * scale[i];
+  }
+}
+
+int rowscale_launch(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out,
+                    cudaStream_t s) {
+  if (rows <= 0 || w <= 0) return MPH_OK;
+  const int64_t total = (int64_t)rows * w;
+  k_rowscale<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 32), 256, 0, s>>>(in, ld_in, scale, rows, w,
+                                                                                          out, ld_out);
+  count_launch();
+  return launch_check("rowscale");
+}
+
+// ------------------------------------------------------------------ sparse-feature path
+// a2 (Alg. 1 Forward SpMM_Tiled(X_csr, W); CPU original keeps W blocks in L1,
+// P:228): warp per row of X; the row's nonzeros are read 32 at a time and broadcast; lanes
+// cover the output columns; W rows are re-read from L1/L2 (W is at most 128 KB here).
+__global__ void k_sparse_xw(const int64_t* ptr, const int32_t* idx, const float* val, int N, const float* W, int F_out,
+                            int ldw, const float* row_scale, float* T, int ldt) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nwarps) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    const int64_t s = ptr[i], e = ptr[i + 1];
+    for (int64_t b = s; b < e; b += 32) {
+      const int nb = (int)min((int64_t)32, e - b);
+      const int kk = lane < nb ? idx[b + lane] : 0;
+      const float xx = lane < nb ? val[b + lane] : 0.0f;
+      for (int t = 0; t < nb; ++t) {
+        const int k = __shfl_sync(0xffffffffu, kk, t);
+        const float x = __shfl_sync(0xffffffffu, xx, t);
+        const float* wr = W + (int64_t)k * ldw;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = lane + 32 * j;
+          if (c < F_out) acc[j] = fmaf(x, __ldg(wr + c), acc[j]);
+        }
+      }
+    }
+    const float rs = row_scale ? row_scale[i] : 1.0f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = lane + 32 * j;
+      if (c < F_out) T[(int64_t)i * ldt + c] = acc[j] * rs;
+    }
+  }
+}
+
+// a7 (Alg. 1 Backward SpMM_Col(X_csc, G); thread-local accumulation without
+// atomics P:229): warp per feature column k, gathering the G rows of its nonzeros.
+__global__ void k_sparse_xtg(const int64_t* cptr, const int32_t* ridx, const float* cval, int F, const float* G,
+                             int F_out, int ldg, float* dW, int lddw) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < F; k += nwarps) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
+    const int64_t s = cptr[k], e = cptr[k + 1];
+    for (int64_t b = s; b < e; b += 32) {
+      const int nb = (int)min((int64_t)32, e - b);
+      const int ii = lane < nb ? ridx[b + lane] : 0;
+      const float xx = lane < nb ? cval[b + lane] : 0.0f;
+      for (int t = 0; t < nb; ++t) {
+        const int i = __shfl_sync(0xffffffffu, ii, t);
+        const float x = __shfl_sync(0xffffffffu, xx, t);
+        const float* gr = G + (int64_t)i * ldg;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int c = lane + 32 * j;
+          if (c < F_out) acc[j] = fmaf(x, __ldg(gr + c), acc[j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int c = lane + 32 * j;
+      if (c < F_out) dW[(int64_t)k * lddw + c] = acc[j];
+    }
+  }
+}
+
+int sparse_xw_launch(const mph_features* f, const float* W, int F_out, int ldw, const float* row_scale, float* T,
+                     int ldt, cudaStream_t s) {
+  if (!f || !W || !T || F_out <= 0 || ldw < F_out || ldt < F_out) return fail(MPH_EINVAL, "sparse_xw: bad arguments");
+  if (f->mode != 1) return fail(MPH_ESTATE, "sparse_xw: features are in dense mode");
+  if (F_out > 256) return fail(MPH_ENOTSUP, "sparse_xw: F_out > 256");
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(f->N, 8), 148 * 16));
+  k_sparse_xw<<<grid, 256, 0, s>>>(f->csr_ptr, f->csr_idx, f->csr_val, f->N, W, F_out, ldw, row_scale, T, ldt);
+  count_launch();
+  return launch_check("sparse_xw");
+}
+
+int sparse_xtg_launch(const mph_features* f, const float* G, int F_out, int ldg, float* dW, int lddw, cudaStream_t s) {
+  if (!f || !G || !dW || F_out <= 0 || ldg < F_out || lddw < F_out) return fail(MPH_EINVAL, "sparse_xtg: bad arguments");
+  if (f->mode != 1) return fail(MPH_ESTATE, "sparse_xtg: features are in dense mode");
+  if (F_out > 256) return fail(MPH_ENOTSUP, "sparse_xtg: F_out > 256");
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(f->F, 8));
+  k_sparse_xtg<<<grid, 256, 0, s>>>(f->csc_ptr, f->csc_idx, f->csc_val, f->F, G, F_out, ldg, dW, lddw);
+  count_launch();
+  return launch_check("sparse_xtg");
+}
+
+}  // namespace mph
+
+using namespace mph;
+
+extern "C" int mph_softmax_ce_workspace(int32_t N, int32_t C, size_t* bytes_h) {
+  if (!bytes_h) return fail(MPH_EINVAL, "null bytes");
+  *bytes_h = softmax_ce_ws_bytes(N, C);
+  return MPH_OK;
+}
+
+extern "C" int mph_softmax_ce(const float* Z_d, int32_t N, int32_t C, int32_t ld, const int32_t* labels_d,
+                              const uint8_t* mask_d, int64_t n_lab, const float* row_scale_d, float* dZ_d, int32_t ld_dz,
+                              float* db_d, double* loss_d, void* ws_d, size_t ws_bytes, void* stream) {
+  return softmax_ce_launch(Z_d, N, C, ld, labels_d, mask_d, n_lab, row_scale_d, dZ_d, ld_dz, db_d, loss_d, ws_d,
+                           ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int mph_adam(float* params_d, const float* grads_d, float* m_d, float* v_d, int64_t n, const mph_adam_cfg* cfg,
+                        int32_t t, void* stream) {
+  return adam_launch(params_d, grads_d, m_d, v_d, n, cfg, t, (cudaStream_t)stream);
+}
+
+extern "C" int mph_xavier_fill(float* W_d, int32_t f_in, int32_t f_out, int32_t ld, uint64_t seed, int32_t layer,
+                               void* stream) {
+  return xavier_launch(W_d, f_in, f_out, ld, seed, layer, (cudaStream_t)stream);
+}
+
+extern "C" int mph_sparse_xw(const mph_features* f, const float* W_d, int32_t F_out, int32_t ldw,
+                             const float* row_scale_d, float* T_d, int32_t ldt, void* stream) {
+  return sparse_xw_launch(f, W_d, F_out, ldw, row_scale_d, T_d, ldt, (cudaStream_t)stream);
+}
+
+extern "C" int mph_sparse_xtg(const mph_features* f, const float* G_d, int32_t F_out, int32_t ldg, float* dW_d,
+                              int32_t lddw, void* stream) {
+  return sparse_xtg_launch(f, G_d, F_out, ldg, dW_d, lddw, (cudaStream_t)stream);
+}

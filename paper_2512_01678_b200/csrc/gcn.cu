@@ -1,0 +1,483 @@
+// The L-layer GCN training step (Listing 1; layer update P:92 with readings Q1, Q6,
+// Q7, Q8; loss Q9; Adam P:170/P:534-535).  This file only orders kernel launches and owns the
+// buffers; every arithmetic step runs in the kernels of spmm.cu / gemm.cu / elementwise.cu.
+//
+// Data layout in HBM (row-major fp32, widths padded to pad_width(F), padding exactly zero):
+//   params  [W_1 (P_0 x P_1) | b_1 (P_1) | ... ]   flat, one Adam launch
+//   wt      [W_1^T (P_1 x P_0) | ...]              K-major B operands of the forward GEMMs
+//   T_l     n_cols x P_l   dinv-prescaled transform output incl. ghost rows (halo target)
+//   out_l   n_rows x P_l   H_l = ReLU(Z_l) (hidden, saved for backward) or logits Z_L
+//   dZ_l    n_cols x P_l   dinv-prescaled loss/input gradient (halo target)
+//   G_l     n_rows x P_l   backward aggregation Â·dZ_l
+//   Y_1     n_rows x P_0   aggregate-first input Â·X (only when layer 1 is AF)
+#include <vector>
+
+#include "internal.cuh"
+#include "profile.cuh"
+
+struct mph_comm;
+extern "C" int mph_halo_exchange(const mph_graph* gc, mph_comm* c, float* buf_d, int32_t w, int32_t ld, void* stream);
+extern "C" int mph_allreduce_sum(mph_comm* c, void* buf_d, int64_t n, int32_t is_double, void* stream);
+extern "C" int mph_comm_info(const mph_comm* c, int32_t* world_h, int32_t* rank_h);
+
+namespace {
+
+struct Layer {
+  int fin = 0, fout = 0, pin = 0, pout = 0;
+  int order = 0;  // 0 transform-first, 1 aggregate-first
+  int64_t off_w = 0, off_b = 0, off_wt = 0;
+  float* T = nullptr;
+  float* out = nullptr;
+  float* dZ = nullptr;
+  float* G = nullptr;
+  float* Y = nullptr;
+  float* colsum = nullptr;
+};
+
+}  // namespace
+
+struct mph_gcn {
+  const mph_graph* g = nullptr;
+  const mph_features* f = nullptr;
+  mph_comm* comm = nullptr;
+  int world = 1;
+  int L = 0;
+  std::vector<Layer> layers;
+  float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *wt = nullptr;
+  int64_t n_params = 0, n_wt = 0;
+  const int32_t* labels = nullptr;
+  const uint8_t* mask = nullptr;
+  int64_t n_lab = 0;
+  float* Xs = nullptr;  // dinv ⊙ X with ghost rows (AF layer 1)
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  float dropout_p = 0.0f;
+  uint64_t dropout_seed = 0;
+  int epoch = 0;
+  bool fwd_done = false, loss_done = false;
+};
+
+namespace mph {
+
+static int64_t align16(int64_t x) { return (x + 15) / 16 * 16; }
+
+static void gcn_free(mph_gcn* m) {
+  if (!m) return;
+  for (auto& l : m->layers) {
+    dev_free(l.T);
+    dev_free(l.out);
+    dev_free(l.dZ);
+    dev_free(l.G);
+    dev_free(l.Y);
+    dev_free(l.colsum);
+  }
+  dev_free(m->params);
+  dev_free(m->grads);
+  dev_free(m->m);
+  dev_free(m->v);
+  dev_free(m->wt);
+  dev_free(m->Xs);
+  dev_free(m->ws);
+  delete m;
+}
+
+static int refresh_wt(mph_gcn* m, cudaStream_t s) {
+  for (auto& l : m->layers)
+    MPH_TRY(transpose_launch(m->params + l.off_w, l.pin, l.pout, l.pout, m->wt + l.off_wt, l.pin, s));
+  return MPH_OK;
+}
+
+// SURVEY §8(d) d.3 algorithmic bytes: per edge 4 B col_idx + 4·w B gathered row (no reuse),
+// per row 8 B row_ptr + 4 B dinv + 4·w B written.
+static int spmm_p(const mph_graph* g, const float* in, int w, int ld_in, float* out, int ld_out, const mph_epilogue* e,
+                  cudaStream_t s) {
+  const double rows = g->n_rows, nnz = (double)g->nnz;
+  prof::Scope sc(MPH_PROF_SPMM, s, 8.0 * (rows + 1) + 4.0 * nnz + 4.0 * rows + 4.0 * nnz * w + 4.0 * rows * w,
+                 2.0 * nnz * w);
+  return spmm_launch(g, -1, in, w, ld_in, out, ld_out, e, s);
+}
+static int gemm_nt_p(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
+                     const mph_epilogue* e, cudaStream_t s) {
+  double extra = (e && (e->flags & MPH_EPI_MASK)) ? 4.0 * M * N : 0.0;
+  prof::Scope sc(MPH_PROF_GEMM_NT, s, 4.0 * ((double)M * K + (double)N * K + (double)M * N) + extra,
+                 2.0 * M * N * K);
+  return gemm_nt_launch(M, N, K, A, lda, Bt, ldb, C, ldc, e, s);
+}
+static int gemm_tn_p(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+                     void* ws, size_t wsb, cudaStream_t s) {
+  prof::Scope sc(MPH_PROF_GEMM_TN, s, 4.0 * ((double)K * M + (double)K * N + (double)M * N), 2.0 * M * N * K);
+  return gemm_tn_launch(M, N, K, A, lda, B, ldb, C, ldc, ws, wsb, s);
+}
+
+static mph_epilogue epi_none() {
+  mph_epilogue e{};
+  e.mask_scale = 1.0f;
+  return e;
+}
+
+static float dropout_scale(float p) { return p > 0.0f ? (float)(1.0 / (1.0 - (double)p)) : 1.0f; }
+
+static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
+  Layer& l = m->layers[li];
+  const mph_graph* g = m->g;
+  const int lnum = li + 1;
+  const bool hidden = lnum < m->L;
+  mph_epilogue eo = epi_none();
+  eo.flags = MPH_EPI_BIAS | (hidden ? MPH_EPI_RELU : 0u);
+  eo.bias = m->params + l.off_b;
+  if (hidden && m->dropout_p > 0.0f) {
+    eo.flags |= MPH_EPI_DROPOUT;
+    eo.dropout_p = m->dropout_p;
+    eo.dropout_seed = m->dropout_seed;
+    eo.dropout_layer = lnum;
+    eo.dropout_epoch = m->epoch;
+    eo.row0 = g->row0;
+  }
+  if (l.order == 0) {
+    // a2/a4: T' = dinv ⊙ (H_{l-1} · W_l)
+    if (li == 0 && m->f->mode == 1) {
+      prof::Scope sc(MPH_PROF_SPARSE, s, 8.0 * m->f->nnz + 4.0 * g->n_rows * l.pout, 2.0 * m->f->nnz * l.pout);
+      MPH_TRY(sparse_xw_launch(m->f, m->params + l.off_w, l.pout, l.pout, g->dinv, l.T, l.pout, s));
+    } else {
+      const float* A = li == 0 ? m->f->X : m->layers[li - 1].out;
+      const int lda = li == 0 ? m->f->P : m->layers[li - 1].pout;
+      mph_epilogue et = epi_none();
+      et.flags = MPH_EPI_ROWSCALE;
+      et.row_scale = g->dinv;
+      MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, A, lda, m->wt + l.off_wt, l.pin, l.T, l.pout, &et, s));
+    }
+    // a10: ghost rows of T' from their owners
+    if (m->world > 1) MPH_TRY(mph_halo_exchange(g, m->comm, l.T, l.pout, l.pout, s));
+    // a3: Z = Â·T + b, ReLU (dropout) fused
+    MPH_TRY(spmm_p(g, l.T, l.pout, l.pout, l.out, l.pout, &eo, s));
+  } else {
+    // aggregate-first layer 1: Y = Â·X (on dinv ⊙ X), Z = Y·W + b with the epilogue fused in the GEMM
+    mph_epilogue en = epi_none();
+    MPH_TRY(spmm_p(g, m->Xs, l.pin, l.pin, l.Y, l.pin, &en, s));
+    MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, l.Y, l.pin, m->wt + l.off_wt, l.pin, l.out, l.pout, &eo, s));
+  }
+  return MPH_OK;
+}
+
+static int do_forward(mph_gcn* m, int epoch, cudaStream_t s) {
+  m->epoch = epoch;
+  for (int li = 0; li < m->L; ++li) MPH_TRY(layer_forward(m, li, s));
+  m->fwd_done = true;
+  m->loss_done = false;
+  return MPH_OK;
+}
+
+static int do_loss(mph_gcn* m, double* loss_d, cudaStream_t s) {
+  if (!m->fwd_done) return fail(MPH_ESTATE, "loss before forward (S:353)");
+  if (!m->labels) return fail(MPH_ESTATE, "labels not set");
+  Layer& l = m->layers[m->L - 1];
+  prof::Scope sc(MPH_PROF_LOSS, s, 8.0 * m->g->n_rows * l.pout + 4.0 * m->g->n_rows, 0.0);
+  MPH_TRY(softmax_ce_launch(l.out, m->g->n_rows, l.fout, l.pout, m->labels, m->mask, m->n_lab,
+                            l.order == 0 ? m->g->dinv : nullptr, l.dZ, l.pout, m->grads + l.off_b, loss_d, m->ws,
+                            m->ws_bytes, s));
+  m->loss_done = true;
+  return MPH_OK;
+}
+
+static int do_backward(mph_gcn* m, cudaStream_t s) {
+  if (!m->loss_done) return fail(MPH_ESTATE, "backward without a matching forward+loss (S:353)");
+  const mph_graph* g = m->g;
+  for (int li = m->L - 1; li >= 0; --li) {
+    Layer& l = m->layers[li];
+    const float* Hin = li == 0 ? (m->f->mode == 0 ? m->f->X : nullptr) : m->layers[li - 1].out;
+    const int ld_in = li == 0 ? m->f->P : m->layers[li - 1].pout;
+    const float* Gsrc;  // gradient w.r.t. the transform output (TF) or Z (AF)
+    if (l.order == 0) {
+      // a6: G = Â·dZ (Â symmetric, same kernel as forward)
+      if (m->world > 1) MPH_TRY(mph_halo_exchange(g, m->comm, l.dZ, l.pout, l.pout, s));
+      mph_epilogue en = epi_none();
+      MPH_TRY(spmm_p(g, l.dZ, l.pout, l.pout, l.G, l.pout, &en, s));
+      Gsrc = l.G;
+      // a7: dW = H^T·G  (sparse layer 1: X_csc^T·G)
+      if (li == 0 && m->f->mode == 1) {
+        prof::Scope sc(MPH_PROF_SPARSE, s, 8.0 * m->f->nnz + 4.0 * m->f->nnz * l.pout, 2.0 * m->f->nnz * l.pout);
+        MPH_TRY(sparse_xtg_launch(m->f, l.G, l.pout, l.pout, m->grads + l.off_w, l.pout, s));
+      } else {
+        MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, Hin, ld_in, l.G, l.pout, m->grads + l.off_w, l.pout, m->ws,
+                          m->ws_bytes, s));
+      }
+    } else {
+      // AF layer 1: dZ_1 (unscaled) is the gradient of Z = Y·W + b
+      Gsrc = l.dZ;
+      MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, l.Y, l.pin, l.dZ, l.pout, m->grads + l.off_w, l.pout, m->ws,
+                        m->ws_bytes, s));
+    }
+    if (li > 0) {
+      // a8: dZ_{l-1} = (G·W^T) ⊙ 1[H_{l-1} > 0] (/(1-p)), db_{l-1} as column sums, then the dinv
+      // pre-scale for the next backward SpMM (TF) — all in one GEMM epilogue.
+      Layer& pl = m->layers[li - 1];
+      mph_epilogue ed = epi_none();
+      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM | (pl.order == 0 ? MPH_EPI_ROWSCALE : 0u);
+      ed.mask_src = pl.out;
+      ed.ld_mask = pl.pout;
+      ed.mask_scale = dropout_scale(m->dropout_p);
+      ed.colsum_out = pl.colsum;
+      ed.row_scale = g->dinv;
+      MPH_TRY(gemm_nt_p(g->n_rows, pl.pout, l.pout, Gsrc, l.pout, m->params + l.off_w, l.pout, pl.dZ, pl.pout, &ed,
+                        s));
+      MPH_TRY(reduce_rows_launch(pl.colsum, (int)ceil_div(g->n_rows, 128), pl.pout, pl.pout, m->grads + pl.off_b, 0, s));
+    }
+  }
+  m->fwd_done = false;
+  m->loss_done = false;
+  return MPH_OK;
+}
+
+}  // namespace mph
+
+using namespace mph;
+
+extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const mph_gcn_desc* desc, mph_comm* comm,
+                              void* stream, mph_gcn** out) {
+  if (!g || !f || !desc || !out || !desc->dims_h || desc->num_layers < 1) return fail(MPH_EINVAL, "gcn_create arguments");
+  *out = nullptr;
+  if (f->N != g->n_rows) return fail(MPH_EINVAL, "features rows (%d) != graph rows (%d)", f->N, g->n_rows);
+  if (desc->dims_h[0] != f->F) return fail(MPH_EINVAL, "dims[0]=%d != feature width %d", desc->dims_h[0], f->F);
+  if (desc->dropout_p < 0.0f || desc->dropout_p >= 1.0f) return fail(MPH_EINVAL, "dropout_p must be in [0,1)");
+  int world = 1;
+  if (comm) MPH_TRY(mph_comm_info(comm, &world, nullptr));
+  if (world > 1 && !g->local) return fail(MPH_EINVAL, "distributed model needs a localized graph");
+  for (int i = 0; i <= desc->num_layers; ++i)
+    if (desc->dims_h[i] <= 0 || pad_width(desc->dims_h[i]) > 256 + (i == 0 ? 1 << 20 : 0))
+      return fail(MPH_ENOTSUP, "layer width %d outside (0, 256]", desc->dims_h[i]);
+  cudaStream_t s = (cudaStream_t)stream;
+  mph_gcn* m = new mph_gcn();
+  m->g = g;
+  m->f = f;
+  m->comm = comm;
+  m->world = world;
+  m->L = desc->num_layers;
+  m->dropout_p = desc->dropout_p;
+  m->dropout_seed = desc->dropout_seed;
+  m->layers.resize(m->L);
+  int64_t off = 0, offt = 0;
+  for (int li = 0; li < m->L; ++li) {
+    Layer& l = m->layers[li];
+    l.fin = desc->dims_h[li];
+    l.fout = desc->dims_h[li + 1];
+    l.pin = li == 0 ? (f->mode == 0 ? f->P : pad_width(f->F)) : pad_width(l.fin);
+    l.pout = pad_width(l.fout);
+    // reading Q7: TF iff F_out <= F_in, or layer 1 in Sparse mode; AF only ever needed on layer 1
+    l.order = (desc->order_policy == 1 || l.fout <= l.fin || (li == 0 && f->mode == 1) || li > 0) ? 0 : 1;
+    l.off_w = off;
+    off = align16(off + (int64_t)l.pin * l.pout);
+    l.off_b = off;
+    off = align16(off + l.pout);
+    l.off_wt = offt;
+    offt = align16(offt + (int64_t)l.pout * l.pin);
+  }
+  m->n_params = off;
+  m->n_wt = offt;
+  int rc = MPH_OK;
+  auto bail = [&](int code) {
+    gcn_free(m);
+    return code;
+  };
+  if ((rc = dev_alloc(&m->params, off)) || (rc = dev_alloc(&m->grads, off)) || (rc = dev_alloc(&m->m, off)) ||
+      (rc = dev_alloc(&m->v, off)) || (rc = dev_alloc(&m->wt, offt)))
+    return bail(rc);
+  size_t ws = softmax_ce_ws_bytes(g->n_rows, m->layers.back().fout);
+  const int64_t nr = g->n_rows, nc = g->n_cols;
+  for (int li = 0; li < m->L; ++li) {
+    Layer& l = m->layers[li];
+    if ((rc = dev_alloc(&l.out, (size_t)nr * l.pout))) return bail(rc);
+    if ((rc = dev_alloc(&l.dZ, (size_t)(l.order == 0 ? nc : nr) * l.pout))) return bail(rc);
+    if ((rc = dev_alloc(&l.colsum, (size_t)ceil_div(nr, 128) * l.pout))) return bail(rc);
+    if (l.order == 0) {
+      if ((rc = dev_alloc(&l.T, (size_t)nc * l.pout))) return bail(rc);
+      if ((rc = dev_alloc(&l.G, (size_t)nr * l.pout))) return bail(rc);
+    } else {
+      if ((rc = dev_alloc(&l.Y, (size_t)nr * l.pin))) return bail(rc);
+    }
+    if (!(li == 0 && f->mode == 1)) ws = std::max(ws, gemm_tn_ws_bytes(l.pin, l.pout, (int)nr));
+  }
+  m->ws_bytes = ws;
+  if ((rc = dev_alloc((char**)&m->ws, ws))) return bail(rc);
+  cudaError_t e = cudaSuccess;
+  for (auto& l : m->layers) {  // padding columns must start (and stay) zero
+    if (e == cudaSuccess) e = cudaMemsetAsync(l.out, 0, (size_t)nr * l.pout * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(l.dZ, 0, (size_t)(l.order == 0 ? nc : nr) * l.pout * 4, s);
+    if (e == cudaSuccess && l.T) e = cudaMemsetAsync(l.T, 0, (size_t)nc * l.pout * 4, s);
+    if (e == cudaSuccess && l.G) e = cudaMemsetAsync(l.G, 0, (size_t)nr * l.pout * 4, s);
+    if (e == cudaSuccess && l.Y) e = cudaMemsetAsync(l.Y, 0, (size_t)nr * l.pin * 4, s);
+  }
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->params, 0, off * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->grads, 0, off * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->m, 0, off * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->v, 0, off * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->wt, 0, offt * 4, s);
+  if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create memset: %s", cudaGetErrorString(e)));
+  if (m->layers[0].order == 1) {
+    // X is constant input data: its dinv pre-scale (and, distributed, its ghost rows) are set up once.
+    const Layer& l = m->layers[0];
+    if ((rc = dev_alloc(&m->Xs, (size_t)nc * l.pin))) return bail(rc);
+    e = cudaMemsetAsync(m->Xs, 0, (size_t)nc * l.pin * 4, s);
+    if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "memset: %s", cudaGetErrorString(e)));
+    if ((rc = rowscale_launch(f->X, f->P, g->dinv, (int)nr, l.pin, m->Xs, l.pin, s))) return bail(rc);
+    if (world > 1 && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
+  }
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create: %s", cudaGetErrorString(e)));
+  *out = m;
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_param_layout(const mph_gcn* m, int64_t* num_params_h, int64_t* offsets_h, int32_t* ld_w_h) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  if (num_params_h) *num_params_h = m->n_params;
+  for (int li = 0; li < m->L; ++li) {
+    if (offsets_h) {
+      offsets_h[2 * li] = m->layers[li].off_w;
+      offsets_h[2 * li + 1] = m->layers[li].off_b;
+    }
+    if (ld_w_h) ld_w_h[li] = m->layers[li].pout;
+  }
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_buffers(const mph_gcn* m, float** params_d, float** grads_d, float** adam_m_d, float** adam_v_d) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  if (params_d) *params_d = m->params;
+  if (grads_d) *grads_d = m->grads;
+  if (adam_m_d) *adam_m_d = m->m;
+  if (adam_v_d) *adam_v_d = m->v;
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_init_xavier(mph_gcn* m, uint64_t seed, void* stream) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  cudaStream_t s = (cudaStream_t)stream;
+  MPH_CUDA_TRY(cudaMemsetAsync(m->params, 0, m->n_params * 4, s));
+  MPH_CUDA_TRY(cudaMemsetAsync(m->m, 0, m->n_params * 4, s));
+  MPH_CUDA_TRY(cudaMemsetAsync(m->v, 0, m->n_params * 4, s));
+  for (int li = 0; li < m->L; ++li) {
+    const Layer& l = m->layers[li];
+    MPH_TRY(xavier_launch(m->params + l.off_w, l.fin, l.fout, l.pout, seed, li + 1, s));
+  }
+  return refresh_wt(m, s);
+}
+
+extern "C" int mph_gcn_params_updated(mph_gcn* m, void* stream) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  return refresh_wt(m, (cudaStream_t)stream);
+}
+
+extern "C" int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_h, void* stream) {
+  if (!m || !X_h || ld_h < m->f->F) return fail(MPH_EINVAL, "upload_features arguments");
+  if (m->f->mode != 0) return fail(MPH_ENOTSUP, "upload_features: sparse-mode features are fixed at creation");
+  cudaStream_t s = (cudaStream_t)stream;
+  const mph_features* f = m->f;
+  MPH_CUDA_TRY(cudaMemcpy2DAsync(f->X, (size_t)f->P * 4, X_h, (size_t)ld_h * 4, (size_t)f->F * 4, (size_t)f->N,
+                                 cudaMemcpyHostToDevice, s));
+  if (m->layers[0].order == 1) {
+    const Layer& l = m->layers[0];
+    MPH_TRY(rowscale_launch(f->X, f->P, m->g->dinv, m->g->n_rows, l.pin, m->Xs, l.pin, s));
+    if (m->world > 1) MPH_TRY(mph_halo_exchange(m->g, m->comm, m->Xs, l.pin, l.pin, s));
+  }
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_set_labels(mph_gcn* m, const int32_t* labels_d, const uint8_t* mask_d, int64_t n_lab_global) {
+  if (!m || !labels_d || n_lab_global <= 0) return fail(MPH_EINVAL, "set_labels arguments");
+  m->labels = labels_d;
+  m->mask = mask_d;
+  m->n_lab = n_lab_global;
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_forward(mph_gcn* m, int32_t epoch, void* stream) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  return do_forward(m, epoch, (cudaStream_t)stream);
+}
+
+extern "C" int mph_gcn_loss(mph_gcn* m, double* loss_d, void* stream) {
+  if (!m || !loss_d) return fail(MPH_EINVAL, "gcn_loss arguments");
+  MPH_TRY(do_loss(m, loss_d, (cudaStream_t)stream));
+  if (m->world > 1) MPH_TRY(mph_allreduce_sum(m->comm, loss_d, 1, 1, stream));
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_backward(mph_gcn* m, void* stream) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  MPH_TRY(do_backward(m, (cudaStream_t)stream));
+  // a11: replicated parameters need the summed gradient
+  if (m->world > 1) MPH_TRY(mph_allreduce_sum(m->comm, m->grads, m->n_params, 0, stream));
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream) {
+  if (!m || !cfg) return fail(MPH_EINVAL, "gcn_adam arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  prof::Scope sc(MPH_PROF_ADAM, s, 28.0 * m->n_params, 0.0);
+  MPH_TRY(adam_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s));
+  return refresh_wt(m, s);
+}
+
+extern "C" int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* loss_d, void* stream) {
+  if (!m || !cfg || !loss_d || t < 1) return fail(MPH_EINVAL, "train_epoch arguments");
+  MPH_TRY(mph_gcn_forward(m, t, stream));
+  MPH_TRY(mph_gcn_loss(m, loss_d, stream));
+  MPH_TRY(mph_gcn_backward(m, stream));
+  return mph_gcn_adam(m, cfg, t, stream);
+}
+
+extern "C" int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, const float** ptr_d, int32_t* rows_h,
+                              int32_t* width_h, int32_t* ld_h) {
+  if (!m || layer < 1 || layer > m->L) return fail(MPH_EINVAL, "gcn_tensor arguments");
+  const Layer& l = m->layers[layer - 1];
+  const float* p = nullptr;
+  int rows = m->g->n_rows, width = 0, ld = 0;
+  switch (kind) {
+    case 0:
+      if (layer == 1) {
+        p = m->f->mode == 0 ? m->f->X : nullptr;
+        width = m->f->F;
+        ld = m->f->P;
+      } else {
+        p = m->layers[layer - 2].out;
+        width = l.fin;
+        ld = l.pin;
+      }
+      break;
+    case 1:
+      p = l.out;
+      width = l.fout;
+      ld = l.pout;
+      break;
+    case 2:
+      p = l.order == 0 ? l.G : l.dZ;
+      width = l.fout;
+      ld = l.pout;
+      break;
+    case 3:
+      p = l.Y;
+      width = l.fin;
+      ld = l.pin;
+      break;
+    default:
+      return fail(MPH_EINVAL, "unknown tensor kind %d", kind);
+  }
+  if (ptr_d) *ptr_d = p;
+  if (rows_h) *rows_h = rows;
+  if (width_h) *width_h = width;
+  if (ld_h) *ld_h = ld;
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_info(const mph_gcn* m, int32_t* order_h, int32_t* mode_h) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  if (order_h)
+    for (int li = 0; li < m->L; ++li) order_h[li] = m->layers[li].order;
+  if (mode_h) *mode_h = m->f->mode;
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_destroy(mph_gcn* m) {
+  gcn_free(m);
+  return MPH_OK;
+}

@@ -1,0 +1,500 @@
+// a2/a4/a7/a8 — dense transforms on 5th-gen tensor cores (tcgen05, TF32 in, FP32 accumulate
+// in TMEM), TMA-fed through a multi-stage mbarrier pipeline ("dense, regular";
+// P:221 vendor GEMM replaced by hand-written sm_100a kernels).
+//
+//   k_gemm_nt : C[M,N] = epi(A[M,K] · Bt[N,K]^T)   both operands K-major (activations x weights)
+//               one CTA per 128-row stripe and the whole N <= 256 width, so A streams from HBM
+//               exactly once; warp 0 = TMA producer, warp 1 = MMA issuer (one thread) and
+//               TMEM owner, warps 2-5 = epilogue (tcgen05.ld -> fused epilogue -> global).
+//   k_gemm_tn : P_s[M,N] = A[K_s,M]^T · B[K_s,N]   contraction over nodes (weight gradient),
+//               both operands MN-major in shared memory; split-K over node ranges, FP32 partials
+//               reduced afterwards in a fixed order (deterministic; "thread-local buffers
+//               before a final reduction", without the paper's atomics P:361).
+//
+// These GEMMs are HBM-bound at GCN shapes (arithmetic intensity 15-64 flop/B < TF32 ridge,
+// SURVEY §8(d) d.2): the design goal is streaming A at full bandwidth.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace mph {
+
+Dropout make_dropout(const mph_epilogue* e);
+
+namespace {
+
+constexpr int kBM = 128;          // UMMA M (rows per CTA tile)
+constexpr int kBK = 32;           // fp32 elements per 128 B swizzle row
+constexpr int kThreads = 192;     // 6 warps
+constexpr uint32_t kATileBytes = kBM * kBK * 4;  // 16 KB
+
+struct EpiG {
+  uint32_t flags;
+  const float* row_scale;
+  const float* bias;
+  const float* mask_src;
+  int ld_mask;
+  float mask_scale;
+  float* colsum_out;
+  Dropout drop;
+  int64_t row0;
+};
+
+struct NtParams {
+  int M, N, K, BN, stages, num_kb;
+  float* C;
+  int ldc;
+  uint32_t idesc, tmem_cols;
+  EpiG epi;
+};
+
+struct TnParams {
+  int M, N, K, BN, stages, num_kb, kb_per_split;
+  float* ws;
+  uint32_t idesc, tmem_cols;
+};
+
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_nt(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, NtParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t b_bytes = (uint32_t)p.BN * kBK * 4;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)p.stages * kATileBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * b_bytes);
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  float* colsum_sm = reinterpret_cast<float*>(tmem_slot + 4);  // [4][BN]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kBM;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        const int s = kb % p.stages;
+        const uint32_t ph = (uint32_t)(kb / p.stages) & 1u;
+        tc::mbar_wait(&empty[s], ph ^ 1u);
+        tc::mbar_arrive_expect_tx(&full[s], kATileBytes + b_bytes);
+        tc::tma_load_2d(sA + (size_t)s * kATileBytes, &tmA, &full[s], kb * kBK, m0);
+        tc::tma_load_2d(sB + (size_t)s * b_bytes, &tmB, &full[s], kb * kBK, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      for (int kb = 0; kb < p.num_kb; ++kb) {
+        const int s = kb % p.stages;
+        const uint32_t ph = (uint32_t)(kb / p.stages) & 1u;
+        tc::mbar_wait(&full[s], ph);
+        tc::fence_after_sync();
+        const uint32_t a_base = tc::smem_u32(sA + (size_t)s * kATileBytes);
+        const uint32_t b_base = tc::smem_u32(sB + (size_t)s * b_bytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 8; ++k) {  // UMMA_K = 8 for tf32 (32 B of each 128 B row)
+          const uint64_t da = tc::smem_desc_sw128(a_base + k * 32, 16, 1024);
+          const uint64_t db = tc::smem_desc_sw128(b_base + k * 32, 16, 1024);
+          tc::mma_tf32(tmem, da, db, p.idesc, (kb | k) != 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
+      }
+      tc::mma_commit(tfull);  // accumulator complete
+    }
+  } else {  // ---------------- epilogue warps 2..5
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = m0 + q * 32 + lane;
+    const bool row_ok = row < p.M;
+    if (p.num_kb > 0) {
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after_sync();
+    }
+    const EpiG& e = p.epi;
+    const float rs = (row_ok && (e.flags & MPH_EPI_ROWSCALE)) ? e.row_scale[row] : 1.0f;
+    float* crow = p.C + (int64_t)row * p.ldc;
+    for (int c0 = 0; c0 < p.BN; c0 += 16) {
+      float v[16];
+      if (p.num_kb > 0)
+        tc::tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+      else
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = c0 + i;
+        float x = v[i];
+        if (c < p.N && row_ok) {
+          if (e.flags & MPH_EPI_BIAS) x += e.bias[c];
+          if (e.flags & MPH_EPI_MASK) x = (e.mask_src[(int64_t)row * e.ld_mask + c] > 0.0f) ? x * e.mask_scale : 0.0f;
+          if (e.flags & MPH_EPI_RELU) x = fmaxf(x, 0.0f);
+        } else {
+          x = 0.0f;
+        }
+        v[i] = x;
+      }
+      if (e.flags & MPH_EPI_DROPOUT) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const int c = c0 + i;
+          PhiloxOut r = philox4x32_10((uint32_t)(e.row0 + row), (uint32_t)(c >> 2), e.drop.layer, e.drop.epoch,
+                                      e.drop.key0, e.drop.key1);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[i + j] = r.v[j] >= e.drop.threshold ? v[i + j] * e.drop.scale : 0.0f;
+        }
+      }
+      if (e.flags & MPH_EPI_COLSUM) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float t = v[i];
+#pragma unroll
+          for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+          if (lane == 0) colsum_sm[q * p.BN + c0 + i] = t;
+        }
+      }
+      if (row_ok) {
+        if (c0 + 16 <= p.N && (p.ldc & 3) == 0) {
+          float4* dst = reinterpret_cast<float4*>(crow + c0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_float4(v[4 * i] * rs, v[4 * i + 1] * rs, v[4 * i + 2] * rs, v[4 * i + 3] * rs);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < p.N) crow[c0 + i] = v[i] * rs;
+        }
+      }
+    }
+    if (e.flags & MPH_EPI_COLSUM) {
+      epi_bar_sync();
+      const int t = threadIdx.x - 64;
+      for (int c = t; c < p.N; c += 128) {
+        float sacc = colsum_sm[c];
+        sacc += colsum_sm[p.BN + c];
+        sacc += colsum_sm[2 * p.BN + c];
+        sacc += colsum_sm[3 * p.BN + c];
+        e.colsum_out[(int64_t)blockIdx.x * p.N + c] = sacc;
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_tn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kChunk = kBK * 128;  // one 32-wide MN chunk of BK rows: 4 KB
+  const uint32_t a_bytes = 4 * kChunk;    // 128 = 4 chunks of 32 along M
+  const uint32_t nchunk_b = (uint32_t)p.BN / 32;
+  const uint32_t b_bytes = nchunk_b * kChunk;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + (size_t)p.stages * a_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * b_bytes);
+  uint64_t* empty = full + p.stages;
+  uint64_t* tfull = empty + p.stages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * kBM;
+  const int split = blockIdx.y;
+  const int kb0 = split * p.kb_per_split;
+  const int kb1 = min(p.num_kb, kb0 + p.kb_per_split);
+  const int nkb = max(0, kb1 - kb0);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(tfull, 1);
+    tc::fence_barrier_init();
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int kb = kb0 + i;
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        tc::mbar_wait(&empty[s], ph ^ 1u);
+        tc::mbar_arrive_expect_tx(&full[s], a_bytes + b_bytes);
+        uint8_t* a_dst = sA + (size_t)s * a_bytes;
+        uint8_t* b_dst = sB + (size_t)s * b_bytes;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tma_load_2d(a_dst + c * kChunk, &tmA, &full[s], m0 + 32 * c, kb * kBK);
+        for (uint32_t c = 0; c < nchunk_b; ++c) tc::tma_load_2d(b_dst + c * kChunk, &tmB, &full[s], 32 * c, kb * kBK);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % p.stages;
+        const uint32_t ph = (uint32_t)(i / p.stages) & 1u;
+        tc::mbar_wait(&full[s], ph);
+        tc::fence_after_sync();
+        const uint32_t a_base = tc::smem_u32(sA + (size_t)s * a_bytes);
+        const uint32_t b_base = tc::smem_u32(sB + (size_t)s * b_bytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 8; ++k) {  // 8 node rows = one 1024 B swizzle atom per chunk
+          const uint64_t da = tc::smem_desc_sw128(a_base + k * 1024, kChunk, 1024);
+          const uint64_t db = tc::smem_desc_sw128(b_base + k * 1024, kChunk, 1024);
+          tc::mma_tf32(tmem, da, db, p.idesc, (i | k) != 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(tfull);
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = m0 + q * 32 + lane;
+    if (nkb > 0) {
+      tc::mbar_wait(tfull, 0);
+      tc::fence_after_sync();
+    }
+    float* out = p.ws + ((int64_t)split * p.M + row) * p.N;
+    for (int c0 = 0; c0 < p.BN; c0 += 16) {
+      float v[16];
+      if (nkb > 0)
+        tc::tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
+      else
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+      if (row < p.M) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < p.N) out[c0 + i] = v[i];
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
+}
+
+__global__ void k_reduce_rows(const float* in, int rows, int cols, int ld, float* out, int accumulate) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
+    float s = accumulate ? out[c] : 0.0f;
+    for (int r = 0; r < rows; ++r) s += in[(int64_t)r * ld + c];
+    out[c] = s;
+  }
+}
+
+// out[r*ldc + c] = sum_s ws[(s*M + r)*N + c]   (fixed order over splits)
+__global__ void k_reduce_splits(const float* ws, int splits, int M, int N, float* C, int ldc) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / N;
+    const int c = (int)(t - r * N);
+    float s = 0.0f;
+    for (int k = 0; k < splits; ++k) s += ws[(int64_t)k * total + t];
+    C[r * ldc + c] = s;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+int make_tmap(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+              uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return fail(MPH_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no device)");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld * sizeof(float)};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(MPH_ECUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu box=%ux%u", (int)r,
+                (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)ld, box_inner, box_outer);
+  return MPH_OK;
+}
+
+uint32_t tmem_cols_for(int n) {
+  uint32_t c = 32;
+  while ((int)c < n) c <<= 1;
+  return c;
+}
+
+constexpr size_t kSmemBudget = 100 * 1024;  // ~2 CTAs per SM (one epilogue overlaps another's mainloop)
+
+int gemm_tn_splits(int M, int N, int K) {
+  const int mtiles = (int)ceil_div(M, kBM);
+  const int num_kb = (int)ceil_div(K, kBK);
+  const int want = std::max(1, (2 * 148 + mtiles - 1) / mtiles);
+  return std::max(1, std::min(want, std::max(1, num_kb / 4)));
+}
+
+}  // namespace
+
+int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
+                   const mph_epilogue* epi, cudaStream_t s) {
+  if (M < 0 || N <= 0 || K < 0 || !A || !Bt || !C) return fail(MPH_EINVAL, "gemm_nt: bad arguments");
+  if (N > 256) return fail(MPH_ENOTSUP, "gemm_nt: N=%d > 256", N);
+  if (lda % 4 || ldb % 4 || lda < K || ldb < K || ldc < N)
+    return fail(MPH_EINVAL, "gemm_nt: lda/ldb must be multiples of 4 >= K, ldc >= N");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Bt)) & 15)
+    return fail(MPH_EINVAL, "gemm_nt: A and Bt must be 16-byte aligned");
+  const uint32_t flags = epi ? epi->flags : 0u;
+  if ((flags & MPH_EPI_BIAS) && !epi->bias) return fail(MPH_EINVAL, "gemm_nt: null bias");
+  if ((flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "gemm_nt: null row_scale");
+  if ((flags & MPH_EPI_MASK) && !epi->mask_src) return fail(MPH_EINVAL, "gemm_nt: null mask_src");
+  if ((flags & MPH_EPI_COLSUM) && !epi->colsum_out) return fail(MPH_EINVAL, "gemm_nt: null colsum_out");
+  if (M == 0) return MPH_OK;
+  const int BN = round_up(N, 16);
+  NtParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.BN = BN;
+  p.num_kb = (int)ceil_div(K, kBK);
+  const size_t stage_bytes = kATileBytes + (size_t)BN * kBK * 4;
+  p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, kSmemBudget / stage_bytes));
+  p.C = C;
+  p.ldc = ldc;
+  p.idesc = tc::idesc_tf32(kBM, BN, 0, 0);
+  p.tmem_cols = tmem_cols_for(BN);
+  p.epi.flags = flags;
+  p.epi.row_scale = epi ? epi->row_scale : nullptr;
+  p.epi.bias = epi ? epi->bias : nullptr;
+  p.epi.mask_src = epi ? epi->mask_src : nullptr;
+  p.epi.ld_mask = epi ? epi->ld_mask : 0;
+  p.epi.mask_scale = epi ? epi->mask_scale : 1.0f;
+  p.epi.colsum_out = epi ? epi->colsum_out : nullptr;
+  p.epi.drop = make_dropout(epi);
+  p.epi.row0 = epi ? epi->row0 : 0;
+  if (p.epi.drop.threshold == 0) p.epi.flags &= ~MPH_EPI_DROPOUT;
+  CUtensorMap ta, tb;
+  MPH_TRY(make_tmap(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM));
+  MPH_TRY(make_tmap(&tb, Bt, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kBK, (uint32_t)BN));
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (2 * p.stages + 1) * 8 + 16 + 4 * BN * sizeof(float);
+  static size_t configured = 0;
+  if (smem > configured) {
+    MPH_CUDA_TRY(cudaFuncSetAttribute(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  k_gemm_nt<<<(unsigned)ceil_div(M, kBM), kThreads, smem, s>>>(ta, tb, p);
+  count_launch();
+  return launch_check("gemm_nt");
+}
+
+size_t gemm_tn_ws_bytes(int M, int N, int K) {
+  if (M <= 0 || N <= 0) return 0;
+  return (size_t)gemm_tn_splits(M, N, K) * M * N * sizeof(float);
+}
+
+int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc, void* ws,
+                   size_t ws_bytes, cudaStream_t s) {
+  if (M <= 0 || N <= 0 || K < 0 || !A || !B || !C) return fail(MPH_EINVAL, "gemm_tn: bad arguments");
+  if (N > 256) return fail(MPH_ENOTSUP, "gemm_tn: N=%d > 256", N);
+  if (lda % 4 || ldb % 4 || lda < M || ldb < N || ldc < N)
+    return fail(MPH_EINVAL, "gemm_tn: lda/ldb must be multiples of 4 with lda >= M, ldb >= N, ldc >= N");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
+    return fail(MPH_EINVAL, "gemm_tn: A and B must be 16-byte aligned");
+  const size_t need = gemm_tn_ws_bytes(M, N, K);
+  if (!ws || ws_bytes < need) return fail(MPH_EINVAL, "gemm_tn: workspace %zu < %zu bytes", ws_bytes, need);
+  const int BN = round_up(N, 32);
+  TnParams p{};
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.BN = BN;
+  p.num_kb = (int)ceil_div(K, kBK);
+  const int splits = gemm_tn_splits(M, N, K);
+  p.kb_per_split = (int)ceil_div(std::max(p.num_kb, 1), splits);
+  const size_t stage_bytes = (size_t)4 * kBK * 128 + (size_t)(BN / 32) * kBK * 128;
+  p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, kSmemBudget / stage_bytes));
+  p.ws = reinterpret_cast<float*>(ws);
+  p.idesc = tc::idesc_tf32(kBM, BN, 1, 1);
+  p.tmem_cols = tmem_cols_for(BN);
+  CUtensorMap ta, tb;
+  MPH_TRY(make_tmap(&ta, A, (uint64_t)M, (uint64_t)std::max(K, 1), (uint64_t)lda, 32, kBK));
+  MPH_TRY(make_tmap(&tb, B, (uint64_t)N, (uint64_t)std::max(K, 1), (uint64_t)ldb, 32, kBK));
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (2 * p.stages + 1) * 8 + 16;
+  static size_t configured = 0;
+  if (smem > configured) {
+    MPH_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  dim3 grid((unsigned)ceil_div(M, kBM), (unsigned)splits);
+  k_gemm_tn<<<grid, kThreads, smem, s>>>(ta, tb, p);
+  count_launch();
+  MPH_TRY(launch_check("gemm_tn"));
+  const int64_t total = (int64_t)M * N;
+  k_reduce_splits<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, s>>>(p.ws, splits, M, N, C, ldc);
+  count_launch();
+  return launch_check("reduce_splits");
+}
+
+int reduce_rows_launch(const float* in, int rows, int cols, int ld, float* out, int accumulate, cudaStream_t s) {
+  if (!in || !out || rows < 0 || cols <= 0 || ld < cols) return fail(MPH_EINVAL, "reduce_rows: bad arguments");
+  k_reduce_rows<<<(unsigned)ceil_div(cols, 128), 128, 0, s>>>(in, rows, cols, ld, out, accumulate);
+  count_launch();
+  return launch_check("reduce_rows");
+}
+
+}  // namespace mph
+
+extern "C" int mph_gemm_nt(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, const float* Bt_d,
+                           int32_t ldb, float* C_d, int32_t ldc, const mph_epilogue* epi, void* stream) {
+  return mph::gemm_nt_launch(M, N, K, A_d, lda, Bt_d, ldb, C_d, ldc, epi, (cudaStream_t)stream);
+}
+
+extern "C" int mph_gemm_tn_workspace(int32_t M, int32_t N, int32_t K, size_t* bytes_h) {
+  if (!bytes_h) return mph::fail(MPH_EINVAL, "null bytes");
+  *bytes_h = mph::gemm_tn_ws_bytes(M, N, K);
+  return MPH_OK;
+}
+
+extern "C" int mph_gemm_tn(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, const float* B_d,
+                           int32_t ldb, float* C_d, int32_t ldc, void* ws_d, size_t ws_bytes, void* stream) {
+  return mph::gemm_tn_launch(M, N, K, A_d, lda, B_d, ldb, C_d, ldc, ws_d, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int mph_reduce_rows(const float* in_d, int32_t rows, int32_t cols, int32_t ld, float* out_d,
+                               int32_t accumulate, void* stream) {
+  return mph::reduce_rows_launch(in_d, rows, cols, ld, out_d, accumulate, (cudaStream_t)stream);
+}

@@ -1,0 +1,76 @@
+// Library-internal handle layouts and kernel launchers shared between translation units.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+struct mph_graph {
+  int32_t n_rows = 0;  // owned rows
+  int32_t n_cols = 0;  // owned + ghost nodes (== n_rows for a global graph)
+  int64_t nnz = 0;
+  int32_t max_deg = 0;
+  int64_t* row_ptr = nullptr;  // [n_rows+1]
+  int32_t* col_idx = nullptr;  // [nnz] (local ids for a localized graph)
+  int32_t* deg = nullptr;      // [n_cols] global degree d~
+  float* dinv = nullptr;       // [n_cols]
+  // localized graphs only (D2-D4)
+  bool local = false;
+  int32_t world = 1, rank = 0;
+  int64_t row0 = 0;
+  int64_t* split = nullptr;  // [n_rows] absolute edge index where ghost columns start
+  std::vector<int64_t> recv_offset, n_recv, send_offset;  // host, per peer
+  int32_t* send_ids = nullptr;                            // device, concatenated per peer
+  int64_t n_send = 0;
+  float* send_buf = nullptr;
+  size_t send_cap = 0;  // floats
+};
+
+struct mph_features {
+  int32_t N = 0, F = 0, P = 0;  // P = padded row stride of the dense copy
+  int64_t nnz = 0;
+  int32_t mode = 0, is_binary = 0;
+  float* X = nullptr;  // dense mode: [N][P]
+  int64_t* csr_ptr = nullptr;
+  int32_t* csr_idx = nullptr;
+  float* csr_val = nullptr;
+  int64_t* csc_ptr = nullptr;
+  int32_t* csc_idx = nullptr;
+  float* csc_val = nullptr;
+};
+
+namespace mph {
+
+// dinv[u] = (float)(1.0 / sqrt((double)deg[u]))  (G6)
+int launch_dinv(const int32_t* deg, float* dinv, int64_t n, cudaStream_t s);
+
+// SpMM driver (spmm.cu). part: -1 whole row, 0 owned columns (raw sums, no epilogue),
+// 1 ghost columns accumulated onto out + epilogue.
+int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
+                const mph_epilogue* epi, cudaStream_t s);
+// Halo pack (spmm.cu): send_buf[j] = buf[send_ids[j]] for the whole send list.
+int pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int w, float* out, cudaStream_t s);
+
+int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
+                   const mph_epilogue* epi, cudaStream_t s);
+size_t gemm_tn_ws_bytes(int M, int N, int K);
+int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
+                   void* ws, size_t ws_bytes, cudaStream_t s);
+int reduce_rows_launch(const float* in, int rows, int cols, int ld, float* out, int accumulate, cudaStream_t s);
+
+size_t softmax_ce_ws_bytes(int N, int C);
+int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* labels, const uint8_t* mask, int64_t n_lab,
+                      const float* row_scale, float* dZ, int ld_dz, float* db, double* loss, void* ws, size_t ws_bytes,
+                      cudaStream_t s);
+int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s);
+int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int layer, cudaStream_t s);
+// dst[j*ld_dst + i] = src[i*ld_src + j] for i < rows, j < cols  (weight transposes)
+int transpose_launch(const float* src, int rows, int cols, int ld_src, float* dst, int ld_dst, cudaStream_t s);
+int sparse_xw_launch(const mph_features* f, const float* W, int F_out, int ldw, const float* row_scale, float* T,
+                     int ldt, cudaStream_t s);
+int sparse_xtg_launch(const mph_features* f, const float* G, int F_out, int ldg, float* dW, int lddw, cudaStream_t s);
+// out[i][c] = in[i][c] * scale[i] for c < w (padded columns copied as zero)
+int rowscale_launch(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out,
+                    cudaStream_t s);
+
+}  // namespace mph

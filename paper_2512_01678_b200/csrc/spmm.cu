@@ -1,0 +1,252 @@
+// a3/a6 — aggregation SpMM with fused epilogue (Alg. 3; fused message passing
+// without |E|xF buffers P:361; T_comp ∝ Σ deg·F P:550-555).
+//
+// B200 design (differs from the paper's block-per-row):
+//  * one warp per output row.  The row's width is covered by LPR lanes holding VPL float4
+//    each; the remaining 32/LPR "edge slots" walk different neighbours of the same row, so
+//    all 32 lanes stay busy for every width (48-wide rows: 4 lanes x 3 float4 x 8 slots).
+//  * neighbour ids are read 32 at a time with one coalesced 128 B load (L1 no-allocate) and
+//    broadcast by shuffles; each lane then issues U independent 16 B gathers before it
+//    consumes any (U x VPL loads in flight per lane).
+//  * per-edge values are pre-scaled by dinv at the producer (T' = dinv ⊙ T), so the kernel
+//    reads no per-edge weight: out[u] = dinv[u] · Σ_v T'[v]  ==  (Â·T)[u]  (Q1).
+//  * partial sums: a pairwise tree over each group of U gathers, a running sum per slot,
+//    and a fixed xor-shuffle tree across slots — deterministic, atomic-free.
+//  * epilogue fused: dinv, bias, ReLU, inverted dropout (Philox, Q10), row scale.
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace mph {
+
+struct EpiDev {
+  uint32_t flags;
+  const float* bias;
+  const float* row_scale;
+  Dropout drop;
+  int64_t row0;
+};
+
+struct SpmmArgs {
+  const int64_t* row_ptr;
+  const int64_t* split;
+  const int32_t* col;
+  const float* dinv;
+  const float* in;
+  float* out;
+  int ld_in, ld_out, n_rows, nv4, part;
+  EpiDev epi;
+};
+
+__device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int64_t grow, int c4) {
+  PhiloxOut r = philox4x32_10((uint32_t)grow, (uint32_t)c4, d.layer, d.epoch, d.key0, d.key1);
+  v.x = r.v[0] >= d.threshold ? v.x * d.scale : 0.0f;
+  v.y = r.v[1] >= d.threshold ? v.y * d.scale : 0.0f;
+  v.z = r.v[2] >= d.threshold ? v.z * d.scale : 0.0f;
+  v.w = r.v[3] >= d.threshold ? v.w * d.scale : 0.0f;
+  return v;
+}
+
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(256, 2) k_spmm(SpmmArgs a) {
+  constexpr int ES = 32 / LPR;
+  // U gathers per slot in flight; U*VPL float4 loads per lane before the first use
+  constexpr int U0 = (32 / ES) < 8 ? (32 / ES) : 8;
+  constexpr int U = (U0 * VPL > 8) ? ((8 / VPL) < 2 ? 2 : (8 / VPL)) : U0;
+  const int lane = threadIdx.x & 31;
+  const int slot = lane / LPR, sub = lane % LPR;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < a.n_rows; row += nwarps) {
+    int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
+    if (a.part == 0) e = a.split[row];
+    if (a.part == 1) s = a.split[row];
+    float4 acc[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
+    for (int64_t base = s; base < e; base += 32) {
+      const int nb = (int)min((int64_t)32, e - base);
+      const int my_c = lane < nb ? ldg_stream_i32(a.col + base + lane) : 0;
+      for (int k0 = 0; k0 < nb; k0 += ES * U) {
+        float4 x[U][VPL];
+#pragma unroll
+        for (int uu = 0; uu < U; ++uu) {
+          const int k = k0 + uu * ES + slot;
+          const int c = __shfl_sync(0xffffffffu, my_c, k & 31);
+          const float4* p = reinterpret_cast<const float4*>(a.in + (int64_t)c * a.ld_in) + sub;
+#pragma unroll
+          for (int j = 0; j < VPL; ++j)
+            x[uu][j] = (k < nb && sub + j * LPR < a.nv4) ? ldg_f4(p + j * LPR) : f4_zero();
+        }
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) {
+#pragma unroll
+          for (int w = 1; w < U; w <<= 1)
+#pragma unroll
+            for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add(x[uu][j], x[uu + w][j]);
+          acc[j] = f4_add(acc[j], x[0][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        acc[j].x += __shfl_xor_sync(0xffffffffu, acc[j].x, off);
+        acc[j].y += __shfl_xor_sync(0xffffffffu, acc[j].y, off);
+        acc[j].z += __shfl_xor_sync(0xffffffffu, acc[j].z, off);
+        acc[j].w += __shfl_xor_sync(0xffffffffu, acc[j].w, off);
+      }
+    if (slot != 0) continue;
+    float4* orow = reinterpret_cast<float4*>(a.out + (int64_t)row * a.ld_out);
+    if (a.part == 0) {
+#pragma unroll
+      for (int j = 0; j < VPL; ++j)
+        if (sub + j * LPR < a.nv4) orow[sub + j * LPR] = acc[j];
+      continue;
+    }
+    const float du = a.dinv[row];
+    const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[row] : 1.0f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c4 = sub + j * LPR;
+      if (c4 >= a.nv4) continue;
+      float4 v = acc[j];
+      if (a.part == 1) v = f4_add(v, orow[c4]);
+      v.x *= du;
+      v.y *= du;
+      v.z *= du;
+      v.w *= du;
+      if (a.epi.flags & MPH_EPI_BIAS) {
+        float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
+        v = f4_add(v, b);
+      }
+      if (a.epi.flags & MPH_EPI_RELU) {
+        v.x = fmaxf(v.x, 0.0f);
+        v.y = fmaxf(v.y, 0.0f);
+        v.z = fmaxf(v.z, 0.0f);
+        v.w = fmaxf(v.w, 0.0f);
+      }
+      if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, c4);
+      if (a.epi.flags & MPH_EPI_ROWSCALE) {
+        v.x *= rs;
+        v.y *= rs;
+        v.z *= rs;
+        v.w *= rs;
+      }
+      orow[c4] = v;
+    }
+  }
+}
+
+Dropout make_dropout(const mph_epilogue* e) {
+  Dropout d{};
+  if (!e || !(e->flags & MPH_EPI_DROPOUT) || e->dropout_p <= 0.0f) {
+    d.threshold = 0;
+    d.scale = 1.0f;
+    return d;
+  }
+  const double p = (double)e->dropout_p;
+  d.threshold = (uint32_t)floor(p * 4294967296.0);
+  d.scale = (float)(1.0 / (1.0 - p));
+  d.key0 = (uint32_t)(e->dropout_seed & 0xffffffffull);
+  d.key1 = (uint32_t)(e->dropout_seed >> 32);
+  d.layer = (uint32_t)e->dropout_layer;
+  d.epoch = (uint32_t)e->dropout_epoch;
+  return d;
+}
+
+template <int LPR, int VPL>
+static void launch_spmm(const SpmmArgs& a, cudaStream_t s) {
+  const int64_t warps = a.n_rows;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(warps, 8));
+  k_spmm<LPR, VPL><<<grid, 256, 0, s>>>(a);
+}
+
+int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
+                const mph_epilogue* epi, cudaStream_t s) {
+  if (!g || !in || !out) return fail(MPH_EINVAL, "spmm: null argument");
+  if (w <= 0 || w % 4 || ld_in % 4 || ld_out % 4 || ld_in < w || ld_out < w)
+    return fail(MPH_EINVAL, "spmm: w, ld_in, ld_out must be multiples of 4 with ld >= w (w=%d)", w);
+  if (w > 512) return fail(MPH_ENOTSUP, "spmm: width %d > 512", w);
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(MPH_EINVAL, "spmm: operands must be 16-byte aligned");
+  if (part != -1 && !g->local) return fail(MPH_EINVAL, "spmm: row parts need a localized graph");
+  const uint32_t allowed = MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE;
+  if (epi && (epi->flags & ~allowed)) return fail(MPH_EINVAL, "spmm: unsupported epilogue flags 0x%x", epi->flags);
+  if (epi && (epi->flags & MPH_EPI_BIAS) && (!epi->bias || (reinterpret_cast<uintptr_t>(epi->bias) & 15)))
+    return fail(MPH_EINVAL, "spmm: bias must be non-null and 16-byte aligned");
+  if (epi && (epi->flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "spmm: null row_scale");
+  if (g->n_rows == 0) return MPH_OK;
+  SpmmArgs a;
+  a.row_ptr = g->row_ptr;
+  a.split = g->split;
+  a.col = g->col_idx;
+  a.dinv = g->dinv;
+  a.in = in;
+  a.out = out;
+  a.ld_in = ld_in;
+  a.ld_out = ld_out;
+  a.n_rows = g->n_rows;
+  a.nv4 = w / 4;
+  a.part = part;
+  a.epi.flags = epi ? epi->flags : 0u;
+  a.epi.bias = epi ? epi->bias : nullptr;
+  a.epi.row_scale = epi ? epi->row_scale : nullptr;
+  a.epi.drop = make_dropout(epi);
+  a.epi.row0 = epi ? epi->row0 : 0;
+  if (a.epi.drop.threshold == 0) a.epi.flags &= ~MPH_EPI_DROPOUT;
+  const int nv4 = a.nv4;
+  if (nv4 <= 1)
+    launch_spmm<1, 1>(a, s);
+  else if (nv4 <= 2)
+    launch_spmm<2, 1>(a, s);
+  else if (nv4 <= 4)
+    launch_spmm<4, 1>(a, s);
+  else if (nv4 <= 8)
+    launch_spmm<8, 1>(a, s);
+  else if (nv4 <= 12)
+    launch_spmm<4, 3>(a, s);
+  else if (nv4 <= 16)
+    launch_spmm<16, 1>(a, s);
+  else if (nv4 <= 32)
+    launch_spmm<32, 1>(a, s);
+  else if (nv4 <= 64)
+    launch_spmm<32, 2>(a, s);
+  else if (nv4 <= 96)
+    launch_spmm<32, 3>(a, s);
+  else
+    launch_spmm<32, 4>(a, s);
+  count_launch();
+  return launch_check("spmm");
+}
+
+__global__ void k_pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int nv4, float* out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < n; j += nwarps) {
+    const float4* src = reinterpret_cast<const float4*>(buf + (int64_t)ids[j] * ld);
+    float4* dst = reinterpret_cast<float4*>(out + j * (int64_t)nv4 * 4);
+    for (int c = lane; c < nv4; c += 32) dst[c] = ldg_f4(src + c);
+  }
+}
+
+int pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int w, float* out, cudaStream_t s) {
+  if (n == 0) return MPH_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(n, 8), 148 * 64);
+  k_pack_rows<<<grid, 256, 0, s>>>(ids, n, buf, ld, w / 4, out);
+  count_launch();
+  return launch_check("pack_rows");
+}
+
+}  // namespace mph
+
+extern "C" int mph_spmm(const mph_graph* g, const float* in_d, int32_t w, int32_t ld_in, float* out_d, int32_t ld_out,
+                        const mph_epilogue* epi, void* stream) {
+  return mph::spmm_launch(g, -1, in_d, w, ld_in, out_d, ld_out, epi, (cudaStream_t)stream);
+}
+
+extern "C" int mph_spmm_part(const mph_graph* g, int32_t part, const float* in_d, int32_t w, int32_t ld_in, float* out_d,
+                             int32_t ld_out, const mph_epilogue* epi, void* stream) {
+  if (part < -1 || part > 1) return mph::fail(MPH_EINVAL, "spmm_part: part must be -1, 0 or 1");
+  return mph::spmm_launch(g, part, in_d, w, ld_in, out_d, ld_out, epi, (cudaStream_t)stream);
+}

@@ -1,0 +1,342 @@
+"""Per-kernel parity on the GPU, through the C-ABI, against the FP64 oracle.
+
+Integer work (graph build, switch, CSR/CSC) is compared bit for bit; FP32 aggregation within
+1e-5 of the magnitude sum |Â|·|T|; TF32 GEMMs within 2e-3·(|A|·|B|).
+Sizes span several tiles plus a ragged tail; edge cases include empty edge lists, self loops,
+duplicate edges, isolated nodes, N = 1 and widths that are not tile multiples.
+"""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth.generate import CONFIGS, make_small, make_workload
+from tests.gpu_helpers import agg_bound, assert_agg_close, assert_gemm_close, cuda, pad_width, padded
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2512_01678_b200 as P
+    from paper_2512_01678_b200 import _lib as L
+    L.mph_device_check(C.byref(C.c_int32()))
+    return P
+
+
+# ------------------------------------------------------------------ a0 graph build (bit-exact)
+def _check_graph(P, src, dst, n):
+    g = P.Graph(src, dst, n)
+    ref = oracle.graph_build(src, dst, n)
+    rp, ci, dg, di = (t.cpu().numpy() for t in g.csr())
+    assert g.nnz == ref.nnz and g.n_rows == n
+    assert np.array_equal(rp, ref.row_ptr)
+    assert np.array_equal(ci, ref.col_idx)
+    assert np.array_equal(dg, ref.deg)
+    assert np.array_equal(di.view(np.uint32), ref.dinv.view(np.uint32))   # G6 bit recipe
+    assert g.max_deg == int(ref.deg.max())
+    return g, ref
+
+
+@pytest.mark.parametrize("seed,n,m", [(0, 1, 0), (1, 7, 0), (2, 50, 300), (3, 1000, 8000), (4, 5003, 40000)])
+def test_graph_build_bit_exact(P, seed, n, m):
+    rng = np.random.default_rng(seed)
+    src = rng.integers(0, n, m).astype(np.int32)
+    dst = rng.integers(0, n, m).astype(np.int32)
+    if m:
+        src[:m // 10] = dst[:m // 10]            # self loops (dropped, Q2)
+        src[m // 10:m // 5] = src[m // 5:m // 5 + (m // 5 - m // 10)]  # duplicates after symmetrising
+    _check_graph(P, src, dst, n)
+
+
+@pytest.mark.parametrize("name", ["cora", "pubmed", "arxiv"])
+def test_graph_build_configs(P, name):
+    w = make_workload(name)
+    g, ref = _check_graph(P, w["src"], w["dst"], w["cfg"].num_nodes)
+    assert g.nnz == w["cfg"].nnz_a + w["cfg"].num_nodes
+
+
+def test_graph_build_errors(P):
+    from paper_2512_01678_b200._lib import MorphlingError
+    with pytest.raises(MorphlingError) as e:
+        P.Graph(np.array([0, 5]), np.array([1, 1]), 5)
+    assert e.value.name == "MPH_ERANGE"
+    with pytest.raises(MorphlingError) as e:
+        P.Graph(np.array([], np.int32), np.array([], np.int32), 0)
+    assert e.value.name == "MPH_EDEGENERATE"
+
+
+# ------------------------------------------------------------------ a1 switch (bit-exact)
+@pytest.mark.parametrize("name", ["cora", "pubmed"])
+def test_feature_switch_configs(P, name):
+    w = make_workload(name)
+    X = w["X"]
+    f = P.Features(cuda(X))
+    ref = oracle.analyze_features(X, 8000)
+    assert (f.nnz, f.mode, f.is_binary) == (ref.nnz, ref.mode, ref.is_binary)
+    assert f.mode == 1                                 # both are Sparse at tau = 0.80 (SURVEY table)
+    for got, exp in zip(f.csr(), ref.csr):
+        assert np.array_equal(got.cpu().numpy(), exp)
+    for got, exp in zip(f.csc(), ref.csc):
+        assert np.array_equal(got.cpu().numpy(), exp)
+
+
+def test_feature_switch_boundary(P):
+    X = np.zeros((10, 10), np.float32)
+    X.flat[:20] = 2.5                                  # s = 0.80 exactly -> Sparse
+    assert P.Features(cuda(X)).mode == 1
+    X.flat[20] = -1.0                                  # s = 0.79 -> Dense
+    f = P.Features(cuda(X))
+    assert f.mode == 0 and f.nnz == 21
+    Xd = f.dense().cpu().numpy()
+    assert np.array_equal(Xd[:, :10], X) and np.all(Xd[:, 10:] == 0)
+    X = np.zeros((3, 5), np.float32)
+    X[1, 1] = -0.0
+    assert P.Features(cuda(X)).nnz == 0                # -0.0 counts as zero (Q12)
+    f = P.Features(cuda(np.ones((4, 4), np.float32)), force_mode=1)
+    assert f.mode == 1 and f.is_binary
+
+
+# ------------------------------------------------------------------ a3/a6 aggregation SpMM
+@pytest.fixture(scope="module")
+def spmm_graph(P):
+    w = make_small(3001, 60000, 4, 5, seed=21, alpha=2.1)       # ragged rows, hubs, 3001 = 8*375+1
+    src = np.concatenate([w["src"], np.zeros(2500, np.int32)])   # one hub of degree > 2500
+    dst = np.concatenate([w["dst"], np.arange(1, 2501, dtype=np.int32)])
+    g = P.Graph(src, dst, 3001)
+    return g, oracle.graph_build(src, dst, 3001)
+
+
+@pytest.mark.parametrize("w", [4, 8, 16, 24, 40, 48, 64, 104, 128, 256, 512])
+def test_spmm_widths(P, spmm_graph, w):
+    g, ref = spmm_graph
+    rng = np.random.default_rng(w)
+    T = rng.standard_normal((ref.num_nodes, w)).astype(np.float32)
+    Tp = (ref.dinv[:, None] * T).astype(np.float32)             # producer pre-scale, f32
+    ld = w + (8 if w % 8 == 0 else 4)                            # non-trivial row strides
+    tin = cuda(padded(Tp, ld))
+    out = torch.zeros((ref.num_nodes, ld), device="cuda")
+    g.spmm(tin, out, w=w)
+    Z = out[:, :w].cpu().numpy()
+    assert np.all(out[:, w:].cpu().numpy() == 0)
+    assert_agg_close(Z, oracle.aggregate(ref, T), agg_bound(ref, T), what=f"spmm w={w}")
+
+
+def test_spmm_bias_relu_and_determinism(P, spmm_graph):
+    from paper_2512_01678_b200._lib import EPI_BIAS, EPI_RELU, Epilogue
+    g, ref = spmm_graph
+    w = 48
+    rng = np.random.default_rng(5)
+    T = rng.standard_normal((ref.num_nodes, w)).astype(np.float32)
+    b = rng.standard_normal(w).astype(np.float32)
+    Tp = (ref.dinv[:, None] * T).astype(np.float32)
+    tin, bias = cuda(Tp), cuda(b)
+    e = Epilogue()
+    e.flags = EPI_BIAS | EPI_RELU
+    e.bias = bias.data_ptr()
+    e.mask_scale = 1.0
+    out1 = torch.zeros((ref.num_nodes, w), device="cuda")
+    out2 = torch.zeros_like(out1)
+    g.spmm(tin, out1, epi=e)
+    g.spmm(tin, out2, epi=e)
+    assert torch.equal(out1, out2)                               # bitwise deterministic
+    Zpre = oracle.aggregate(ref, T) + b
+    bound = agg_bound(ref, T) + np.abs(b)
+    Z = out1.cpu().numpy()
+    # ReLU is 1-Lipschitz: |relu(z) - relu(z*)| <= |z - z*|
+    assert_agg_close(Z, np.maximum(Zpre, 0), bound, what="spmm bias+relu")
+
+
+def test_spmm_dropout_mask_matches_oracle(P, spmm_graph):
+    from paper_2512_01678_b200._lib import EPI_BIAS, EPI_DROPOUT, EPI_RELU, Epilogue
+    g, ref = spmm_graph
+    w, p, seed, layer, epoch = 64, 0.3, 0x1234567890ABCDEF, 1, 7
+    rng = np.random.default_rng(9)
+    T = np.abs(rng.standard_normal((ref.num_nodes, w))).astype(np.float32) + 0.5   # strictly positive
+    Tp = (ref.dinv[:, None] * T).astype(np.float32)
+    bias = cuda(np.zeros(w, np.float32))
+    e = Epilogue()
+    e.flags = EPI_BIAS | EPI_RELU | EPI_DROPOUT
+    e.bias = bias.data_ptr()
+    e.dropout_p, e.dropout_seed, e.dropout_layer, e.dropout_epoch = p, seed, layer, epoch
+    out = torch.zeros((ref.num_nodes, w), device="cuda")
+    g.spmm(cuda(Tp), out, epi=e)
+    Z = out.cpu().numpy()
+    keep = oracle.dropout_keep(ref.num_nodes, w, p, seed, layer, epoch)
+    assert np.array_equal(Z != 0, keep)                          # mask decisions bit-exact
+    ref_z = oracle.aggregate(ref, T) * keep / (1.0 - float(np.float32(p)))
+    assert_agg_close(Z, ref_z, agg_bound(ref, T) / (1 - p), rtol=2e-5, what="spmm dropout")
+
+
+# ------------------------------------------------------------------ a2/a4/a8 GEMM (tcgen05)
+@pytest.mark.parametrize("M,N,K", [(1, 16, 8), (300, 16, 16), (1000, 48, 104), (4099, 128, 608),
+                                   (2050, 256, 256), (777, 8, 16), (513, 40, 256), (1200, 64, 500)])
+def test_gemm_nt(P, M, N, K):
+    from paper_2512_01678_b200._lib import mph_gemm_nt
+    rng = np.random.default_rng(M + N + K)
+    lda, ldb = (K + 3) // 4 * 4, (K + 3) // 4 * 4
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    Bt = rng.standard_normal((N, K)).astype(np.float32)
+    a, bt = cuda(padded(A, lda)), cuda(padded(Bt, ldb))
+    ldc = N + 8
+    c = torch.full((M, ldc), 7.0, device="cuda")
+    mph_gemm_nt(M, N, K, a.data_ptr(), lda, bt.data_ptr(), ldb, c.data_ptr(), ldc, None,
+                torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    Cg = c.cpu().numpy()
+    assert np.all(Cg[:, N:] == 7.0)                               # nothing written past N
+    assert_gemm_close(Cg[:, :N], A, Bt.T, what=f"gemm_nt {M}x{N}x{K}")
+
+
+def test_gemm_nt_epilogue(P):
+    from paper_2512_01678_b200._lib import (EPI_BIAS, EPI_COLSUM, EPI_MASK, EPI_RELU, EPI_ROWSCALE, Epilogue,
+                                            mph_gemm_nt, mph_reduce_rows)
+    M, N, K = 1500, 48, 128
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    Bt = rng.standard_normal((N, K)).astype(np.float32)
+    rs = rng.random(M).astype(np.float32) + 0.1
+    b = rng.standard_normal(N).astype(np.float32)
+    msk = rng.standard_normal((M, N)).astype(np.float32)
+    a, bt, trs, tb, tm = cuda(A), cuda(Bt), cuda(rs), cuda(b), cuda(msk)
+    nt = (M + 127) // 128
+    cs = torch.zeros((nt, N), device="cuda")
+    e = Epilogue()
+    e.flags = EPI_BIAS | EPI_MASK | EPI_RELU | EPI_COLSUM | EPI_ROWSCALE
+    e.row_scale, e.bias, e.mask_src, e.ld_mask, e.mask_scale = trs.data_ptr(), tb.data_ptr(), tm.data_ptr(), N, 1.25
+    e.colsum_out = cs.data_ptr()
+    c = torch.zeros((M, N), device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    mph_gemm_nt(M, N, K, a.data_ptr(), K, bt.data_ptr(), K, c.data_ptr(), N, C.byref(e), s)
+    db = torch.zeros(N, device="cuda")
+    mph_reduce_rows(cs.data_ptr(), nt, N, N, db.data_ptr(), 0, s)
+    torch.cuda.synchronize()
+    acc = A.astype(np.float64) @ Bt.T.astype(np.float64)
+    pre = np.maximum(np.where(msk > 0, (acc + b) * 1.25, 0.0), 0.0)
+    bound = (np.abs(A.astype(np.float64)) @ np.abs(Bt.T.astype(np.float64)) + np.abs(b)) * 1.25
+    err = np.abs(c.cpu().numpy() - pre * rs[:, None])
+    assert float((err / (2e-3 * bound * rs[:, None])).max()) <= 1.0
+    err_db = np.abs(db.cpu().numpy() - pre.sum(0))
+    assert float((err_db / (2e-3 * bound.sum(0))).max()) <= 1.0
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 16, 100), (104, 256, 3001), (608, 128, 20000), (256, 48, 131072),
+                                   (500, 64, 19717), (1433, 16, 2708)])
+def test_gemm_tn(P, M, N, K):
+    from paper_2512_01678_b200._lib import mph_gemm_tn, mph_gemm_tn_workspace
+    rng = np.random.default_rng(M * N + K)
+    A = rng.standard_normal((K, M)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    lda, ldb = (M + 3) // 4 * 4, (N + 3) // 4 * 4
+    a, b = cuda(padded(A, lda)), cuda(padded(B, ldb))
+    ws_bytes = C.c_size_t()
+    mph_gemm_tn_workspace(M, N, K, C.byref(ws_bytes))
+    ws = torch.empty(max(1, ws_bytes.value // 4), device="cuda")
+    c = torch.zeros((M, N), device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    mph_gemm_tn(M, N, K, a.data_ptr(), lda, b.data_ptr(), ldb, c.data_ptr(), N, ws.data_ptr(), ws_bytes.value, s)
+    c2 = torch.zeros_like(c)
+    mph_gemm_tn(M, N, K, a.data_ptr(), lda, b.data_ptr(), ldb, c2.data_ptr(), N, ws.data_ptr(), ws_bytes.value, s)
+    torch.cuda.synchronize()
+    assert torch.equal(c, c2)                                    # deterministic split-K
+    assert_gemm_close(c.cpu().numpy(), A.T, B, what=f"gemm_tn {M}x{N}x{K}")
+
+
+# ------------------------------------------------------------------ a5 loss, a9 Adam, Xavier
+@pytest.mark.parametrize("N,C_,masked", [(1, 3, False), (5000, 41, False), (3001, 47, True), (777, 7, True)])
+def test_softmax_ce(P, N, C_, masked):
+    from paper_2512_01678_b200._lib import mph_softmax_ce, mph_softmax_ce_workspace
+    rng = np.random.default_rng(N)
+    ld = pad_width(C_)
+    Z = (rng.standard_normal((N, C_)) * 5).astype(np.float32)
+    y = rng.integers(0, C_, N).astype(np.int32)
+    mask = (rng.random(N) < 0.6).astype(np.uint8) if masked else None
+    if mask is not None:
+        mask[0] = 1
+    rs = rng.random(N).astype(np.float32) + 0.2
+    n_lab = int(mask.sum()) if masked else N
+    z, ty, trs = cuda(padded(Z, ld)), cuda(y), cuda(rs)
+    tm = cuda(mask) if masked else None
+    dz = torch.zeros((N, ld), device="cuda")
+    db = torch.zeros(C_, device="cuda")
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    wsb = C.c_size_t()
+    mph_softmax_ce_workspace(N, C_, C.byref(wsb))
+    ws = torch.empty(wsb.value // 4 + 4, device="cuda")
+    mph_softmax_ce(z.data_ptr(), N, C_, ld, ty.data_ptr(), tm.data_ptr() if masked else None, n_lab, trs.data_ptr(),
+                   dz.data_ptr(), ld, db.data_ptr(), loss.data_ptr(), ws.data_ptr(), wsb.value,
+                   torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref_loss, ref_dz = oracle.softmax_ce(Z, y, mask)
+    assert math.isclose(loss.item(), ref_loss, rel_tol=1e-5, abs_tol=1e-7)
+    got = dz.cpu().numpy()
+    assert np.all(got[:, C_:] == 0)
+    assert np.allclose(got[:, :C_], ref_dz * rs[:, None], rtol=1e-5, atol=1e-6 / n_lab)
+    assert np.allclose(db.cpu().numpy(), ref_dz.sum(0), rtol=1e-4, atol=1e-6)
+
+
+def test_adam_matches_oracle(P):
+    from paper_2512_01678_b200._lib import AdamCfg, mph_adam
+    rng = np.random.default_rng(0)
+    n = 100003
+    p0 = rng.standard_normal(n).astype(np.float32)
+    p, m, v = cuda(p0), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    rp, rm, rv = [p0.astype(np.float64)], [np.zeros(n)], [np.zeros(n)]
+    s = torch.cuda.current_stream().cuda_stream
+    cfg = AdamCfg(0.01, 0.9, 0.999, 1e-8)
+    for t in range(1, 6):
+        g = rng.standard_normal(n).astype(np.float32)
+        g[:10] = 0.0
+        mph_adam(p.data_ptr(), cuda(g).data_ptr(), m.data_ptr(), v.data_ptr(), n, C.byref(cfg), t, s)
+        oracle.adam_step(rp, [g.astype(np.float64)], rm, rv, t)
+    torch.cuda.synchronize()
+    got = p.cpu().numpy()
+    assert np.all(got[:10] == p0[:10])                           # zero gradient: no change
+    assert np.allclose(got, rp[0], rtol=0, atol=2e-6)
+
+
+@pytest.mark.parametrize("fi,fo,layer", [(1433, 16, 1), (128, 256, 2), (602, 128, 1), (256, 47, 3)])
+def test_xavier_bit_exact(P, fi, fo, layer):
+    from paper_2512_01678_b200._lib import mph_xavier_fill
+    seed = 42
+    ld = pad_width(fo)
+    W = torch.zeros((fi, ld), device="cuda")
+    mph_xavier_fill(W.data_ptr(), fi, fo, ld, seed, layer, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    dims = [1] * (layer - 1) + [fi, fo]
+    ref = oracle.xavier_init(dims, seed)[0][layer - 1]
+    got = W.cpu().numpy()
+    assert np.array_equal(got[:, :fo].view(np.uint32), ref.view(np.uint32))
+    assert np.all(got[:, fo:] == 0)
+
+
+# ------------------------------------------------------------------ sparse-feature kernels
+@pytest.mark.parametrize("name", ["cora", "pubmed"])
+def test_sparse_feature_kernels(P, name):
+    from paper_2512_01678_b200._lib import mph_sparse_xtg, mph_sparse_xw
+    w = make_workload(name)
+    X = w["X"]
+    N, F = X.shape
+    fo = w["cfg"].dims[1]
+    f = P.Features(cuda(X))
+    rng = np.random.default_rng(1)
+    W = rng.standard_normal((F, fo)).astype(np.float32)
+    rs = rng.random(N).astype(np.float32) + 0.5
+    G = rng.standard_normal((N, fo)).astype(np.float32)
+    tw, trs, tg = cuda(W), cuda(rs), cuda(G)
+    T = torch.zeros((N, fo), device="cuda")
+    dW = torch.zeros((F, fo), device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    mph_sparse_xw(f.h, tw.data_ptr(), fo, fo, trs.data_ptr(), T.data_ptr(), fo, s)
+    mph_sparse_xtg(f.h, tg.data_ptr(), fo, fo, dW.data_ptr(), fo, s)
+    torch.cuda.synchronize()
+    X64 = X.astype(np.float64)
+    ref_T = (X64 @ W) * rs[:, None]
+    bound_T = (np.abs(X64) @ np.abs(W)) * rs[:, None]
+    assert float((np.abs(T.cpu().numpy() - ref_T) / (1e-5 * bound_T + 1e-30)).max()) <= 1.0
+    ref_dW = X64.T @ G
+    bound_dW = np.abs(X64.T) @ np.abs(G)
+    assert float((np.abs(dW.cpu().numpy() - ref_dW) / (1e-5 * bound_dW + 1e-30)).max()) <= 1.0
