@@ -115,6 +115,8 @@ int mph_features_destroy(mph_features* f);
 #define MPH_EPI_MASK 8u      /* * (mask_src[r,c] > 0 ? mask_scale : 0)  (ReLU'/dropout mask)  */
 #define MPH_EPI_DROPOUT 16u  /* inverted dropout after ReLU, Philox4x32-10 (Q10)              */
 #define MPH_EPI_COLSUM 32u   /* per-CTA column sums of the value before ROWSCALE -> colsum_out */
+#define MPH_EPI_TF32 64u     /* round the stored value to TF32 (cvt.rna), for outputs that only feed
+                                tensor-core GEMMs: unbiased operand rounding (reading R2) */
 
 typedef struct {
   uint32_t flags;
@@ -289,7 +291,8 @@ int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream);
 int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* loss_d, void* stream);
 /* Borrowed views of activations for tests: kind 0 = layer input H_{l-1} (l=1 is X),
  * 1 = layer output Z_l (hidden: post-ReLU H_l; last: logits), 2 = G_l (backward SpMM out
- * or dZ_1 for an AF layer 1), 3 = aggregate-first Y_1. */
+ * or dZ_1 for an AF layer 1), 3 = aggregate-first Y_1, 4 = transform output T'_l = dinv ⊙ (H·W)
+ * (n_cols rows incl. ghosts), 5 = dZ'_l (dinv-prescaled gradient, n_cols rows; AF layer 1: dZ_1). */
 int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, const float** ptr_d, int32_t* rows_h,
                    int32_t* width_h, int32_t* ld_h);
 /* order_h[l-1] = 0 transform-first, 1 aggregate-first; mode_h = feature mode. */

@@ -72,7 +72,12 @@ def graph_build(src, dst, num_nodes: int) -> Graph:
     v = np.concatenate([dst[off], src[off]])
     diag = np.arange(n, dtype=np.int64)
     keys = np.concatenate([u * n + v, diag * n + diag])                  # G3: S ∪ I
-    keys = np.unique(keys)                                               # G2 dedup, G4 (u,v) order
+    keys = np.sort(keys)                                                 # G4 (u,v) order
+    if keys.size:                                                        # G2 dedup
+        keep = np.empty(keys.size, dtype=bool)
+        keep[0] = True
+        np.not_equal(keys[1:], keys[:-1], out=keep[1:])
+        keys = keys[keep]
     rows = keys // n
     cols = keys % n
     counts = np.bincount(rows, minlength=n).astype(np.int64)

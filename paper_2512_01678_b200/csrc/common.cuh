@@ -82,6 +82,16 @@ __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 __device__ __forceinline__ float4 f4_zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+// Round to the nearest TF32 value (ties away from zero), kept in an fp32 container: the
+// tensor cores then read it exactly instead of truncating the low 13 mantissa bits.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ float4 f4_tf32(float4 v) {
+  return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+}
 
 // Philox4x32-10 (Salmon et al., SC'11) — the dropout mask of reading Q10.
 struct PhiloxOut {

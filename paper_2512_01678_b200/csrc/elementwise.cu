@@ -174,44 +174,54 @@ int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int laye
   return launch_check("xavier");
 }
 
-// ------------------------------------------------------------------ transposes / row scale
-__global__ void k_transpose(const float* src, int rows, int cols, int ld_src, float* dst, int ld_dst) {
+// ------------------------------------------------------------------ weight copies / row scale
+// The tensor-core operand copies of W_l: dst_t = round_tf32(W^T) (K-major B of the forward
+// GEMM) and dst_r = round_tf32(W) (B of the dH GEMM).  The FP32 master copy stays in params.
+__global__ void k_weight_copies(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,
+                                int ld_r) {
   __shared__ float tile[32][33];
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
-    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[(int64_t)r * ld_src + c] : 0.0f;
+    const float v = (r < rows && c < cols) ? tf32_rna(src[(int64_t)r * ld_src + c]) : 0.0f;
+    tile[i][threadIdx.x] = v;
+    if (dst_r && r < rows && c < cols) dst_r[(int64_t)r * ld_r + c] = v;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int c = c0 + i, r = r0 + threadIdx.x;
-    if (c < cols && r < rows) dst[(int64_t)c * ld_dst + r] = tile[threadIdx.x][i];
+    if (c < cols && r < rows) dst_t[(int64_t)c * ld_t + r] = tile[threadIdx.x][i];
   }
 }
 
-int transpose_launch(const float* src, int rows, int cols, int ld_src, float* dst, int ld_dst, cudaStream_t s) {
+int weight_copies_launch(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,
+                         int ld_r, cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return MPH_OK;
   dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
-  k_transpose<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld_src, dst, ld_dst);
+  k_weight_copies<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld_src, dst_t, ld_t, dst_r, ld_r);
   count_launch();
-  return launch_check("transpose");
+  return launch_check("weight_copies");
 }
 
-__global__ void k_rowscale(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out) {
+// out[i][c] = in[i][c] * scale[i] (scale nullable), optionally rounded to TF32
+__global__ void k_rowscale(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out,
+                           int round) {
   const int64_t total = (int64_t)rows * w;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = t / w;
     const int c = (int)(t - i * w);
-    out[i * ld_out + c] = in[i * ld_in + c] * scale[i];
+    float v = in[i * ld_in + c];
+    if (scale) v *= scale[i];
+    out[i * ld_out + c] = round ? tf32_rna(v) : v;
   }
 }
 
-int rowscale_launch(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out,
+int rowscale_launch(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out, int round,
                     cudaStream_t s) {
   if (rows <= 0 || w <= 0) return MPH_OK;
   const int64_t total = (int64_t)rows * w;
   k_rowscale<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 32), 256, 0, s>>>(in, ld_in, scale, rows, w,
-                                                                                          out, ld_out);
+                                                                                          out, ld_out, round);
   count_launch();
   return launch_check("rowscale");
 }

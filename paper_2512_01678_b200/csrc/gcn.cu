@@ -44,6 +44,8 @@ struct mph_gcn {
   int L = 0;
   std::vector<Layer> layers;
   float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *wt = nullptr;
+  float* wr = nullptr;  // TF32-rounded copy of the W segments (B operand of the dH GEMM)
+  float* Xr = nullptr;  // TF32-rounded copy of X (A operand of a dense transform-first layer 1)
   int64_t n_params = 0, n_wt = 0;
   const int32_t* labels = nullptr;
   const uint8_t* mask = nullptr;
@@ -76,6 +78,8 @@ static void gcn_free(mph_gcn* m) {
   dev_free(m->m);
   dev_free(m->v);
   dev_free(m->wt);
+  dev_free(m->wr);
+  dev_free(m->Xr);
   dev_free(m->Xs);
   dev_free(m->ws);
   delete m;
@@ -83,7 +87,8 @@ static void gcn_free(mph_gcn* m) {
 
 static int refresh_wt(mph_gcn* m, cudaStream_t s) {
   for (auto& l : m->layers)
-    MPH_TRY(transpose_launch(m->params + l.off_w, l.pin, l.pout, l.pout, m->wt + l.off_wt, l.pin, s));
+    MPH_TRY(weight_copies_launch(m->params + l.off_w, l.pin, l.pout, l.pout, m->wt + l.off_wt, l.pin, m->wr + l.off_w,
+                                 l.pout, s));
   return MPH_OK;
 }
 
@@ -123,7 +128,8 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
   const int lnum = li + 1;
   const bool hidden = lnum < m->L;
   mph_epilogue eo = epi_none();
-  eo.flags = MPH_EPI_BIAS | (hidden ? MPH_EPI_RELU : 0u);
+  // hidden outputs only feed tensor-core GEMMs (and the ReLU-mask sign test): store them as TF32
+  eo.flags = MPH_EPI_BIAS | (hidden ? (MPH_EPI_RELU | MPH_EPI_TF32) : 0u);
   eo.bias = m->params + l.off_b;
   if (hidden && m->dropout_p > 0.0f) {
     eo.flags |= MPH_EPI_DROPOUT;
@@ -139,7 +145,7 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
       prof::Scope sc(MPH_PROF_SPARSE, s, 8.0 * m->f->nnz + 4.0 * g->n_rows * l.pout, 2.0 * m->f->nnz * l.pout);
       MPH_TRY(sparse_xw_launch(m->f, m->params + l.off_w, l.pout, l.pout, g->dinv, l.T, l.pout, s));
     } else {
-      const float* A = li == 0 ? m->f->X : m->layers[li - 1].out;
+      const float* A = li == 0 ? m->Xr : m->layers[li - 1].out;
       const int lda = li == 0 ? m->f->P : m->layers[li - 1].pout;
       mph_epilogue et = epi_none();
       et.flags = MPH_EPI_ROWSCALE;
@@ -153,6 +159,7 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
   } else {
     // aggregate-first layer 1: Y = Â·X (on dinv ⊙ X), Z = Y·W + b with the epilogue fused in the GEMM
     mph_epilogue en = epi_none();
+    en.flags = MPH_EPI_TF32;  // Y only feeds the GEMMs
     MPH_TRY(spmm_p(g, m->Xs, l.pin, l.pin, l.Y, l.pin, &en, s));
     MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, l.Y, l.pin, m->wt + l.off_wt, l.pin, l.out, l.pout, &eo, s));
   }
@@ -184,13 +191,14 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
   const mph_graph* g = m->g;
   for (int li = m->L - 1; li >= 0; --li) {
     Layer& l = m->layers[li];
-    const float* Hin = li == 0 ? (m->f->mode == 0 ? m->f->X : nullptr) : m->layers[li - 1].out;
+    const float* Hin = li == 0 ? m->Xr : m->layers[li - 1].out;
     const int ld_in = li == 0 ? m->f->P : m->layers[li - 1].pout;
     const float* Gsrc;  // gradient w.r.t. the transform output (TF) or Z (AF)
     if (l.order == 0) {
       // a6: G = Â·dZ (Â symmetric, same kernel as forward)
       if (m->world > 1) MPH_TRY(mph_halo_exchange(g, m->comm, l.dZ, l.pout, l.pout, s));
       mph_epilogue en = epi_none();
+      en.flags = MPH_EPI_TF32;  // G only feeds the dW and dH GEMMs
       MPH_TRY(spmm_p(g, l.dZ, l.pout, l.pout, l.G, l.pout, &en, s));
       Gsrc = l.G;
       // a7: dW = H^T·G  (sparse layer 1: X_csc^T·G)
@@ -212,13 +220,14 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       // pre-scale for the next backward SpMM (TF) — all in one GEMM epilogue.
       Layer& pl = m->layers[li - 1];
       mph_epilogue ed = epi_none();
-      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM | (pl.order == 0 ? MPH_EPI_ROWSCALE : 0u);
+      // TF: dZ' feeds the FP32 SpMM (keep FP32); AF: dZ_1 feeds only the dW GEMM (TF32)
+      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM | (pl.order == 0 ? MPH_EPI_ROWSCALE : MPH_EPI_TF32);
       ed.mask_src = pl.out;
       ed.ld_mask = pl.pout;
       ed.mask_scale = dropout_scale(m->dropout_p);
       ed.colsum_out = pl.colsum;
       ed.row_scale = g->dinv;
-      MPH_TRY(gemm_nt_p(g->n_rows, pl.pout, l.pout, Gsrc, l.pout, m->params + l.off_w, l.pout, pl.dZ, pl.pout, &ed,
+      MPH_TRY(gemm_nt_p(g->n_rows, pl.pout, l.pout, Gsrc, l.pout, m->wr + l.off_w, l.pout, pl.dZ, pl.pout, &ed,
                         s));
       MPH_TRY(reduce_rows_launch(pl.colsum, (int)ceil_div(g->n_rows, 128), pl.pout, pl.pout, m->grads + pl.off_b, 0, s));
     }
@@ -279,7 +288,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     return code;
   };
   if ((rc = dev_alloc(&m->params, off)) || (rc = dev_alloc(&m->grads, off)) || (rc = dev_alloc(&m->m, off)) ||
-      (rc = dev_alloc(&m->v, off)) || (rc = dev_alloc(&m->wt, offt)))
+      (rc = dev_alloc(&m->v, off)) || (rc = dev_alloc(&m->wt, offt)) || (rc = dev_alloc(&m->wr, off)))
     return bail(rc);
   size_t ws = softmax_ce_ws_bytes(g->n_rows, m->layers.back().fout);
   const int64_t nr = g->n_rows, nc = g->n_cols;
@@ -311,6 +320,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   if (e == cudaSuccess) e = cudaMemsetAsync(m->m, 0, off * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(m->v, 0, off * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(m->wt, 0, offt * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->wr, 0, off * 4, s);
   if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create memset: %s", cudaGetErrorString(e)));
   if (m->layers[0].order == 1) {
     // X is constant input data: its dinv pre-scale (and, distributed, its ghost rows) are set up once.
@@ -318,8 +328,13 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     if ((rc = dev_alloc(&m->Xs, (size_t)nc * l.pin))) return bail(rc);
     e = cudaMemsetAsync(m->Xs, 0, (size_t)nc * l.pin * 4, s);
     if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "memset: %s", cudaGetErrorString(e)));
-    if ((rc = rowscale_launch(f->X, f->P, g->dinv, (int)nr, l.pin, m->Xs, l.pin, s))) return bail(rc);
+    if ((rc = rowscale_launch(f->X, f->P, g->dinv, (int)nr, l.pin, m->Xs, l.pin, 0, s))) return bail(rc);
     if (world > 1 && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
+  }
+  if (m->layers[0].order == 0 && f->mode == 0) {
+    // TF32-rounded copy of X: the A operand of the layer-1 transform and of its dW GEMM
+    if ((rc = dev_alloc(&m->Xr, (size_t)nr * f->P))) return bail(rc);
+    if ((rc = rowscale_launch(f->X, f->P, nullptr, (int)nr, f->P, m->Xr, f->P, 1, s))) return bail(rc);
   }
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create: %s", cudaGetErrorString(e)));
@@ -376,8 +391,10 @@ extern "C" int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_
                                  cudaMemcpyHostToDevice, s));
   if (m->layers[0].order == 1) {
     const Layer& l = m->layers[0];
-    MPH_TRY(rowscale_launch(f->X, f->P, m->g->dinv, m->g->n_rows, l.pin, m->Xs, l.pin, s));
+    MPH_TRY(rowscale_launch(f->X, f->P, m->g->dinv, m->g->n_rows, l.pin, m->Xs, l.pin, 0, s));
     if (m->world > 1) MPH_TRY(mph_halo_exchange(m->g, m->comm, m->Xs, l.pin, l.pin, s));
+  } else {
+    MPH_TRY(rowscale_launch(f->X, f->P, nullptr, m->g->n_rows, f->P, m->Xr, f->P, 1, s));
   }
   return MPH_OK;
 }
@@ -458,6 +475,18 @@ extern "C" int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, con
       p = l.Y;
       width = l.fin;
       ld = l.pin;
+      break;
+    case 4:
+      p = l.T;
+      width = l.fout;
+      ld = l.pout;
+      rows = m->g->n_cols;
+      break;
+    case 5:
+      p = l.dZ;
+      width = l.fout;
+      ld = l.pout;
+      rows = l.order == 0 ? m->g->n_cols : m->g->n_rows;
       break;
     default:
       return fail(MPH_EINVAL, "unknown tensor kind %d", kind);

@@ -172,16 +172,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) colsum_sm[q * p.BN + c0 + i] = t;
         }
       }
+      if (e.flags & MPH_EPI_TF32) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = tf32_rna(v[i] * rs);
+      } else if (e.flags & MPH_EPI_ROWSCALE) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= rs;
+      }
       if (row_ok) {
         if (c0 + 16 <= p.N && (p.ldc & 3) == 0) {
           float4* dst = reinterpret_cast<float4*>(crow + c0);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_float4(v[4 * i] * rs, v[4 * i + 1] * rs, v[4 * i + 2] * rs, v[4 * i + 3] * rs);
+          for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (c0 + i < p.N) crow[c0 + i] = v[i] * rs;
+            if (c0 + i < p.N) crow[c0 + i] = v[i];
         }
       }
     }
@@ -266,9 +272,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t a_base = tc::smem_u32(sA + (size_t)s * a_bytes);
         const uint32_t b_base = tc::smem_u32(sB + (size_t)s * b_bytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {  // 8 node rows = one 1024 B swizzle atom per chunk
-          const uint64_t da = tc::smem_desc_sw128(a_base + k * 1024, kChunk, 1024);
-          const uint64_t db = tc::smem_desc_sw128(b_base + k * 1024, kChunk, 1024);
+        for (int k = 0; k < kBK / 8; ++k) {  // 8 node rows = two 512 B SW128_32B atoms per chunk
+          const uint64_t da = tc::smem_desc_sw128(a_base + k * 1024, kChunk, 512, 1);
+          const uint64_t db = tc::smem_desc_sw128(b_base + k * 1024, kChunk, 512, 1);
           tc::mma_tf32(tmem, da, db, p.idesc, (i | k) != 0 ? 1u : 0u);
         }
         tc::mma_commit(&empty[s]);
@@ -337,7 +343,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 int make_tmap(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-              uint32_t box_outer) {
+              uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(MPH_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no device)");
   cuuint64_t dims[2] = {inner, outer};
@@ -345,7 +351,7 @@ int make_tmap(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer,
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(MPH_ECUDA, "cuTensorMapEncodeTiled failed (%d): inner=%llu outer=%llu ld=%llu box=%ux%u", (int)r,
@@ -451,8 +457,10 @@ int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B,
   p.idesc = tc::idesc_tf32(kBM, BN, 1, 1);
   p.tmem_cols = tmem_cols_for(BN);
   CUtensorMap ta, tb;
-  MPH_TRY(make_tmap(&ta, A, (uint64_t)M, (uint64_t)std::max(K, 1), (uint64_t)lda, 32, kBK));
-  MPH_TRY(make_tmap(&tb, B, (uint64_t)N, (uint64_t)std::max(K, 1), (uint64_t)ldb, 32, kBK));
+  MPH_TRY(make_tmap(&ta, A, (uint64_t)M, (uint64_t)std::max(K, 1), (uint64_t)lda, 32, kBK,
+                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  MPH_TRY(make_tmap(&tb, B, (uint64_t)N, (uint64_t)std::max(K, 1), (uint64_t)ldb, 32, kBK,
+                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (2 * p.stages + 1) * 8 + 16;
   static size_t configured = 0;
   if (smem > configured) {

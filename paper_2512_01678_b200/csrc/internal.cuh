@@ -64,13 +64,14 @@ int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* label
                       cudaStream_t s);
 int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s);
 int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int layer, cudaStream_t s);
-// dst[j*ld_dst + i] = src[i*ld_src + j] for i < rows, j < cols  (weight transposes)
-int transpose_launch(const float* src, int rows, int cols, int ld_src, float* dst, int ld_dst, cudaStream_t s);
+// dst_t[j*ld_t + i] = tf32(src[i*ld_src + j]), dst_r[i*ld_r + j] = tf32(src[i*ld_src + j]) (dst_r nullable)
+int weight_copies_launch(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,
+                         int ld_r, cudaStream_t s);
 int sparse_xw_launch(const mph_features* f, const float* W, int F_out, int ldw, const float* row_scale, float* T,
                      int ldt, cudaStream_t s);
 int sparse_xtg_launch(const mph_features* f, const float* G, int F_out, int ldg, float* dW, int lddw, cudaStream_t s);
-// out[i][c] = in[i][c] * scale[i] for c < w (padded columns copied as zero)
-int rowscale_launch(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out,
+// out[i][c] = in[i][c] * scale[i] (scale nullable) for c < w, optionally rounded to TF32
+int rowscale_launch(const float* in, int ld_in, const float* scale, int rows, int w, float* out, int ld_out, int round,
                     cudaStream_t s);
 
 }  // namespace mph

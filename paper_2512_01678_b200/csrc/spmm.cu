@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm(SpmmArgs a) {
         if (sub + j * LPR < a.nv4) orow[sub + j * LPR] = acc[j];
       continue;
     }
+    const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
     const float du = a.dinv[row];
     const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[row] : 1.0f;
 #pragma unroll
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(256, 2) k_spmm(SpmmArgs a) {
         v.z *= rs;
         v.w *= rs;
       }
-      orow[c4] = v;
+      orow[c4] = to_tf32 ? f4_tf32(v) : v;
     }
   }
 }
@@ -171,7 +172,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(MPH_EINVAL, "spmm: operands must be 16-byte aligned");
   if (part != -1 && !g->local) return fail(MPH_EINVAL, "spmm: row parts need a localized graph");
-  const uint32_t allowed = MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE;
+  const uint32_t allowed = MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE | MPH_EPI_TF32;
   if (epi && (epi->flags & ~allowed)) return fail(MPH_EINVAL, "spmm: unsupported epilogue flags 0x%x", epi->flags);
   if (epi && (epi->flags & MPH_EPI_BIAS) && (!epi->bias || (reinterpret_cast<uintptr_t>(epi->bias) & 15)))
     return fail(MPH_EINVAL, "spmm: bias must be non-null and 16-byte aligned");

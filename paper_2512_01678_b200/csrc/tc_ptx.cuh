@@ -97,14 +97,17 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, float* v) {
 }
 
 // ---------------------------------------------------------------- descriptors
-// Shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), descriptor version 1 (sm_100).
-__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// Shared-memory matrix descriptor, descriptor version 1 (sm_100).  layout: 2 = SWIZZLE_128B
+// (16 B granules, 8-row atom; K-major operands), 1 = SWIZZLE_128B_BASE32B (32 B granules,
+// 4-row atom; the only smem layout tcgen05 accepts for MN-major tf32 operands).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                                    uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;  // version
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 // Instruction descriptor: kind::tf32, FP32 accumulate, M x N, operand majors (0 K-major, 1 MN-major).

@@ -92,7 +92,12 @@ def test_first_epoch_gradients_and_layers_arxiv(P):
     # layer 1 aggregate-first: Y = Â·X  (FP32 aggregation tolerance)
     Y = m.tensor(3, 1).cpu().numpy()
     X64 = w["X"].astype(np.float64)
-    assert_agg_close(Y[:, :128], oracle.aggregate(ref_g, X64), agg_bound(ref_g, X64), what="arxiv Y1")
+    # Y is stored TF32-rounded (it only feeds GEMMs, reading R2): FP32 aggregation bound + half a TF32 ulp
+    Yref = oracle.aggregate(ref_g, X64)
+    err = np.abs(Y[:, :128] - Yref)
+    lim = 1e-5 * agg_bound(ref_g, X64) + 2.0 ** -11 * np.abs(Yref)
+    assert float((err / lim).max()) <= 1.0, "arxiv Y1"
+    assert np.array_equal(Y.view(np.uint32) & 0x1FFF, np.zeros_like(Y.view(np.uint32)))  # TF32 values
     # layer 1 transform on the GPU's own Y (per-kernel isolation): H1 = relu(Y·W1 + b1)
     (W1, b1), _, _ = m.params()
     H1 = m.tensor(1, 1).cpu().numpy()
@@ -139,7 +144,11 @@ def test_order_policy_equivalence(P):
     dims = (16, 64, 4)
     a = _gpu_losses(_gpu_model(P, w, dims, order_policy=0)[2], 5)
     b = _gpu_losses(_gpu_model(P, w, dims, order_policy=1)[2], 5)
-    _check_traj(a, b, tol=1e-4)
+    _check_traj(a, b, tol=1e-3)      # different TF32 operand roundings: the loss tolerance applies
+    g = oracle.graph_build(w["src"], w["dst"], 3000)
+    ref, _ = oracle.train(g, w["X"], w["y"], dims, epochs=5, seed=42)
+    _check_traj(a, ref)
+    _check_traj(b, ref)
 
 
 def test_training_is_deterministic(P):
