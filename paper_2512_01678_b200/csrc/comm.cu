@@ -63,35 +63,53 @@ extern "C" int mph_comm_destroy(mph_comm* c) {
   return MPH_OK;
 }
 
-extern "C" int mph_halo_exchange(const mph_graph* gc, mph_comm* c, float* buf_d, int32_t w, int32_t ld, void* stream) {
-  if (!gc || !c || !buf_d) return fail(MPH_EINVAL, "halo_exchange: null argument");
-  if (!gc->local) return fail(MPH_EINVAL, "halo_exchange: graph is not localized");
-  if (gc->world != c->world || gc->rank != c->rank) return fail(MPH_EINVAL, "halo_exchange: graph/comm rank mismatch");
-  if (w <= 0 || w % 4 || ld != w) return fail(MPH_EINVAL, "halo_exchange: needs ld == w, w % 4 == 0");
+namespace mph {
+
+int halo_reserve(const mph_graph* gc, int w) {
   mph_graph* g = const_cast<mph_graph*>(gc);
-  cudaStream_t s = (cudaStream_t)stream;
   const size_t need = (size_t)g->n_send * w;
-  if (need > g->send_cap) {
-    dev_free(g->send_buf);
-    g->send_buf = nullptr;
-    g->send_cap = 0;
-    MPH_TRY(dev_alloc(&g->send_buf, need));
-    g->send_cap = need;
-  }
-  MPH_TRY(pack_rows(g->send_ids, g->n_send, buf_d, ld, w, g->send_buf, s));
+  if (need <= g->send_cap) return MPH_OK;
+  dev_free(g->send_buf);
+  g->send_buf = nullptr;
+  g->send_cap = 0;
+  MPH_TRY(dev_alloc(&g->send_buf, need));
+  g->send_cap = need;
+  return MPH_OK;
+}
+
+// K-b7: gather the owned boundary rows of every peer's send list into the send buffer.
+int halo_pack(const mph_graph* g, const float* buf, int w, int ld, cudaStream_t s) {
+  MPH_TRY(halo_reserve(g, w));
+  return pack_rows(g->send_ids, g->n_send, buf, ld, w, g->send_buf, s);
+}
+
+// One grouped ncclSend/ncclRecv per peer; receives land in the ghost rows [n_rows, n_cols).
+int halo_sendrecv(const mph_graph* g, mph_comm* c, float* buf, int w, int ld, cudaStream_t s) {
   ncclResult_t r = ncclGroupStart();
   for (int q = 0; q < g->world && r == ncclSuccess; ++q) {
     if (q == g->rank) continue;
     const int64_t ns = g->send_offset[q + 1] - g->send_offset[q];
     if (ns > 0) r = ncclSend(g->send_buf + g->send_offset[q] * w, (size_t)ns * w, ncclFloat, q, c->nccl, s);
     if (r == ncclSuccess && g->n_recv[q] > 0)
-      r = ncclRecv(buf_d + ((int64_t)g->n_rows + g->recv_offset[q]) * ld, (size_t)g->n_recv[q] * w, ncclFloat, q,
+      r = ncclRecv(buf + ((int64_t)g->n_rows + g->recv_offset[q]) * ld, (size_t)g->n_recv[q] * w, ncclFloat, q,
                    c->nccl, s);
   }
   ncclResult_t r2 = ncclGroupEnd();
   if (r != ncclSuccess) return nccl_fail(r, "halo send/recv");
   if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
   return MPH_OK;
+}
+
+}  // namespace mph
+
+extern "C" int mph_halo_exchange(const mph_graph* gc, mph_comm* c, float* buf_d, int32_t w, int32_t ld, void* stream) {
+  if (!gc || !c || !buf_d) return fail(MPH_EINVAL, "halo_exchange: null argument");
+  if (!gc->local) return fail(MPH_EINVAL, "halo_exchange: graph is not localized");
+  if (gc->world != c->world || gc->rank != c->rank) return fail(MPH_EINVAL, "halo_exchange: graph/comm rank mismatch");
+  if (w <= 0 || w % 4 || ld != w) return fail(MPH_EINVAL, "halo_exchange: needs ld == w, w % 4 == 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  MPH_TRY(halo_pack(gc, buf_d, w, ld, s));
+  return halo_sendrecv(gc, c, buf_d, w, ld, s);
 }
 
 extern "C" int mph_allreduce_sum(mph_comm* c, void* buf_d, int64_t n, int32_t is_double, void* stream) {

@@ -10,6 +10,7 @@
 //   dZ_l    n_cols x P_l   dinv-prescaled loss/input gradient (halo target)
 //   G_l     n_rows x P_l   backward aggregation Â·dZ_l
 //   Y_1     n_rows x P_0   aggregate-first input Â·X (only when layer 1 is AF)
+#include <algorithm>
 #include <vector>
 
 #include "internal.cuh"
@@ -57,6 +58,9 @@ struct mph_gcn {
   uint64_t dropout_seed = 0;
   int epoch = 0;
   bool fwd_done = false, loss_done = false;
+  // P > 1: NCCL runs on its own stream, ordered against the compute stream by events
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_grad = nullptr, ev_comm_done = nullptr, ev_loss = nullptr;
 };
 
 namespace mph {
@@ -82,6 +86,9 @@ static void gcn_free(mph_gcn* m) {
   dev_free(m->Xr);
   dev_free(m->Xs);
   dev_free(m->ws);
+  for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss})
+    if (e) cudaEventDestroy(e);
+  if (m->cs) cudaStreamDestroy(m->cs);
   delete m;
 }
 
@@ -94,12 +101,46 @@ static int refresh_wt(mph_gcn* m, cudaStream_t s) {
 
 // SURVEY §8(d) d.3 algorithmic bytes: per edge 4 B col_idx + 4·w B gathered row (no reuse),
 // per row 8 B row_ptr + 4 B dinv + 4·w B written.
+static double spmm_bytes(const mph_graph* g, int w) {
+  const double rows = g->n_rows, nnz = (double)g->nnz;
+  return 8.0 * (rows + 1) + 4.0 * nnz + 4.0 * rows + 4.0 * nnz * w + 4.0 * rows * w;
+}
 static int spmm_p(const mph_graph* g, const float* in, int w, int ld_in, float* out, int ld_out, const mph_epilogue* e,
                   cudaStream_t s) {
-  const double rows = g->n_rows, nnz = (double)g->nnz;
-  prof::Scope sc(MPH_PROF_SPMM, s, 8.0 * (rows + 1) + 4.0 * nnz + 4.0 * rows + 4.0 * nnz * w + 4.0 * rows * w,
-                 2.0 * nnz * w);
+  prof::Scope sc(MPH_PROF_SPMM, s, spmm_bytes(g, w), 2.0 * (double)g->nnz * w);
   return spmm_launch(g, -1, in, w, ld_in, out, ld_out, e, s);
+}
+
+// a10 + a3/a6: aggregation whose input's ghost rows come from their owners.  With P > 1 the
+// pack runs on the compute stream, the grouped send/recv on the comm stream, and the
+// local-edge part of the SpMM overlaps the transfer; the ghost-edge part and the fused
+// epilogue run once the halo has landed (overlap P:765).
+static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogue* e, cudaStream_t s) {
+  const mph_graph* g = m->g;
+  if (m->world == 1) return spmm_p(g, in, w, w, out, w, e, s);
+  MPH_TRY(halo_pack(g, in, w, w, s));
+  MPH_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
+  MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_pack, 0));
+  {
+    prof::Scope sc(MPH_PROF_HALO, m->cs, 4.0 * (double)(g->n_cols - g->n_rows) * w, 0.0);
+    MPH_TRY(halo_sendrecv(g, m->comm, in, w, w, m->cs));
+  }
+  MPH_CUDA_TRY(cudaEventRecord(m->ev_halo, m->cs));
+  prof::Scope sc(MPH_PROF_SPMM, s, spmm_bytes(g, w), 2.0 * (double)g->nnz * w);
+  MPH_TRY(spmm_launch(g, 0, in, w, w, out, w, nullptr, s));
+  MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_halo, 0));
+  return spmm_launch(g, 1, in, w, w, out, w, e, s);
+}
+
+// a11: all-reduce one layer's [dW_l | b_l] gradient segment on the comm stream as soon as it is
+// complete, overlapping the rest of the backward pass (P:525-532 pipelined backward).
+static int grad_allreduce_async(mph_gcn* m, int li, cudaStream_t s) {
+  if (m->world == 1) return MPH_OK;
+  const int64_t a = m->layers[li].off_w;
+  const int64_t b = li + 1 < m->L ? m->layers[li + 1].off_w : m->n_params;
+  MPH_CUDA_TRY(cudaEventRecord(m->ev_grad, s));
+  MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_grad, 0));
+  return mph_allreduce_sum(m->comm, m->grads + a, b - a, 0, m->cs);
 }
 static int gemm_nt_p(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
                      const mph_epilogue* e, cudaStream_t s) {
@@ -152,10 +193,8 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
       et.row_scale = g->dinv;
       MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, A, lda, m->wt + l.off_wt, l.pin, l.T, l.pout, &et, s));
     }
-    // a10: ghost rows of T' from their owners
-    if (m->world > 1) MPH_TRY(mph_halo_exchange(g, m->comm, l.T, l.pout, l.pout, s));
-    // a3: Z = Â·T + b, ReLU (dropout) fused
-    MPH_TRY(spmm_p(g, l.T, l.pout, l.pout, l.out, l.pout, &eo, s));
+    // a10 + a3: ghost rows of T' from their owners; Z = Â·T + b, ReLU (dropout) fused
+    MPH_TRY(spmm_halo(m, l.T, l.pout, l.out, &eo, s));
   } else {
     // aggregate-first layer 1: Y = Â·X (on dinv ⊙ X), Z = Y·W + b with the epilogue fused in the GEMM
     mph_epilogue en = epi_none();
@@ -195,11 +234,10 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
     const int ld_in = li == 0 ? m->f->P : m->layers[li - 1].pout;
     const float* Gsrc;  // gradient w.r.t. the transform output (TF) or Z (AF)
     if (l.order == 0) {
-      // a6: G = Â·dZ (Â symmetric, same kernel as forward)
-      if (m->world > 1) MPH_TRY(mph_halo_exchange(g, m->comm, l.dZ, l.pout, l.pout, s));
+      // a10 + a6: G = Â·dZ (Â symmetric, same kernel as forward)
       mph_epilogue en = epi_none();
       en.flags = MPH_EPI_TF32;  // G only feeds the dW and dH GEMMs
-      MPH_TRY(spmm_p(g, l.dZ, l.pout, l.pout, l.G, l.pout, &en, s));
+      MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, s));
       Gsrc = l.G;
       // a7: dW = H^T·G  (sparse layer 1: X_csc^T·G)
       if (li == 0 && m->f->mode == 1) {
@@ -215,6 +253,9 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, l.Y, l.pin, l.dZ, l.pout, m->grads + l.off_w, l.pout, m->ws,
                         m->ws_bytes, s));
     }
+    // [dW_l | db_l] complete (db_l came from the loss or the layer above): reduce it across ranks
+    // while this layer's dH and the layers below proceed (a11)
+    MPH_TRY(grad_allreduce_async(m, li, s));
     if (li > 0) {
       // a8: dZ_{l-1} = (G·W^T) ⊙ 1[H_{l-1} > 0] (/(1-p)), db_{l-1} as column sums, then the dinv
       // pre-scale for the next backward SpMM (TF) — all in one GEMM epilogue.
@@ -231,6 +272,10 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
                         s));
       MPH_TRY(reduce_rows_launch(pl.colsum, (int)ceil_div(g->n_rows, 128), pl.pout, pl.pout, m->grads + pl.off_b, 0, s));
     }
+  }
+  if (m->world > 1) {  // Adam needs every summed gradient segment
+    MPH_CUDA_TRY(cudaEventRecord(m->ev_comm_done, m->cs));
+    MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm_done, 0));
   }
   m->fwd_done = false;
   m->loss_done = false;
@@ -331,6 +376,15 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     if ((rc = rowscale_launch(f->X, f->P, g->dinv, (int)nr, l.pin, m->Xs, l.pin, 0, s))) return bail(rc);
     if (world > 1 && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
   }
+  if (world > 1) {
+    e = cudaStreamCreateWithFlags(&m->cs, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&m->ev_pack, &m->ev_halo, &m->ev_grad, &m->ev_comm_done, &m->ev_loss})
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create streams: %s", cudaGetErrorString(e)));
+    int wmax = m->layers[0].pin;
+    for (const auto& l : m->layers) wmax = std::max(wmax, l.pout);
+    if ((rc = halo_reserve(g, wmax))) return bail(rc);  // no reallocation while sends are in flight
+  }
   if (m->layers[0].order == 0 && f->mode == 0) {
     // TF32-rounded copy of X: the A operand of the layer-1 transform and of its dW GEMM
     if ((rc = dev_alloc(&m->Xr, (size_t)nr * f->P))) return bail(rc);
@@ -387,8 +441,11 @@ extern "C" int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_
   if (m->f->mode != 0) return fail(MPH_ENOTSUP, "upload_features: sparse-mode features are fixed at creation");
   cudaStream_t s = (cudaStream_t)stream;
   const mph_features* f = m->f;
-  MPH_CUDA_TRY(cudaMemcpy2DAsync(f->X, (size_t)f->P * 4, X_h, (size_t)ld_h * 4, (size_t)f->F * 4, (size_t)f->N,
-                                 cudaMemcpyHostToDevice, s));
+  if (ld_h == f->P)  // host rows already padded: one contiguous copy (the padding must be zero)
+    MPH_CUDA_TRY(cudaMemcpyAsync(f->X, X_h, (size_t)f->N * f->P * 4, cudaMemcpyHostToDevice, s));
+  else
+    MPH_CUDA_TRY(cudaMemcpy2DAsync(f->X, (size_t)f->P * 4, X_h, (size_t)ld_h * 4, (size_t)f->F * 4, (size_t)f->N,
+                                   cudaMemcpyHostToDevice, s));
   if (m->layers[0].order == 1) {
     const Layer& l = m->layers[0];
     MPH_TRY(rowscale_launch(f->X, f->P, m->g->dinv, m->g->n_rows, l.pin, m->Xs, l.pin, 0, s));
@@ -414,17 +471,22 @@ extern "C" int mph_gcn_forward(mph_gcn* m, int32_t epoch, void* stream) {
 
 extern "C" int mph_gcn_loss(mph_gcn* m, double* loss_d, void* stream) {
   if (!m || !loss_d) return fail(MPH_EINVAL, "gcn_loss arguments");
-  MPH_TRY(do_loss(m, loss_d, (cudaStream_t)stream));
-  if (m->world > 1) MPH_TRY(mph_allreduce_sum(m->comm, loss_d, 1, 1, stream));
+  cudaStream_t s = (cudaStream_t)stream;
+  MPH_TRY(do_loss(m, loss_d, s));
+  if (m->world > 1) {  // global loss = sum of per-rank partial sums / global N_lab
+    MPH_CUDA_TRY(cudaEventRecord(m->ev_loss, s));
+    MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_loss, 0));
+    MPH_TRY(mph_allreduce_sum(m->comm, loss_d, 1, 1, m->cs));
+    MPH_CUDA_TRY(cudaEventRecord(m->ev_loss, m->cs));
+    MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_loss, 0));
+  }
   return MPH_OK;
 }
 
 extern "C" int mph_gcn_backward(mph_gcn* m, void* stream) {
   if (!m) return fail(MPH_EINVAL, "null model");
-  MPH_TRY(do_backward(m, (cudaStream_t)stream));
-  // a11: replicated parameters need the summed gradient
-  if (m->world > 1) MPH_TRY(mph_allreduce_sum(m->comm, m->grads, m->n_params, 0, stream));
-  return MPH_OK;
+  // a11 happens inside: per-layer gradient all-reduce pipelined on the comm stream
+  return do_backward(m, (cudaStream_t)stream);
 }
 
 extern "C" int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream) {

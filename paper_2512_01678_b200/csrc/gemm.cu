@@ -309,11 +309,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
 }
 
-__global__ void k_reduce_rows(const float* in, int rows, int cols, int ld, float* out, int accumulate) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += gridDim.x * blockDim.x) {
-    float s = accumulate ? out[c] : 0.0f;
-    for (int r = 0; r < rows; ++r) s += in[(int64_t)r * ld + c];
-    out[c] = s;
+// Column sums in a fixed order: 8 row-groups per 32-column chunk (group g sums rows g, g+8, ...),
+// then the 8 group sums in order.  Deterministic for a given shape.
+__global__ void __launch_bounds__(256) k_reduce_rows(const float* in, int rows, int cols, int ld, float* out,
+                                                     int accumulate) {
+  __shared__ float part[8][33];
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int grp = threadIdx.x >> 5;
+  float s = 0.0f;
+  if (c < cols) {
+#pragma unroll 4
+    for (int r = grp; r < rows; r += 8) s += in[(int64_t)r * ld + c];
+  }
+  part[grp][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (grp == 0 && c < cols) {
+    float t = accumulate ? out[c] : 0.0f;
+#pragma unroll
+    for (int g2 = 0; g2 < 8; ++g2) t += part[g2][threadIdx.x];
+    out[c] = t;
   }
 }
 
@@ -479,7 +493,7 @@ int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B,
 
 int reduce_rows_launch(const float* in, int rows, int cols, int ld, float* out, int accumulate, cudaStream_t s) {
   if (!in || !out || rows < 0 || cols <= 0 || ld < cols) return fail(MPH_EINVAL, "reduce_rows: bad arguments");
-  k_reduce_rows<<<(unsigned)ceil_div(cols, 128), 128, 0, s>>>(in, rows, cols, ld, out, accumulate);
+  k_reduce_rows<<<(unsigned)ceil_div(cols, 32), 256, 0, s>>>(in, rows, cols, ld, out, accumulate);
   count_launch();
   return launch_check("reduce_rows");
 }

@@ -48,6 +48,10 @@ int launch_dinv(const int32_t* deg, float* dinv, int64_t n, cudaStream_t s);
 // 1 ghost columns accumulated onto out + epilogue.
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
                 const mph_epilogue* epi, cudaStream_t s);
+// Halo exchange in two halves (comm.cu) so the model can overlap them with the local-edge SpMM.
+int halo_reserve(const mph_graph* g, int w);
+int halo_pack(const mph_graph* g, const float* buf, int w, int ld, cudaStream_t s);
+int halo_sendrecv(const mph_graph* g, mph_comm* c, float* buf, int w, int ld, cudaStream_t s);
 // Halo pack (spmm.cu): send_buf[j] = buf[send_ids[j]] for the whole send list.
 int pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int w, float* out, cudaStream_t s);
 
