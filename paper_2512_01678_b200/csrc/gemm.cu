@@ -44,14 +44,6 @@ struct EpiG {
   int64_t row0;
 };
 
-struct NtParams {
-  int M, N, K, BN, stages, num_kb;
-  float* C;
-  int ldc;
-  uint32_t idesc, tmem_cols;
-  EpiG epi;
-};
-
 struct TnParams {
   int M, N, K, BN, stages, num_kb, kb_per_split;
   float* ws;
@@ -60,154 +52,7 @@ struct TnParams {
 
 __device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kThreads, 1)
-    k_gemm_nt(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, NtParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t b_bytes = (uint32_t)p.BN * kBK * 4;
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + (size_t)p.stages * kATileBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (size_t)p.stages * b_bytes);
-  uint64_t* empty = full + p.stages;
-  uint64_t* tfull = empty + p.stages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
-  float* colsum_sm = reinterpret_cast<float*>(tmem_slot + 4);  // [4][BN]
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * kBM;
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < p.stages; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
-    }
-    tc::mbar_init(tfull, 1);
-    tc::fence_barrier_init();
-    tc::tma_prefetch_desc(&tmA);
-    tc::tma_prefetch_desc(&tmB);
-  }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        const int s = kb % p.stages;
-        const uint32_t ph = (uint32_t)(kb / p.stages) & 1u;
-        tc::mbar_wait(&empty[s], ph ^ 1u);
-        tc::mbar_arrive_expect_tx(&full[s], kATileBytes + b_bytes);
-        tc::tma_load_2d(sA + (size_t)s * kATileBytes, &tmA, &full[s], kb * kBK, m0);
-        tc::tma_load_2d(sB + (size_t)s * b_bytes, &tmB, &full[s], kb * kBK, 0);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      for (int kb = 0; kb < p.num_kb; ++kb) {
-        const int s = kb % p.stages;
-        const uint32_t ph = (uint32_t)(kb / p.stages) & 1u;
-        tc::mbar_wait(&full[s], ph);
-        tc::fence_after_sync();
-        const uint32_t a_base = tc::smem_u32(sA + (size_t)s * kATileBytes);
-        const uint32_t b_base = tc::smem_u32(sB + (size_t)s * b_bytes);
-#pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {  // UMMA_K = 8 for tf32 (32 B of each 128 B row)
-          const uint64_t da = tc::smem_desc_sw128(a_base + k * 32, 16, 1024);
-          const uint64_t db = tc::smem_desc_sw128(b_base + k * 32, 16, 1024);
-          tc::mma_tf32(tmem, da, db, p.idesc, (kb | k) != 0 ? 1u : 0u);
-        }
-        tc::mma_commit(&empty[s]);  // frees the smem slot once these MMAs have read it
-      }
-      tc::mma_commit(tfull);  // accumulator complete
-    }
-  } else {  // ---------------- epilogue warps 2..5
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = m0 + q * 32 + lane;
-    const bool row_ok = row < p.M;
-    if (p.num_kb > 0) {
-      tc::mbar_wait(tfull, 0);
-      tc::fence_after_sync();
-    }
-    const EpiG& e = p.epi;
-    const float rs = (row_ok && (e.flags & MPH_EPI_ROWSCALE)) ? e.row_scale[row] : 1.0f;
-    float* crow = p.C + (int64_t)row * p.ldc;
-    for (int c0 = 0; c0 < p.BN; c0 += 16) {
-      float v[16];
-      if (p.num_kb > 0)
-        tc::tmem_ld_32x32b_x16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, v);
-      else
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = c0 + i;
-        float x = v[i];
-        if (c < p.N && row_ok) {
-          if (e.flags & MPH_EPI_BIAS) x += e.bias[c];
-          if (e.flags & MPH_EPI_MASK) x = (e.mask_src[(int64_t)row * e.ld_mask + c] > 0.0f) ? x * e.mask_scale : 0.0f;
-          if (e.flags & MPH_EPI_RELU) x = fmaxf(x, 0.0f);
-        } else {
-          x = 0.0f;
-        }
-        v[i] = x;
-      }
-      if (e.flags & MPH_EPI_DROPOUT) {
-#pragma unroll
-        for (int i = 0; i < 16; i += 4) {
-          const int c = c0 + i;
-          PhiloxOut r = philox4x32_10((uint32_t)(e.row0 + row), (uint32_t)(c >> 2), e.drop.layer, e.drop.epoch,
-                                      e.drop.key0, e.drop.key1);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) v[i + j] = r.v[j] >= e.drop.threshold ? v[i + j] * e.drop.scale : 0.0f;
-        }
-      }
-      if (e.flags & MPH_EPI_COLSUM) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float t = v[i];
-#pragma unroll
-          for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-          if (lane == 0) colsum_sm[q * p.BN + c0 + i] = t;
-        }
-      }
-      if (e.flags & MPH_EPI_TF32) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = tf32_rna(v[i] * rs);
-      } else if (e.flags & MPH_EPI_ROWSCALE) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] *= rs;
-      }
-      if (row_ok) {
-        if (c0 + 16 <= p.N && (p.ldc & 3) == 0) {
-          float4* dst = reinterpret_cast<float4*>(crow + c0);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c0 + i < p.N) crow[c0 + i] = v[i];
-        }
-      }
-    }
-    if (e.flags & MPH_EPI_COLSUM) {
-      epi_bar_sync();
-      const int t = threadIdx.x - 64;
-      for (int c = t; c < p.N; c += 128) {
-        float sacc = colsum_sm[c];
-        sacc += colsum_sm[p.BN + c];
-        sacc += colsum_sm[2 * p.BN + c];
-        sacc += colsum_sm[3 * p.BN + c];
-        e.colsum_out[(int64_t)blockIdx.x * p.N + c] = sacc;
-      }
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
-}
+#include "gemm_nt.inc"
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TnParams p) {
@@ -394,29 +239,40 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
                    const mph_epilogue* epi, cudaStream_t s) {
   if (M < 0 || N <= 0 || K < 0 || !A || !Bt || !C) return fail(MPH_EINVAL, "gemm_nt: bad arguments");
   if (N > 256) return fail(MPH_ENOTSUP, "gemm_nt: N=%d > 256", N);
-  if (lda % 4 || ldb % 4 || lda < K || ldb < K || ldc < N)
-    return fail(MPH_EINVAL, "gemm_nt: lda/ldb must be multiples of 4 >= K, ldc >= N");
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Bt)) & 15)
-    return fail(MPH_EINVAL, "gemm_nt: A and Bt must be 16-byte aligned");
+  if (lda % 4 || ldb % 4 || ldc % 4 || lda < K || ldb < K || ldc < N)
+    return fail(MPH_EINVAL, "gemm_nt: lda/ldb/ldc must be multiples of 4 with lda, ldb >= K and ldc >= N");
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Bt) | reinterpret_cast<uintptr_t>(C)) & 15)
+    return fail(MPH_EINVAL, "gemm_nt: A, Bt and C must be 16-byte aligned");
   const uint32_t flags = epi ? epi->flags : 0u;
   if ((flags & MPH_EPI_BIAS) && !epi->bias) return fail(MPH_EINVAL, "gemm_nt: null bias");
   if ((flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "gemm_nt: null row_scale");
-  if ((flags & MPH_EPI_MASK) && !epi->mask_src) return fail(MPH_EINVAL, "gemm_nt: null mask_src");
+  if ((flags & MPH_EPI_MASK) && (!epi->mask_src || epi->ld_mask % 4 || epi->ld_mask < N ||
+                                 (reinterpret_cast<uintptr_t>(epi->mask_src) & 15)))
+    return fail(MPH_EINVAL, "gemm_nt: mask_src must be 16-byte aligned with ld_mask %% 4 == 0, >= N");
   if ((flags & MPH_EPI_COLSUM) && !epi->colsum_out) return fail(MPH_EINVAL, "gemm_nt: null colsum_out");
   if (M == 0) return MPH_OK;
-  const int BN = round_up(N, 16);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int BN = round_up(N, 32);
   NtParams p{};
   p.M = M;
   p.N = N;
   p.K = K;
   p.BN = BN;
   p.num_kb = (int)ceil_div(K, kBK);
+  p.n_tiles = (int)ceil_div(M, kBM);
+  p.colsum_rows = p.n_tiles;
   const size_t stage_bytes = kATileBytes + (size_t)BN * kBK * 4;
-  p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, kSmemBudget / stage_bytes));
-  p.C = C;
-  p.ldc = ldc;
+  const size_t epi_bytes = 16 * (size_t)kEpiChunkBytes;
+  const size_t fixed = 1024 + epi_bytes + 64 * 8 + 16 + 4 * (size_t)BN * sizeof(float);
+  p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, (224 * 1024 - fixed) / stage_bytes));
   p.idesc = tc::idesc_tf32(kBM, BN, 0, 0);
-  p.tmem_cols = tmem_cols_for(BN);
+  p.tmem_cols = tmem_cols_for(2 * BN);
   p.epi.flags = flags;
   p.epi.row_scale = epi ? epi->row_scale : nullptr;
   p.epi.bias = epi ? epi->bias : nullptr;
@@ -427,16 +283,22 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
   p.epi.drop = make_dropout(epi);
   p.epi.row0 = epi ? epi->row0 : 0;
   if (p.epi.drop.threshold == 0) p.epi.flags &= ~MPH_EPI_DROPOUT;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tcm, tm;
   MPH_TRY(make_tmap(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM));
   MPH_TRY(make_tmap(&tb, Bt, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kBK, (uint32_t)BN));
-  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (2 * p.stages + 1) * 8 + 16 + 4 * BN * sizeof(float);
+  MPH_TRY(make_tmap(&tcm, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, 32, 32));
+  if (flags & MPH_EPI_MASK)
+    MPH_TRY(make_tmap(&tm, epi->mask_src, (uint64_t)N, (uint64_t)M, (uint64_t)epi->ld_mask, 32, 32));
+  else
+    tm = tcm;
+  const size_t smem = fixed + (size_t)p.stages * stage_bytes;
   static size_t configured = 0;
   if (smem > configured) {
     MPH_CUDA_TRY(cudaFuncSetAttribute(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  k_gemm_nt<<<(unsigned)ceil_div(M, kBM), kThreads, smem, s>>>(ta, tb, p);
+  const int grid = std::min(p.n_tiles, sms);
+  k_gemm_nt<<<grid, kThreads, smem, s>>>(ta, tb, tcm, tm, p);
   count_launch();
   return launch_check("gemm_nt");
 }

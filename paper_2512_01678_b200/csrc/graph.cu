@@ -96,6 +96,8 @@ static void graph_free(mph_graph* g) {
   dev_free(g->split);
   dev_free(g->send_ids);
   dev_free(g->send_buf);
+  dev_free(g->items);
+  dev_free(g->item_counter);
   delete g;
 }
 

@@ -24,6 +24,10 @@ struct mph_graph {
   int64_t n_send = 0;
   float* send_buf = nullptr;
   size_t send_cap = 0;  // floats
+  // edge-balanced SpMM work items (spmm.cu): [first_row, end_row) runs, hubs first
+  int2* items = nullptr;
+  int n_items = 0;
+  int* item_counter = nullptr;
 };
 
 struct mph_features {

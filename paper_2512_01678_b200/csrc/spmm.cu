@@ -4,16 +4,24 @@
 // B200 design (differs from the paper's block-per-row):
 //  * one warp per output row.  The row's width is covered by LPR lanes holding VPL float4
 //    each; the remaining 32/LPR "edge slots" walk different neighbours of the same row, so
-//    all 32 lanes stay busy for every width (48-wide rows: 4 lanes x 3 float4 x 8 slots).
-//  * neighbour ids are read 32 at a time with one coalesced 128 B load (L1 no-allocate) and
-//    broadcast by shuffles; each lane then issues U independent 16 B gathers before it
-//    consumes any (U x VPL loads in flight per lane).
+//    all 32 lanes stay busy for every width (48-wide rows: 4 lanes x 3 float4 x 8 slots) and
+//    every warp-wide load moves up to 512 B.
+//  * neighbour ids are read 32 at a time with one coalesced 128 B load (L1 no-allocate); the
+//    next 32 are prefetched while the current ones are gathered; each lane issues U×VPL
+//    independent 16 B gathers before it consumes any.
+//  * persistent warps pull work items from a global counter.  A work item is a run of
+//    consecutive rows holding about the same number of edges (built once per graph), so the
+//    power-law degree skew (Reddit hubs have 20x the mean degree) never idles a warp the way
+//    a block-per-row grid does; items holding a hub row are served first, so the longest
+//    rows start at t = 0 instead of forming the tail; rows are never split, so the summation
+//    order of every row is fixed (deterministic).
 //  * per-edge values are pre-scaled by dinv at the producer (T' = dinv ⊙ T), so the kernel
 //    reads no per-edge weight: out[u] = dinv[u] · Σ_v T'[v]  ==  (Â·T)[u]  (Q1).
 //  * partial sums: a pairwise tree over each group of U gathers, a running sum per slot,
-//    and a fixed xor-shuffle tree across slots — deterministic, atomic-free.
-//  * epilogue fused: dinv, bias, ReLU, inverted dropout (Philox, Q10), row scale.
+//    and a fixed xor-shuffle tree across slots.
+//  * epilogue fused: dinv, bias, ReLU, inverted dropout (Philox, Q10), row scale, TF32 store.
 #include <algorithm>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -34,6 +42,9 @@ struct SpmmArgs {
   const float* dinv;
   const float* in;
   float* out;
+  const int2* items;  // [first_row, end_row) per work item, hubs first
+  int* counter;
+  int n_items;
   int ld_in, ld_out, n_rows, nv4, part;
   EpiDev epi;
 };
@@ -48,94 +59,105 @@ __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int6
 }
 
 template <int LPR, int VPL>
-__global__ void __launch_bounds__(256, 2) k_spmm(SpmmArgs a) {
+__device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   constexpr int ES = 32 / LPR;
   // U gathers per slot in flight; U*VPL float4 loads per lane before the first use
   constexpr int U0 = (32 / ES) < 8 ? (32 / ES) : 8;
   constexpr int U = (U0 * VPL > 8) ? ((8 / VPL) < 2 ? 2 : (8 / VPL)) : U0;
-  const int lane = threadIdx.x & 31;
   const int slot = lane / LPR, sub = lane % LPR;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < a.n_rows; row += nwarps) {
-    int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
-    if (a.part == 0) e = a.split[row];
-    if (a.part == 1) s = a.split[row];
-    float4 acc[VPL];
+  int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
+  if (a.part == 0) e = a.split[row];
+  if (a.part == 1) s = a.split[row];
+  float4 acc[VPL];
 #pragma unroll
-    for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
-    for (int64_t base = s; base < e; base += 32) {
-      const int nb = (int)min((int64_t)32, e - base);
-      const int my_c = lane < nb ? ldg_stream_i32(a.col + base + lane) : 0;
-      for (int k0 = 0; k0 < nb; k0 += ES * U) {
-        float4 x[U][VPL];
+  for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
+  int nxt = (s + lane < e) ? ldg_stream_i32(a.col + s + lane) : 0;
+  for (int64_t base = s; base < e; base += 32) {
+    const int nb = (int)min((int64_t)32, e - base);
+    const int my_c = nxt;
+    nxt = (base + 32 + lane < e) ? ldg_stream_i32(a.col + base + 32 + lane) : 0;  // prefetch next ids
+    for (int k0 = 0; k0 < nb; k0 += ES * U) {
+      float4 x[U][VPL];
 #pragma unroll
-        for (int uu = 0; uu < U; ++uu) {
-          const int k = k0 + uu * ES + slot;
-          const int c = __shfl_sync(0xffffffffu, my_c, k & 31);
-          const float4* p = reinterpret_cast<const float4*>(a.in + (int64_t)c * a.ld_in) + sub;
+      for (int uu = 0; uu < U; ++uu) {
+        const int k = k0 + uu * ES + slot;
+        const int c = __shfl_sync(0xffffffffu, my_c, k & 31);
+        const float4* p = reinterpret_cast<const float4*>(a.in + (int64_t)c * a.ld_in) + sub;
 #pragma unroll
-          for (int j = 0; j < VPL; ++j)
-            x[uu][j] = (k < nb && sub + j * LPR < a.nv4) ? ldg_f4(p + j * LPR) : f4_zero();
-        }
-#pragma unroll
-        for (int j = 0; j < VPL; ++j) {
-#pragma unroll
-          for (int w = 1; w < U; w <<= 1)
-#pragma unroll
-            for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add(x[uu][j], x[uu + w][j]);
-          acc[j] = f4_add(acc[j], x[0][j]);
-        }
+        for (int j = 0; j < VPL; ++j)
+          x[uu][j] = (k < nb && sub + j * LPR < a.nv4) ? ldg_f4(p + j * LPR) : f4_zero();
       }
-    }
-#pragma unroll
-    for (int off = LPR; off < 32; off <<= 1)
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
-        acc[j].x += __shfl_xor_sync(0xffffffffu, acc[j].x, off);
-        acc[j].y += __shfl_xor_sync(0xffffffffu, acc[j].y, off);
-        acc[j].z += __shfl_xor_sync(0xffffffffu, acc[j].z, off);
-        acc[j].w += __shfl_xor_sync(0xffffffffu, acc[j].w, off);
-      }
-    if (slot != 0) continue;
-    float4* orow = reinterpret_cast<float4*>(a.out + (int64_t)row * a.ld_out);
-    if (a.part == 0) {
 #pragma unroll
-      for (int j = 0; j < VPL; ++j)
-        if (sub + j * LPR < a.nv4) orow[sub + j * LPR] = acc[j];
-      continue;
+        for (int w = 1; w < U; w <<= 1)
+#pragma unroll
+          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add(x[uu][j], x[uu + w][j]);
+        acc[j] = f4_add(acc[j], x[0][j]);
+      }
     }
-    const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
-    const float du = a.dinv[row];
-    const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[row] : 1.0f;
+  }
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1)
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
-      const int c4 = sub + j * LPR;
-      if (c4 >= a.nv4) continue;
-      float4 v = acc[j];
-      if (a.part == 1) v = f4_add(v, orow[c4]);
-      v.x *= du;
-      v.y *= du;
-      v.z *= du;
-      v.w *= du;
-      if (a.epi.flags & MPH_EPI_BIAS) {
-        float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
-        v = f4_add(v, b);
-      }
-      if (a.epi.flags & MPH_EPI_RELU) {
-        v.x = fmaxf(v.x, 0.0f);
-        v.y = fmaxf(v.y, 0.0f);
-        v.z = fmaxf(v.z, 0.0f);
-        v.w = fmaxf(v.w, 0.0f);
-      }
-      if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, c4);
-      if (a.epi.flags & MPH_EPI_ROWSCALE) {
-        v.x *= rs;
-        v.y *= rs;
-        v.z *= rs;
-        v.w *= rs;
-      }
-      orow[c4] = to_tf32 ? f4_tf32(v) : v;
+      acc[j].x += __shfl_xor_sync(0xffffffffu, acc[j].x, off);
+      acc[j].y += __shfl_xor_sync(0xffffffffu, acc[j].y, off);
+      acc[j].z += __shfl_xor_sync(0xffffffffu, acc[j].z, off);
+      acc[j].w += __shfl_xor_sync(0xffffffffu, acc[j].w, off);
     }
+  if (slot != 0) return;
+  float4* orow = reinterpret_cast<float4*>(a.out + (int64_t)row * a.ld_out);
+  if (a.part == 0) {
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+      if (sub + j * LPR < a.nv4) orow[sub + j * LPR] = acc[j];
+    return;
+  }
+  const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
+  const float du = a.dinv[row];
+  const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[row] : 1.0f;
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int c4 = sub + j * LPR;
+    if (c4 >= a.nv4) continue;
+    float4 v = acc[j];
+    if (a.part == 1) v = f4_add(v, orow[c4]);
+    v.x *= du;
+    v.y *= du;
+    v.z *= du;
+    v.w *= du;
+    if (a.epi.flags & MPH_EPI_BIAS) {
+      float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
+      v = f4_add(v, b);
+    }
+    if (a.epi.flags & MPH_EPI_RELU) {
+      v.x = fmaxf(v.x, 0.0f);
+      v.y = fmaxf(v.y, 0.0f);
+      v.z = fmaxf(v.z, 0.0f);
+      v.w = fmaxf(v.w, 0.0f);
+    }
+    if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, c4);
+    if (a.epi.flags & MPH_EPI_ROWSCALE) {
+      v.x *= rs;
+      v.y *= rs;
+      v.z *= rs;
+      v.w *= rs;
+    }
+    orow[c4] = to_tf32 ? f4_tf32(v) : v;
+  }
+}
+
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(256, 3) k_spmm(SpmmArgs a) {
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(a.counter, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= a.n_items) break;
+    const int2 rr = a.items[it];
+    for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL>(a, row, lane);
   }
 }
 
@@ -156,11 +178,77 @@ Dropout make_dropout(const mph_epilogue* e) {
   return d;
 }
 
+// Work items (built once per graph, on the host from row_ptr): runs of consecutive rows of
+// about E edges, E = nnz / (8 items per resident warp) clamped to [64, 2048]; a row longer
+// than E is an item of its own.  Items holding a row longer than 4E ("hubs") come first,
+// longest first.
+static int build_items(const mph_graph* gc, cudaStream_t s) {
+  mph_graph* g = const_cast<mph_graph*>(gc);
+  if (g->items) return MPH_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, g->nnz / ((int64_t)sms * 24 * 8)));
+  std::vector<int64_t> rp((size_t)g->n_rows + 1);
+  MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), g->row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  MPH_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<int2> hubs, rest;
+  std::vector<int64_t> hub_len;
+  int r0 = 0;
+  int64_t acc = 0;
+  for (int r = 0; r < g->n_rows; ++r) {
+    const int64_t d = rp[r + 1] - rp[r];
+    if (d > kItemEdges) {  // long row: flush the current run, then the row alone
+      if (r > r0) rest.push_back(make_int2(r0, r));
+      if (d > 4 * kItemEdges) {
+        hubs.push_back(make_int2(r, r + 1));
+        hub_len.push_back(d);
+      } else {
+        rest.push_back(make_int2(r, r + 1));
+      }
+      r0 = r + 1;
+      acc = 0;
+      continue;
+    }
+    acc += d;
+    if (acc >= kItemEdges) {
+      rest.push_back(make_int2(r0, r + 1));
+      r0 = r + 1;
+      acc = 0;
+    }
+  }
+  if (r0 < g->n_rows) rest.push_back(make_int2(r0, g->n_rows));
+  std::vector<size_t> order(hubs.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return hub_len[x] > hub_len[y]; });
+  std::vector<int2> items;
+  items.reserve(hubs.size() + rest.size());
+  for (size_t i : order) items.push_back(hubs[i]);
+  items.insert(items.end(), rest.begin(), rest.end());
+  MPH_TRY(dev_alloc(&g->items, items.size()));
+  MPH_TRY(dev_alloc(&g->item_counter, 1));
+  MPH_CUDA_TRY(cudaMemcpyAsync(g->items, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+  MPH_CUDA_TRY(cudaStreamSynchronize(s));
+  g->n_items = (int)items.size();
+  return MPH_OK;
+}
+
 template <int LPR, int VPL>
-static void launch_spmm(const SpmmArgs& a, cudaStream_t s) {
-  const int64_t warps = a.n_rows;
-  const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(warps, 8));
-  k_spmm<LPR, VPL><<<grid, 256, 0, s>>>(a);
+static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
+  static int blocks_per_sm = 0;
+  static int sms = 0;
+  if (!blocks_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<LPR, VPL>, 256, 0);
+    blocks_per_sm = std::max(1, blocks_per_sm);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t grid = std::min<int64_t>((int64_t)sms * blocks_per_sm, ceil_div(a.n_items, 8));
+  MPH_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
+  k_spmm<LPR, VPL><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
+  count_launch();
+  return launch_check("spmm");
 }
 
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
@@ -178,6 +266,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
     return fail(MPH_EINVAL, "spmm: bias must be non-null and 16-byte aligned");
   if (epi && (epi->flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "spmm: null row_scale");
   if (g->n_rows == 0) return MPH_OK;
+  MPH_TRY(build_items(g, s));
   SpmmArgs a;
   a.row_ptr = g->row_ptr;
   a.split = g->split;
@@ -185,6 +274,9 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.dinv = g->dinv;
   a.in = in;
   a.out = out;
+  a.items = g->items;
+  a.counter = g->item_counter;
+  a.n_items = g->n_items;
   a.ld_in = ld_in;
   a.ld_out = ld_out;
   a.n_rows = g->n_rows;
@@ -197,28 +289,16 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.epi.row0 = epi ? epi->row0 : 0;
   if (a.epi.drop.threshold == 0) a.epi.flags &= ~MPH_EPI_DROPOUT;
   const int nv4 = a.nv4;
-  if (nv4 <= 1)
-    launch_spmm<1, 1>(a, s);
-  else if (nv4 <= 2)
-    launch_spmm<2, 1>(a, s);
-  else if (nv4 <= 4)
-    launch_spmm<4, 1>(a, s);
-  else if (nv4 <= 8)
-    launch_spmm<8, 1>(a, s);
-  else if (nv4 <= 12)
-    launch_spmm<4, 3>(a, s);
-  else if (nv4 <= 16)
-    launch_spmm<16, 1>(a, s);
-  else if (nv4 <= 32)
-    launch_spmm<32, 1>(a, s);
-  else if (nv4 <= 64)
-    launch_spmm<32, 2>(a, s);
-  else if (nv4 <= 96)
-    launch_spmm<32, 3>(a, s);
-  else
-    launch_spmm<32, 4>(a, s);
-  count_launch();
-  return launch_check("spmm");
+  if (nv4 <= 1) return launch_spmm<1, 1>(a, s);
+  if (nv4 <= 2) return launch_spmm<2, 1>(a, s);
+  if (nv4 <= 4) return launch_spmm<4, 1>(a, s);
+  if (nv4 <= 8) return launch_spmm<8, 1>(a, s);
+  if (nv4 <= 12) return launch_spmm<4, 3>(a, s);
+  if (nv4 <= 16) return launch_spmm<16, 1>(a, s);
+  if (nv4 <= 32) return launch_spmm<32, 1>(a, s);
+  if (nv4 <= 64) return launch_spmm<32, 2>(a, s);
+  if (nv4 <= 96) return launch_spmm<32, 3>(a, s);
+  return launch_spmm<32, 4>(a, s);
 }
 
 __global__ void k_pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int nv4, float* out) {
