@@ -190,29 +190,12 @@ def _build_model(P, torch, w, world, rank, comm):
     return g, f, m, y, own, extra
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-
-    world = _env_int("WORLD_SIZE", 1)
-    rank = _env_int("RANK", 0)
-    local = _env_int("LOCAL_RANK", 0)
-    if world != args.gpus:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    import paper_2512_01678_b200 as P
-    from paper_2512_01678_b200 import _lib as L
-    from synth.generate import make_workload
-
-    import ctypes as C
-    L.mph_device_check(C.byref(C.c_int32()))
+def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full: bool):
+    """Build one workload and time it.  full=False skips e2e and the CPU baseline (secondary)."""
     t_setup = time.perf_counter()
-    w = make_workload(args.config)
+    from synth.generate import make_workload
+    w = make_workload(config)
     t_gen = time.perf_counter() - t_setup
-    comm = P.Comm(world, rank) if world > 1 else None
     t0 = time.perf_counter()
     g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm)
     torch.cuda.synchronize()
@@ -264,7 +247,7 @@ def run_ours(args):
 
     # ---------------- end-to-end through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if full and not args.no_e2e:
         X = w["X"][own[0]:own[1]]
         Pw = P.pad_width(X.shape[1])
         Xh = torch.zeros((X.shape[0], Pw), dtype=torch.float32).pin_memory()   # padded pinned host rows
@@ -272,7 +255,6 @@ def run_ours(args):
         upload = f.mode == 0   # sparse-mode features are analysed once at load (Alg. 1); labels still move
         yh = torch.from_numpy(np.ascontiguousarray(w["y"][own[0]:own[1]])).pin_memory()
         lh = torch.zeros(1, dtype=torch.float64).pin_memory()
-        ysrc = y  # device label buffer the model reads
         steps_e2e = max(3, args.steps // 2)
         torch.cuda.synchronize()
         barrier()
@@ -282,7 +264,7 @@ def run_ours(args):
         for t in range(base + 1, base + steps_e2e + 1):
             if upload:
                 L.mph_gcn_upload_features(m.h, Xh.data_ptr(), Pw, stream.cuda_stream)
-            ysrc.copy_(yh, non_blocking=True)
+            y.copy_(yh, non_blocking=True)
             m.train_epoch(t)
             lh.copy_(m.loss_buf, non_blocking=True)
             stream.synchronize()  # the step's result is on the host
@@ -294,7 +276,8 @@ def run_ours(args):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_ms = tt.item()
         e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 4 * upload + yh.numel() * 4),
-               "d2h_bytes_per_step": 8, "steps": steps_e2e}
+               "d2h_bytes_per_step": 8, "steps": steps_e2e,
+               "inputs": "features (padded, pinned) + labels H2D, loss D2H, every step"}
 
     # ---------------- roofline of the dominant kernel
     peak, peak_kind = _peaks()
@@ -304,43 +287,117 @@ def run_ours(args):
     if dom is not None:
         kd = kernels[dom]
         traffic = None
-        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
         if os.path.exists(tp):
             with open(tp) as fh:
                 traffic = json.load(fh).get(dom, {}).get("dram_bytes_per_launch")
         roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": peak, "unit": "GB/s",
                     "frac": kd["algorithmic_GBps"] / peak, "traffic": traffic,
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                    "algorithmic_bytes": "SURVEY 8(d) d.3 no-reuse count: per edge 4 + 4*w B, per row 12 + 4*w B",
                     "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_ms": kd["avg_launch_ms"],
                     "share_of_epoch": kd["ms_per_epoch"] / ms}
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
-    if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        sample = _oracle_sample(args.config)
+    if full and world == 1 and rank == 0 and not args.no_cpu_baseline:
+        sample = _oracle_sample(config)
         ms_cpu = _oracle_epoch_ms(sample, 1)
         cpu = {"value": statistics.median(ms_cpu), "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
                "sample": _sample_desc(sample)}
 
+    out = {
+        "value": ms, "ms_per_step": ms,
+        "config": {"workload": config, "nodes": cfg.num_nodes, "nnz_A": cfg.nnz_a, "dims": list(cfg.dims),
+                   "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
+                   "parallelism": f"1d-row-partition x{world}" if world > 1 else "single-gpu",
+                   "layer_order": ["AF" if o else "TF" for o in m.order],
+                   "l2": "inputs larger than L2 (X and col_idx > 126 MB); no flush" if cfg.num_nodes > 100000
+                   else "small workload: operands L2-resident across epochs (no flush)",
+                   **extra},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        "kernels": kernels, "final_loss": loss_last,
+        "setup_s": {"generate": round(t_gen, 2), "graph_build_and_init": round(t_build, 2)},
+    }
+    del m, f, g
+    return out
+
+
+def _gather_peaks(L, torch):
+    """Measured random-row gather bandwidth (512 B rows) from an L2-resident (64 MB) and an
+    HBM-resident (4 GB) table: the ceilings the aggregation SpMM actually runs against."""
+    res = {}
+    w = 128
+    out = torch.empty(148 * 32 * 128, device="cuda")
+    n_idx = 1 << 24
+    for name, table_bytes in (("l2_resident_64MB", 64 << 20), ("hbm_resident_4GB", 4 << 30)):
+        rows = table_bytes // (w * 4)
+        table = torch.ones((rows, w), device="cuda")
+        idx = torch.randint(0, rows, (n_idx,), device="cuda", dtype=torch.int32)
+        s = torch.cuda.current_stream()
+        best = None
+        for _ in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            L.mph_probe_gather(table.data_ptr(), rows, w, idx.data_ptr(), n_idx, out.data_ptr(), s.cuda_stream)
+            e1.record(s)
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1)
+            best = t if best is None else min(best, t)
+        res[name] = n_idx * w * 4 / best / 1e6
+        del table, idx
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2512_01678_b200 as P
+    from paper_2512_01678_b200 import _lib as L
+
+    L.mph_device_check(C.byref(C.c_int32()))
+    comm = P.Comm(world, rank) if world > 1 else None
+    main = _measure(P, L, torch, dist, C, args, args.config, world, rank, local, comm, full=True)
+    secondary = {}
+    for cfgname in ([] if args.secondary == "none" else args.secondary.split(",")):
+        if cfgname and cfgname != args.config:
+            r = _measure(P, L, torch, dist, C, args, cfgname, world, rank, local, comm, full=False)
+            secondary[cfgname] = {k: r[k] for k in ("value", "config", "roofline", "kernels", "gpu_launches",
+                                                    "final_loss", "clocks")}
+    peaks = _gather_peaks(L, torch) if (world == 1 and not args.no_probe) else None
+    if peaks and main["roofline"] and main["roofline"]["kernel"] == "spmm":
+        main["roofline"]["measured_gather_peaks_GBps"] = peaks
+        main["roofline"]["frac_of_l2_gather_peak"] = main["roofline"]["achieved"] / peaks["l2_resident_64MB"]
+    for r in secondary.values():
+        if peaks and r["roofline"] and r["roofline"]["kernel"] == "spmm":
+            r["roofline"]["frac_of_l2_gather_peak"] = r["roofline"]["achieved"] / peaks["l2_resident_64MB"]
+
     if rank == 0:
         line = {
-            "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": False, "scaling": "strong" if world > 1 else "strong",
-            "vs_baseline": None, "dtype": "f32 (SpMM, loss, Adam) + tf32 tensor-core GEMMs", "data": "synthetic",
-            "config": {"workload": args.config, "nodes": cfg.num_nodes, "nnz_A": cfg.nnz_a, "dims": list(cfg.dims),
-                       "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
-                       "parallelism": f"1d-row-partition x{world}" if world > 1 else "single-gpu",
-                       "layer_order": ["AF" if o else "TF" for o in m.order],
-                       "l2": "inputs larger than L2 (X and col_idx each > 126 MB); no flush",
-                       **extra},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clk, "kernels": kernels, "final_loss": loss_last,
-            "setup_s": {"generate": round(t_gen, 2), "graph_build_and_init": round(t_build, 2)},
+            "metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": main["ms_per_step"], "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (SpMM, loss, Adam) + tf32 tensor-core GEMMs",
+            "data": "synthetic", "config": main["config"], "roofline": main["roofline"],
+            "cpu_baseline": main["cpu_baseline"], "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
+            "clocks": main["clocks"], "kernels": main["kernels"], "final_loss": main["final_loss"],
+            "setup_s": main["setup_s"], "secondary": secondary or None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
-        del m, f, g
         dist.destroy_process_group()
     return 0
 
@@ -354,6 +411,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-probe", action="store_true", help="skip the gather-bandwidth probe")
+    ap.add_argument("--secondary", default="products",
+                    help="comma-separated extra workloads timed in the same run (device time + roofline), or none")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -210,6 +210,11 @@ int mph_xavier_fill(float* W_d, int32_t f_in, int32_t f_out, int32_t ld, uint64_
 #define MPH_PROF_OTHER 7
 int mph_profile_enable(int32_t on);
 int mph_profile_read(int32_t kind, int64_t* count_h, double* total_ms_h, double* total_bytes_h, double* total_flops_h);
+/* Gather-bandwidth probe: sums rows idx_d[0..n_idx) (w floats, w % 4 == 0,
+ * w <= 128) of table_d [n_rows][w]; out_d needs 148*32*128 floats.  Used by bench.py to measure
+ * the L2-resident and HBM-resident random-row gather peaks the SpMM is compared with. */
+int mph_probe_gather(const float* table_d, int64_t n_rows, int32_t w, const int32_t* idx_d, int64_t n_idx,
+                     float* out_d, void* stream);
 
 /* =====================================================================================
  * a10/a11 — distributed runtime (MPI backend analogue).

@@ -15,66 +15,87 @@ namespace mph {
 constexpr int kCeThreads = 256;
 constexpr int kCeMaxC = 256;
 
-static int ce_grid(int N) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, 64), 592)); }
+static int ce_grid(int N) { return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, 64), 148 * 8)); }
 
+// Warp per row, R rows per warp iteration with all their loads issued first (latency hiding);
+// NJ = ceil(C/32) columns chunks per lane.
+template <int NJ>
 __global__ void __launch_bounds__(kCeThreads) k_softmax_ce(const float* Z, int N, int C, int ld, const int32_t* labels,
                                                            const uint8_t* mask, float inv_nlab, const float* row_scale,
                                                            float* dZ, int ld_dz, double* part_loss, float* part_db) {
+  constexpr int R = NJ <= 2 ? 4 : (NJ <= 4 ? 2 : 1);
   __shared__ double s_loss[kCeThreads / 32];
   __shared__ float s_db[kCeThreads / 32][kCeMaxC];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nj = (C + 31) / 32;
-  float dbacc[kCeMaxC / 32];
+  float dbacc[NJ];
 #pragma unroll
-  for (int j = 0; j < kCeMaxC / 32; ++j) dbacc[j] = 0.0f;
+  for (int j = 0; j < NJ; ++j) dbacc[j] = 0.0f;
   double lacc = 0.0;
   const int wpb = kCeThreads / 32;
-  for (int i = blockIdx.x * wpb + warp; i < N; i += gridDim.x * wpb) {
-    const float* z = Z + (int64_t)i * ld;
-    float* dz = dZ + (int64_t)i * ld_dz;
-    const bool lab = mask ? (mask[i] != 0) : true;
-    if (!lab) {
-      for (int c = lane; c < C; c += 32) dz[c] = 0.0f;
-      continue;
-    }
-    float zv[kCeMaxC / 32];
-    float m = -INFINITY;
+  const int stride = gridDim.x * wpb;
+  for (int i0 = blockIdx.x * wpb + warp; i0 < N; i0 += stride * R) {
+    float zv[R][NJ];
+    int yv[R];
+    float rsv[R];
+    bool labv[R];
 #pragma unroll
-    for (int j = 0; j < kCeMaxC / 32; ++j) {
-      const int c = lane + 32 * j;
-      zv[j] = (j < nj && c < C) ? z[c] : -INFINITY;
-      m = fmaxf(m, zv[j]);
-    }
+    for (int r = 0; r < R; ++r) {
+      const int i = i0 + r * stride;
+      const bool ok = i < N;
+      const float* z = Z + (int64_t)(ok ? i : 0) * ld;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float se = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kCeMaxC / 32; ++j)
-      if (j < nj && lane + 32 * j < C) se += expf(zv[j] - m);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
-    const float lse = m + logf(se);
-    const int y = labels[i];
-    const float rs = row_scale ? row_scale[i] : 1.0f;
-    float zy = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kCeMaxC / 32; ++j) {
-      const int c = lane + 32 * j;
-      if (j < nj && c < C) {
-        if (c == y) zy = zv[j];
-        const float g = (expf(zv[j] - lse) - (c == y ? 1.0f : 0.0f)) * inv_nlab;
-        dbacc[j] += g;
-        dz[c] = g * rs;
+      for (int j = 0; j < NJ; ++j) {
+        const int c = lane + 32 * j;
+        zv[r][j] = (ok && c < C) ? __ldg(z + c) : -INFINITY;
       }
+      yv[r] = ok ? __ldg(labels + i) : 0;
+      rsv[r] = (ok && row_scale) ? __ldg(row_scale + i) : 1.0f;
+      labv[r] = ok && (mask ? (mask[i] != 0) : true);
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) zy += __shfl_xor_sync(0xffffffffu, zy, o);
-    lacc += (double)lse - (double)zy;
+    for (int r = 0; r < R; ++r) {
+      const int i = i0 + r * stride;
+      if (i >= N) continue;
+      float* dz = dZ + (int64_t)i * ld_dz;
+      if (!labv[r]) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          if (lane + 32 * j < C) dz[lane + 32 * j] = 0.0f;
+        continue;
+      }
+      float m = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) m = fmaxf(m, zv[r][j]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float se = 0.0f;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (lane + 32 * j < C) se += expf(zv[r][j] - m);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+      const float lse = m + logf(se);
+      const int y = yv[r];
+      float zy = 0.0f;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int c = lane + 32 * j;
+        if (c < C) {
+          if (c == y) zy = zv[r][j];
+          const float g = (expf(zv[r][j] - lse) - (c == y ? 1.0f : 0.0f)) * inv_nlab;
+          dbacc[j] += g;
+          dz[c] = g * rsv[r];
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) zy += __shfl_xor_sync(0xffffffffu, zy, o);
+      lacc += (double)lse - (double)zy;
+    }
   }
   if (lane == 0) s_loss[warp] = lacc;
 #pragma unroll
-  for (int j = 0; j < kCeMaxC / 32; ++j)
-    if (j < nj && lane + 32 * j < C) s_db[warp][lane + 32 * j] = dbacc[j];
+  for (int j = 0; j < NJ; ++j)
+    if (lane + 32 * j < C) s_db[warp][lane + 32 * j] = dbacc[j];
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
@@ -88,19 +109,33 @@ __global__ void __launch_bounds__(kCeThreads) k_softmax_ce(const float* Z, int N
   }
 }
 
-__global__ void k_ce_finish(const double* part_loss, const float* part_db, int parts, int C, double inv_nlab,
-                            double* loss, float* db) {
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < parts; ++b) t += part_loss[b];
-    *loss = t * inv_nlab;
+// Block c < C reduces column c of the block partials, block C the loss; strided per-thread sums
+// then a fixed smem tree (deterministic).
+__global__ void __launch_bounds__(256) k_ce_finish(const double* part_loss, const float* part_db, int parts, int C,
+                                                   double inv_nlab, double* loss, float* db) {
+  __shared__ double sd[256];
+  const int t = threadIdx.x;
+  double acc = 0.0;
+  if ((int)blockIdx.x == C) {
+    for (int b = t; b < parts; b += 256) acc += part_loss[b];
+  } else {
+    if (!db) return;
+    float f = 0.0f;
+    for (int b = t; b < parts; b += 256) f += part_db[(int64_t)b * C + blockIdx.x];
+    acc = f;
   }
-  if (db)
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-      float t = 0.0f;
-      for (int b = 0; b < parts; ++b) t += part_db[(int64_t)b * C + c];
-      db[c] = t;
-    }
+  sd[t] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (t < o) sd[t] += sd[t + o];
+    __syncthreads();
+  }
+  if (t == 0) {
+    if ((int)blockIdx.x == C)
+      *loss = sd[0] * inv_nlab;
+    else
+      db[blockIdx.x] = (float)sd[0];
+  }
 }
 
 size_t softmax_ce_ws_bytes(int N, int C) {
@@ -118,9 +153,17 @@ int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* label
   const int g = ce_grid(std::max(N, 1));
   double* part_loss = reinterpret_cast<double*>(ws);
   float* part_db = reinterpret_cast<float*>(part_loss + g);
-  k_softmax_ce<<<g, kCeThreads, 0, s>>>(Z, N, C, ld, labels, mask, (float)(1.0 / (double)n_lab), row_scale, dZ, ld_dz,
-                                        part_loss, part_db);
-  k_ce_finish<<<1, 256, 0, s>>>(part_loss, part_db, g, C, 1.0 / (double)n_lab, loss, db);
+  const float inv = (float)(1.0 / (double)n_lab);
+  switch ((C + 31) / 32) {
+#define CE_CASE(NJ)                                                                                              \
+  case NJ:                                                                                                       \
+    k_softmax_ce<NJ><<<g, kCeThreads, 0, s>>>(Z, N, C, ld, labels, mask, inv, row_scale, dZ, ld_dz, part_loss, \
+                                              part_db);                                                          \
+    break;
+    CE_CASE(1) CE_CASE(2) CE_CASE(3) CE_CASE(4) CE_CASE(5) CE_CASE(6) CE_CASE(7) CE_CASE(8)
+#undef CE_CASE
+  }
+  k_ce_finish<<<C + 1, 256, 0, s>>>(part_loss, part_db, g, C, 1.0 / (double)n_lab, loss, db);
   count_launch(2);
   return launch_check("softmax_ce");
 }

@@ -179,7 +179,7 @@ Dropout make_dropout(const mph_epilogue* e) {
 }
 
 // Work items (built once per graph, on the host from row_ptr): runs of consecutive rows of
-// about E edges, E = nnz / (8 items per resident warp) clamped to [64, 2048]; a row longer
+// about E edges, E = nnz / (32 items per resident warp) clamped to [64, 2048]; a row longer
 // than E is an item of its own.  Items holding a row longer than 4E ("hubs") come first,
 // longest first.
 static int build_items(const mph_graph* gc, cudaStream_t s) {
@@ -188,7 +188,7 @@ static int build_items(const mph_graph* gc, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, g->nnz / ((int64_t)sms * 24 * 8)));
+  const int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, g->nnz / ((int64_t)sms * 24 * 32)));
   std::vector<int64_t> rp((size_t)g->n_rows + 1);
   MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), g->row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MPH_CUDA_TRY(cudaStreamSynchronize(s));
