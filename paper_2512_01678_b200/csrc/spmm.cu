@@ -33,6 +33,7 @@ struct EpiDev {
   const float* row_scale;
   Dropout drop;
   int64_t row0;
+  int c4_0;  // float4-column offset of this launch inside the full row (dropout counter)
 };
 
 struct SpmmArgs {
@@ -71,11 +72,12 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   float4 acc[VPL];
 #pragma unroll
   for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
-  int nxt = (s + lane < e) ? ldg_stream_i32(a.col + s + lane) : 0;
+  const uint64_t pol = l2_policy_evict_first();
+  int nxt = (s + lane < e) ? ldg_stream_i32_hint(a.col + s + lane, pol) : 0;
   for (int64_t base = s; base < e; base += 32) {
     const int nb = (int)min((int64_t)32, e - base);
     const int my_c = nxt;
-    nxt = (base + 32 + lane < e) ? ldg_stream_i32(a.col + base + 32 + lane) : 0;  // prefetch next ids
+    nxt = (base + 32 + lane < e) ? ldg_stream_i32_hint(a.col + base + 32 + lane, pol) : 0;  // prefetch next ids
     for (int k0 = 0; k0 < nb; k0 += ES * U) {
       float4 x[U][VPL];
 #pragma unroll
@@ -137,14 +139,14 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
       v.z = fmaxf(v.z, 0.0f);
       v.w = fmaxf(v.w, 0.0f);
     }
-    if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, c4);
+    if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, a.epi.c4_0 + c4);
     if (a.epi.flags & MPH_EPI_ROWSCALE) {
       v.x *= rs;
       v.y *= rs;
       v.z *= rs;
       v.w *= rs;
     }
-    orow[c4] = to_tf32 ? f4_tf32(v) : v;
+    st_f4_hint(orow + c4, to_tf32 ? f4_tf32(v) : v, pol);
   }
 }
 
@@ -288,6 +290,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.epi.drop = make_dropout(epi);
   a.epi.row0 = epi ? epi->row0 : 0;
   if (a.epi.drop.threshold == 0) a.epi.flags &= ~MPH_EPI_DROPOUT;
+  a.epi.c4_0 = 0;
   const int nv4 = a.nv4;
   if (nv4 <= 1) return launch_spmm<1, 1>(a, s);
   if (nv4 <= 2) return launch_spmm<2, 1>(a, s);
