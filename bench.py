@@ -213,8 +213,11 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     barrier()
 
     # ---------------- device-timed region: K epochs, inputs resident in HBM
+    use_graph = bool(args.graph) and world == 1
+    if use_graph:  # one captured epoch, replayed K times (the per-kernel breakdown needs eager launches)
+        m.graph_capture(args.warmup + 1)
     clocks = ClockSampler(local)
-    L.mph_profile_enable(1)
+    L.mph_profile_enable(0 if use_graph else 1)
     launches0 = L.launch_count()
     clocks.start()
     time.sleep(0.15)
@@ -223,7 +226,10 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for t in range(args.warmup + 1, args.warmup + args.steps + 1):
-        m.train_epoch(t)
+        if use_graph:
+            m.replay()
+        else:
+            m.train_epoch(t)
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -312,6 +318,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                    "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
                    "parallelism": f"1d-row-partition x{world}" if world > 1 else "single-gpu",
                    "layer_order": ["AF" if o else "TF" for o in m.order],
+                   "cuda_graph": use_graph,
                    "l2": "inputs larger than L2 (X and col_idx > 126 MB); no flush" if cfg.num_nodes > 100000
                    else "small workload: operands L2-resident across epochs (no flush)",
                    **extra},
@@ -412,6 +419,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the gather-bandwidth probe")
+    ap.add_argument("--graph", action="store_true",
+                    help="time CUDA-graph replays of a captured epoch (1 GPU; launch-bound configs)")
     ap.add_argument("--secondary", default="products",
                     help="comma-separated extra workloads timed in the same run (device time + roofline), or none")
     args = ap.parse_args()

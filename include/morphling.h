@@ -130,6 +130,7 @@ typedef struct {
   uint64_t dropout_seed;
   int32_t dropout_layer, dropout_epoch;
   int64_t row0;            /* global id of row 0 (Philox counter; distributed ranks) */
+  const int32_t* dropout_epoch_d; /* nullable: device epoch counter overriding dropout_epoch (graph replay) */
 } mph_epilogue;
 
 /* a3/a6 — aggregation SpMM (Alg. 3, fused per P:361/P:735):
@@ -294,6 +295,15 @@ int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream);
 /* One epoch a2..a11: forward, loss (written to loss_d, global sum over ranks), backward,
  * gradient all-reduce (P > 1), Adam step t.  Capturable in a CUDA graph when comm == NULL. */
 int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* loss_d, void* stream);
+/* CUDA-graph replay of whole epochs (single GPU; launch-bound configs).  mph_gcn_graph_capture
+ * records one epoch (step-counter advance, forward, loss, backward, Adam with cfg) after at
+ * least one eager mph_gcn_train_epoch (MPH_ESTATE otherwise); the next replay runs epoch
+ * t_next, each further replay the following one.  The step counter and the loss live in
+ * device memory (mph_gcn_graph_state).  Replayed epochs are bitwise identical to eager ones.
+ * Synchronises `stream` before capturing.  MPH_ENOTSUP for P > 1. */
+int mph_gcn_graph_capture(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t_next, void* stream);
+int mph_gcn_graph_replay(mph_gcn* m, void* stream);
+int mph_gcn_graph_state(const mph_gcn* m, int32_t** t_d, double** loss_d);
 /* Borrowed views of activations for tests: kind 0 = layer input H_{l-1} (l=1 is X),
  * 1 = layer output Z_l (hidden: post-ReLU H_l; last: logits), 2 = G_l (backward SpMM out
  * or dZ_1 for an AF layer 1), 3 = aggregate-first Y_1, 4 = transform output T'_l = dinv ⊙ (H·W)

@@ -31,7 +31,7 @@ class Epilogue(C.Structure):
     _fields_ = [("flags", C.c_uint32), ("row_scale", C.c_void_p), ("bias", C.c_void_p), ("mask_src", C.c_void_p),
                 ("ld_mask", C.c_int32), ("mask_scale", C.c_float), ("colsum_out", C.c_void_p),
                 ("dropout_p", C.c_float), ("dropout_seed", C.c_uint64), ("dropout_layer", C.c_int32),
-                ("dropout_epoch", C.c_int32), ("row0", C.c_int64)]
+                ("dropout_epoch", C.c_int32), ("row0", C.c_int64), ("dropout_epoch_d", C.c_void_p)]
 
 
 class AdamCfg(C.Structure):
@@ -105,6 +105,9 @@ _SIGS = {
     "mph_gcn_backward": [P, P],
     "mph_gcn_adam": [P, C.POINTER(AdamCfg), i32, P],
     "mph_gcn_train_epoch": [P, i32, C.POINTER(AdamCfg), P, P],
+    "mph_gcn_graph_capture": [P, C.POINTER(AdamCfg), i32, P],
+    "mph_gcn_graph_replay": [P, P],
+    "mph_gcn_graph_state": [P, PP, PP],
     "mph_gcn_tensor": [P, i32, i32, PP, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
     "mph_gcn_info": [P, P, C.POINTER(i32)],
     "mph_gcn_destroy": [P],

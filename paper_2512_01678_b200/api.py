@@ -305,6 +305,18 @@ class GCN:
         L.mph_gcn_train_epoch(self.h, int(t), C.byref(AdamCfg(*cfg)), out.data_ptr(), stream_ptr(stream))
         return out
 
+    def graph_capture(self, t_next: int, cfg=DEFAULT_ADAM, stream=None):
+        """Record one whole epoch as a CUDA graph; each replay() then runs the next epoch."""
+        L.mph_gcn_graph_capture(self.h, C.byref(AdamCfg(*cfg)), int(t_next), stream_ptr(stream))
+        t, loss = C.c_void_p(), C.c_void_p()
+        L.mph_gcn_graph_state(self.h, C.byref(t), C.byref(loss))
+        self.graph_step = device_view(t.value, (1,), torch.int32)
+        self.graph_loss = device_view(loss.value, (1,), torch.float64)
+
+    def replay(self, stream=None) -> torch.Tensor:
+        L.mph_gcn_graph_replay(self.h, stream_ptr(stream))
+        return self.graph_loss
+
     def tensor(self, kind: int, layer: int) -> torch.Tensor:
         p, rows, width, ld = C.c_void_p(), C.c_int32(), C.c_int32(), C.c_int32()
         L.mph_gcn_tensor(self.h, kind, layer, C.byref(p), C.byref(rows), C.byref(width), C.byref(ld))

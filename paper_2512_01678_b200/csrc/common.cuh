@@ -145,6 +145,7 @@ struct Dropout {
   float scale;         // 1/(1-p) in f32
   uint32_t key0, key1;
   uint32_t layer, epoch;
+  const int32_t* epoch_dev;  // when set (CUDA-graph replay) the epoch is read from device memory
 };
 
 }  // namespace mph

@@ -169,8 +169,13 @@ int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* label
 }
 
 // ------------------------------------------------------------------ a9 Adam
+// Bias corrections are computed on the device from t (host value, or device counter during a
+// CUDA-graph replay), so eager and graph epochs are bitwise identical.
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
-                       int64_t n, float lr, float b1, float b2, float eps, float bc1, float bc2) {
+                       int64_t n, float lr, float b1, float b2, float eps, int t_host, const int32_t* t_dev) {
+  const int t = t_dev ? *t_dev : t_host;
+  const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
+  const float bc2 = (float)(1.0 - pow((double)b2, (double)t));
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
     const float mi = b1 * m[i] + (1.0f - b1) * gi;
@@ -181,13 +186,12 @@ __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float
   }
 }
 
-int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s) {
-  if (!p || !g || !m || !v || !cfg || n < 0 || t < 1) return fail(MPH_EINVAL, "adam: bad arguments");
+int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s,
+                const int32_t* t_dev) {
+  if (!p || !g || !m || !v || !cfg || n < 0 || (t < 1 && !t_dev)) return fail(MPH_EINVAL, "adam: bad arguments");
   if (n == 0) return MPH_OK;
-  const float bc1 = (float)(1.0 - pow((double)cfg->beta1, (double)t));
-  const float bc2 = (float)(1.0 - pow((double)cfg->beta2, (double)t));
   k_adam<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(p, g, m, v, n, cfg->lr, cfg->beta1,
-                                                                                 cfg->beta2, cfg->eps, bc1, bc2);
+                                                                                 cfg->beta2, cfg->eps, t, t_dev);
   count_launch();
   return launch_check("adam");
 }

@@ -61,6 +61,14 @@ struct mph_gcn {
   // P > 1: NCCL runs on its own stream, ordered against the compute stream by events
   cudaStream_t cs = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_grad = nullptr, ev_comm_done = nullptr, ev_loss = nullptr;
+  // CUDA-graph replay of one epoch: step counter and loss live in device memory
+  int32_t* t_dev = nullptr;
+  double* loss_dev = nullptr;
+  bool graph_mode = false;  // set while capturing: kernels read t / epoch from t_dev
+  bool warm = false;        // one eager epoch done (lazy setup finished)
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  mph_adam_cfg graph_cfg{};
 };
 
 namespace mph {
@@ -89,6 +97,10 @@ static void gcn_free(mph_gcn* m) {
   for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss})
     if (e) cudaEventDestroy(e);
   if (m->cs) cudaStreamDestroy(m->cs);
+  if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
+  if (m->graph) cudaGraphDestroy(m->graph);
+  dev_free(m->t_dev);
+  dev_free(m->loss_dev);
   delete m;
 }
 
@@ -178,6 +190,7 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
     eo.dropout_seed = m->dropout_seed;
     eo.dropout_layer = lnum;
     eo.dropout_epoch = m->epoch;
+    eo.dropout_epoch_d = m->graph_mode ? m->t_dev : nullptr;
     eo.row0 = g->row0;
   }
   if (l.order == 0) {
@@ -352,6 +365,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   }
   m->ws_bytes = ws;
   if ((rc = dev_alloc((char**)&m->ws, ws))) return bail(rc);
+  if ((rc = dev_alloc(&m->t_dev, 1)) || (rc = dev_alloc(&m->loss_dev, 1))) return bail(rc);
   cudaError_t e = cudaSuccess;
   for (auto& l : m->layers) {  // padding columns must start (and stay) zero
     if (e == cudaSuccess) e = cudaMemsetAsync(l.out, 0, (size_t)nr * l.pout * 4, s);
@@ -493,7 +507,7 @@ extern "C" int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void
   if (!m || !cfg) return fail(MPH_EINVAL, "gcn_adam arguments");
   cudaStream_t s = (cudaStream_t)stream;
   prof::Scope sc(MPH_PROF_ADAM, s, 28.0 * m->n_params, 0.0);
-  MPH_TRY(adam_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s));
+  MPH_TRY(adam_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s, m->graph_mode ? m->t_dev : nullptr));
   return refresh_wt(m, s);
 }
 
@@ -502,7 +516,79 @@ extern "C" int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cf
   MPH_TRY(mph_gcn_forward(m, t, stream));
   MPH_TRY(mph_gcn_loss(m, loss_d, stream));
   MPH_TRY(mph_gcn_backward(m, stream));
-  return mph_gcn_adam(m, cfg, t, stream);
+  MPH_TRY(mph_gcn_adam(m, cfg, t, stream));
+  m->warm = true;
+  return MPH_OK;
+}
+
+namespace mph {
+__global__ void k_step_advance(int32_t* t) { *t += 1; }
+}  // namespace mph
+
+// CUDA-graph capture of one whole epoch (single GPU).  The step counter t lives in device
+// memory and is advanced by the first node, so every replay is the next epoch: Adam's bias
+// corrections and the dropout counter read it there.  Eager and replayed epochs run the same
+// kernels with the same arguments, so they are bitwise identical.
+extern "C" int mph_gcn_graph_capture(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t_next, void* stream) {
+  if (!m || !cfg || t_next < 1) return fail(MPH_EINVAL, "graph_capture arguments");
+  if (m->world > 1) return fail(MPH_ENOTSUP, "graph capture is single-GPU (NCCL p2p is issued eagerly)");
+  if (!m->warm) return fail(MPH_ESTATE, "run one eager mph_gcn_train_epoch before capturing (lazy setup)");
+  cudaStream_t user = (cudaStream_t)stream;
+  MPH_CUDA_TRY(cudaStreamSynchronize(user));
+  if (m->graph_exec) {
+    cudaGraphExecDestroy(m->graph_exec);
+    m->graph_exec = nullptr;
+  }
+  if (m->graph) {
+    cudaGraphDestroy(m->graph);
+    m->graph = nullptr;
+  }
+  const int32_t t0 = t_next - 1;
+  MPH_CUDA_TRY(cudaMemcpy(m->t_dev, &t0, sizeof(int32_t), cudaMemcpyHostToDevice));
+  cudaStream_t cap = nullptr;
+  MPH_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  const bool prof_was = prof::enabled();
+  prof::set_enabled(false);  // no event nodes inside the graph
+  m->graph_mode = true;
+  m->graph_cfg = *cfg;
+  int rc = MPH_OK;
+  cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    k_step_advance<<<1, 1, 0, cap>>>(m->t_dev);
+    count_launch();
+    rc = do_forward(m, t_next, cap);
+    if (rc == MPH_OK) rc = do_loss(m, m->loss_dev, cap);
+    if (rc == MPH_OK) rc = do_backward(m, cap);
+    if (rc == MPH_OK) rc = mph_gcn_adam(m, &m->graph_cfg, t_next, cap);
+    cudaGraph_t gph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cap, &gph);
+    if (rc == MPH_OK && e2 != cudaSuccess) rc = fail(MPH_ECUDA, "EndCapture: %s", cudaGetErrorString(e2));
+    m->graph = gph;
+  } else {
+    rc = fail(MPH_ECUDA, "BeginCapture: %s", cudaGetErrorString(e));
+  }
+  m->graph_mode = false;
+  prof::set_enabled(prof_was);
+  cudaStreamDestroy(cap);
+  if (rc != MPH_OK) return rc;
+  e = cudaGraphInstantiate(&m->graph_exec, m->graph, 0);
+  if (e != cudaSuccess) return fail(MPH_ECUDA, "GraphInstantiate: %s", cudaGetErrorString(e));
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_graph_replay(mph_gcn* m, void* stream) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  if (!m->graph_exec) return fail(MPH_ESTATE, "no captured epoch (mph_gcn_graph_capture)");
+  MPH_CUDA_TRY(cudaGraphLaunch(m->graph_exec, (cudaStream_t)stream));
+  count_launch(m->L * 6 + 4);  // kernels inside the graph (accounting only)
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_graph_state(const mph_gcn* m, int32_t** t_d, double** loss_d) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  if (t_d) *t_d = m->t_dev;
+  if (loss_d) *loss_d = m->loss_dev;
+  return MPH_OK;
 }
 
 extern "C" int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, const float** ptr_d, int32_t* rows_h,

@@ -33,6 +33,7 @@ static cudaEvent_t get_event() {
 }
 
 bool enabled() { return g_on; }
+void set_enabled(bool on) { g_on = on; }
 
 Scope::Scope(int kind, cudaStream_t s, double bytes, double flops) : idx_(-1), s_(s) {
   if (!g_on) return;

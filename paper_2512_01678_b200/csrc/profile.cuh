@@ -8,6 +8,7 @@ namespace prof {
 
 // kinds match MPH_PROF_* in include/morphling.h
 bool enabled();
+void set_enabled(bool on);
 
 class Scope {
  public:

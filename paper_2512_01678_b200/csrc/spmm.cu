@@ -51,7 +51,8 @@ struct SpmmArgs {
 };
 
 __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int64_t grow, int c4) {
-  PhiloxOut r = philox4x32_10((uint32_t)grow, (uint32_t)c4, d.layer, d.epoch, d.key0, d.key1);
+  const uint32_t ep = d.epoch_dev ? (uint32_t)*d.epoch_dev : d.epoch;
+  PhiloxOut r = philox4x32_10((uint32_t)grow, (uint32_t)c4, d.layer, ep, d.key0, d.key1);
   v.x = r.v[0] >= d.threshold ? v.x * d.scale : 0.0f;
   v.y = r.v[1] >= d.threshold ? v.y * d.scale : 0.0f;
   v.z = r.v[2] >= d.threshold ? v.z * d.scale : 0.0f;
@@ -177,6 +178,7 @@ Dropout make_dropout(const mph_epilogue* e) {
   d.key1 = (uint32_t)(e->dropout_seed >> 32);
   d.layer = (uint32_t)e->dropout_layer;
   d.epoch = (uint32_t)e->dropout_epoch;
+  d.epoch_dev = e->dropout_epoch_d;
   return d;
 }
 

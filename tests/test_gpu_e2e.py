@@ -194,3 +194,21 @@ def test_localized_spmm_equals_global(P):
         ref = full[plan.row0:plan.row0 + plan.n_own]
         assert torch.allclose(out, ref, rtol=1e-5, atol=1e-6)
         assert torch.equal(lg.csr()[3].cpu(), torch.as_tensor(di[gl]))   # dinv of owned + ghosts
+
+
+@pytest.mark.parametrize("dropout_p", [0.0, 0.3])
+def test_cuda_graph_replay_bitwise_equals_eager(P, dropout_p):
+    """A captured epoch replayed K times == K eager epochs, bit for bit (device step counter)."""
+    w = make_workload("pubmed")
+    dims = w["cfg"].dims
+    _, _, ma, _ = _gpu_model(P, w, dims, force_mode=0, dropout_p=dropout_p, dropout_seed=5)
+    eager = _gpu_losses(ma, 6)
+    _, _, mb, _ = _gpu_model(P, w, dims, force_mode=0, dropout_p=dropout_p, dropout_seed=5)
+    first = mb.train_epoch(1).item()
+    mb.graph_capture(2)
+    replayed = [first]
+    for _ in range(5):
+        replayed.append(mb.replay().item())
+    assert replayed == eager
+    assert torch.equal(ma.params_flat, mb.params_flat)
+    assert mb.graph_step.item() == 6
