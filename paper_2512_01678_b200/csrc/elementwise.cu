@@ -290,15 +290,24 @@ __global__ void k_sparse_xw(const int64_t* ptr, const int32_t* idx, const float*
       const int nb = (int)min((int64_t)32, e - b);
       const int kk = lane < nb ? idx[b + lane] : 0;
       const float xx = lane < nb ? val[b + lane] : 0.0f;
-      for (int t = 0; t < nb; ++t) {
-        const int k = __shfl_sync(0xffffffffu, kk, t);
-        const float x = __shfl_sync(0xffffffffu, xx, t);
-        const float* wr = W + (int64_t)k * ldw;
+      for (int t = 0; t < nb; t += 4) {  // four independent W-row loads in flight
+        float w[4][8];
+        float x[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int c = lane + 32 * j;
-          if (c < F_out) acc[j] = fmaf(x, __ldg(wr + c), acc[j]);
+        for (int u = 0; u < 4; ++u) {
+          const int k = __shfl_sync(0xffffffffu, kk, (t + u) & 31);
+          x[u] = t + u < nb ? __shfl_sync(0xffffffffu, xx, (t + u) & 31) : 0.0f;
+          const float* wr = W + (int64_t)k * ldw;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = lane + 32 * j;
+            w[u][j] = (c < F_out && t + u < nb) ? __ldg(wr + c) : 0.0f;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = fmaf(x[u], w[u][j], acc[j]);
       }
     }
     const float rs = row_scale ? row_scale[i] : 1.0f;
@@ -310,37 +319,61 @@ __global__ void k_sparse_xw(const int64_t* ptr, const int32_t* idx, const float*
   }
 }
 
-// a7 (Alg. 1 Backward SpMM_Col(X_csc, G); thread-local accumulation without
-// atomics P:229): warp per feature column k, gathering the G rows of its nonzeros.
-__global__ void k_sparse_xtg(const int64_t* cptr, const int32_t* ridx, const float* cval, int F, const float* G,
-                             int F_out, int ldg, float* dW, int lddw) {
+// a7 (Alg. 1 Backward SpMM_Col(X_csc, G); "thread-local buffers before a final
+// reduction" without atomics): each column of X is cut into segments of at most
+// kSegNnz nonzeros (built once per feature set); a warp per segment gathers the G rows of its
+// nonzeros into a partial row, then the partials of each column are summed in segment order.
+__global__ void k_sparse_xtg_seg(const int32_t* seg_col, const int64_t* seg_begin, const int64_t* cptr,
+                                 const int32_t* ridx, const float* cval, int64_t n_seg, const float* G, int F_out,
+                                 int ldg, float* part) {
   const int lane = threadIdx.x & 31;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < F; k += nwarps) {
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sg = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < n_seg; sg += nwarps) {
+    const int k = seg_col[sg];
+    const int64_t s = seg_begin[sg], e = min(cptr[k + 1], s + kSegNnz);
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.0f;
-    const int64_t s = cptr[k], e = cptr[k + 1];
     for (int64_t b = s; b < e; b += 32) {
       const int nb = (int)min((int64_t)32, e - b);
       const int ii = lane < nb ? ridx[b + lane] : 0;
       const float xx = lane < nb ? cval[b + lane] : 0.0f;
-      for (int t = 0; t < nb; ++t) {
-        const int i = __shfl_sync(0xffffffffu, ii, t);
-        const float x = __shfl_sync(0xffffffffu, xx, t);
-        const float* gr = G + (int64_t)i * ldg;
+      for (int t = 0; t < nb; t += 4) {
+        float g[4][8];
+        float x[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int c = lane + 32 * j;
-          if (c < F_out) acc[j] = fmaf(x, __ldg(gr + c), acc[j]);
+        for (int u = 0; u < 4; ++u) {
+          const int i = __shfl_sync(0xffffffffu, ii, (t + u) & 31);
+          x[u] = t + u < nb ? __shfl_sync(0xffffffffu, xx, (t + u) & 31) : 0.0f;
+          const float* gr = G + (int64_t)i * ldg;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = lane + 32 * j;
+            g[u][j] = (c < F_out && t + u < nb) ? __ldg(gr + c) : 0.0f;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = fmaf(x[u], g[u][j], acc[j]);
       }
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int c = lane + 32 * j;
-      if (c < F_out) dW[(int64_t)k * lddw + c] = acc[j];
+      if (c < F_out) part[sg * F_out + c] = acc[j];
     }
+  }
+}
+
+__global__ void k_sparse_xtg_sum(const int64_t* col_seg0, int F, const float* part, int F_out, float* dW, int lddw) {
+  const int64_t total = (int64_t)F * F_out;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / F_out;
+    const int c = (int)(t - k * F_out);
+    float acc = 0.0f;
+    for (int64_t sg = col_seg0[k]; sg < col_seg0[k + 1]; ++sg) acc += part[sg * F_out + c];
+    dW[k * lddw + c] = acc;
   }
 }
 
@@ -355,13 +388,28 @@ int sparse_xw_launch(const mph_features* f, const float* W, int F_out, int ldw, 
   return launch_check("sparse_xw");
 }
 
-int sparse_xtg_launch(const mph_features* f, const float* G, int F_out, int ldg, float* dW, int lddw, cudaStream_t s) {
-  if (!f || !G || !dW || F_out <= 0 || ldg < F_out || lddw < F_out) return fail(MPH_EINVAL, "sparse_xtg: bad arguments");
-  if (f->mode != 1) return fail(MPH_ESTATE, "sparse_xtg: features are in dense mode");
+int sparse_xtg_launch(const mph_features* fc, const float* G, int F_out, int ldg, float* dW, int lddw, cudaStream_t s) {
+  if (!fc || !G || !dW || F_out <= 0 || ldg < F_out || lddw < F_out) return fail(MPH_EINVAL, "sparse_xtg: bad arguments");
+  if (fc->mode != 1) return fail(MPH_ESTATE, "sparse_xtg: features are in dense mode");
   if (F_out > 256) return fail(MPH_ENOTSUP, "sparse_xtg: F_out > 256");
-  const unsigned grid = (unsigned)std::max<int64_t>(1, ceil_div(f->F, 8));
-  k_sparse_xtg<<<grid, 256, 0, s>>>(f->csc_ptr, f->csc_idx, f->csc_val, f->F, G, F_out, ldg, dW, lddw);
-  count_launch();
+  mph_features* f = const_cast<mph_features*>(fc);
+  const size_t need = (size_t)std::max<int64_t>(f->n_seg, 1) * F_out;
+  if (need > f->part_cap) {  // partial rows: grows once, outside the steady state
+    dev_free(f->part);
+    f->part = nullptr;
+    f->part_cap = 0;
+    MPH_TRY(dev_alloc(&f->part, need));
+    f->part_cap = need;
+  }
+  if (f->n_seg > 0) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(f->n_seg, 8), 148 * 16));
+    k_sparse_xtg_seg<<<grid, 256, 0, s>>>(f->seg_col, f->seg_begin, f->csc_ptr, f->csc_idx, f->csc_val, f->n_seg, G,
+                                          F_out, ldg, f->part);
+  }
+  const int64_t total = (int64_t)f->F * F_out;
+  k_sparse_xtg_sum<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 16)), 256, 0, s>>>(
+      f->col_seg0, f->F, f->part, F_out, dW, lddw);
+  count_launch(2);
   return launch_check("sparse_xtg");
 }
 

@@ -4,6 +4,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -102,6 +103,10 @@ static void features_free(mph_features* f) {
   dev_free(f->csc_ptr);
   dev_free(f->csc_idx);
   dev_free(f->csc_val);
+  dev_free(f->seg_col);
+  dev_free(f->seg_begin);
+  dev_free(f->col_seg0);
+  dev_free(f->part);
   delete f;
 }
 
@@ -203,6 +208,31 @@ extern "C" int mph_features_create(const float* X_d, int32_t N, int32_t F, int32
   e = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_bail(e, "build");
+  if (f->mode == 1) {  // segments of <= kSegNnz nonzeros per CSC column (parallel, ordered dW reduction)
+    std::vector<int64_t> cptr((size_t)F + 1);
+    e = cudaMemcpy(cptr.data(), f->csc_ptr, cptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_bail(e, "segments");
+    std::vector<int32_t> sc;
+    std::vector<int64_t> sb, c0((size_t)F + 1);
+    for (int32_t k = 0; k < F; ++k) {
+      c0[k] = (int64_t)sc.size();
+      for (int64_t b = cptr[k]; b < cptr[k + 1]; b += kSegNnz) {
+        sc.push_back(k);
+        sb.push_back(b);
+      }
+    }
+    c0[F] = (int64_t)sc.size();
+    f->n_seg = (int64_t)sc.size();
+    if ((rc = dev_alloc(&f->col_seg0, (size_t)F + 1)) || (rc = dev_alloc(&f->seg_col, sc.size())) ||
+        (rc = dev_alloc(&f->seg_begin, sb.size())))
+      return bail(rc);
+    e = cudaMemcpy(f->col_seg0, c0.data(), c0.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !sc.empty())
+      e = cudaMemcpy(f->seg_col, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !sb.empty())
+      e = cudaMemcpy(f->seg_begin, sb.data(), sb.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_bail(e, "segments upload");
+  }
   cleanup();
   *out = f;
   return MPH_OK;

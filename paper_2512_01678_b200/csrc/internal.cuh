@@ -41,7 +41,16 @@ struct mph_features {
   int64_t* csc_ptr = nullptr;
   int32_t* csc_idx = nullptr;
   float* csc_val = nullptr;
+  // X_csc cut into segments of <= kSegNnz nonzeros per column (sparse-path dW, elementwise.cu)
+  int64_t n_seg = 0;
+  int32_t* seg_col = nullptr;
+  int64_t* seg_begin = nullptr;
+  int64_t* col_seg0 = nullptr;  // [F+1] first segment of each column
+  float* part = nullptr;
+  size_t part_cap = 0;
 };
+
+constexpr int64_t kSegNnz = 128;
 
 namespace mph {
 
