@@ -95,6 +95,16 @@ int mph_graph_destroy(mph_graph* g);
 typedef struct mph_features mph_features;
 int mph_features_create(const float* X_d, int32_t N, int32_t F, int32_t ld, int32_t tau_bp,
                         int32_t force_mode, void* stream, mph_features** out);
+/* Same switch from a HOST CSR matrix, for feature matrices too large to hold densely (NELL:
+ * 65,755 x 61,278 at s = 99.21%).  ptr_h[N+1] (int64, ptr_h[0] = 0,
+ * monotone), idx_h[ptr_h[N]] (int32 columns in [0,F), strictly ascending within each row: S3),
+ * val_h[ptr_h[N]] (fp32).  Explicit zeros are dropped (S1 counts x != 0 only), so nnz and the
+ * stored pattern equal what mph_features_create would give on the densified matrix.  Sparse mode
+ * uploads X_csr and builds X_csc + segments on the device; dense mode scatters into the padded
+ * copy.  Host arrays are only read during the call (pageable or pinned).  MPH_EINVAL on a
+ * malformed CSR (nothing allocated).  Synchronises. */
+int mph_features_create_csr(const int64_t* ptr_h, const int32_t* idx_h, const float* val_h, int32_t N,
+                            int32_t F, int32_t tau_bp, int32_t force_mode, void* stream, mph_features** out);
 int mph_features_info(const mph_features* f, int64_t* nnz_h, int32_t* mode_h, int32_t* is_binary_h);
 /* Borrowed device views (sparse mode only; MPH_ESTATE in dense mode). */
 int mph_features_csr(const mph_features* f, const int64_t** ptr_d, const int32_t** idx_d, const float** val_d);

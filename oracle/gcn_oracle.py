@@ -136,7 +136,31 @@ class FeatureAnalysis:
     csc: tuple | None      # (ptr int64[F+1], idx int32[nnz] rows ascending, val f32[nnz])
 
 
-def analyze_features(X: np.ndarray, tau_bp: int = 8000, force_mode: int = -1) -> FeatureAnalysis:
+def analyze_features(X, tau_bp: int = 8000, force_mode: int = -1) -> FeatureAnalysis:
+    if sp.issparse(X):  # CSR input (NELL-scale features): the same S1-S3 on the stored entries
+        X = sp.csr_matrix(X, dtype=np.float32)
+        n, f = X.shape
+        if n * f == 0:
+            raise OracleError("EDEGENERATE", "N*F = 0")
+        keep = X.data != np.float32(0.0)                                        # S1
+        rows = np.repeat(np.arange(n), np.diff(X.indptr))[keep]
+        cols = X.indices[keep].astype(np.int64)
+        vals = X.data[keep]
+        order = np.lexsort((cols, rows))
+        rows, cols, vals = rows[order], cols[order], vals[order]
+        nnz = int(vals.size)
+        sparse = 10000 * nnz <= (10000 - int(tau_bp)) * n * f                  # S2
+        mode = int(sparse) if force_mode < 0 else int(force_mode)
+        csr = csc = None
+        if mode == 1:                                                          # S3
+            ptr = np.zeros(n + 1, np.int64)
+            np.cumsum(np.bincount(rows, minlength=n), out=ptr[1:])
+            csr = (ptr, cols.astype(np.int32), vals.astype(np.float32))
+            o2 = np.lexsort((rows, cols))
+            cptr = np.zeros(f + 1, np.int64)
+            np.cumsum(np.bincount(cols, minlength=f), out=cptr[1:])
+            csc = (cptr, rows[o2].astype(np.int32), vals[o2].astype(np.float32))
+        return FeatureAnalysis(nnz, mode, bool(np.all(vals == np.float32(1.0))), 1.0 - nnz / (n * f), csr, csc)
     X = np.asarray(X, dtype=np.float32)
     n, f = X.shape
     if n * f == 0:
@@ -250,7 +274,8 @@ def dropout_keep(n_rows: int, n_cols: int, p: float, seed: int, layer: int, epoc
 # Q8 (ReLU hidden, identity output), Q10 (dropout after ReLU).
 # ---------------------------------------------------------------------------
 def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1):
-    H = np.asarray(X, dtype=np.float64)
+    # X may be a scipy CSR matrix (sparse features): X·W_1 and X^T·G are then sparse products
+    H = X.astype(np.float64).tocsr() if sp.issparse(X) else np.asarray(X, dtype=np.float64)
     hs, zs = [H], []
     L = len(Ws)
     for l in range(1, L + 1):

@@ -61,6 +61,7 @@ _SIGS = {
     "mph_graph_csr": [P, PP, PP, PP, PP],
     "mph_graph_destroy": [P],
     "mph_features_create": [P, i32, i32, i32, i32, i32, P, PP],
+    "mph_features_create_csr": [P, P, P, i32, i32, i32, i32, P, PP],
     "mph_features_info": [P, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)],
     "mph_features_csr": [P, PP, PP, PP],
     "mph_features_csc": [P, PP, PP, PP],

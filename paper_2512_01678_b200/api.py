@@ -108,11 +108,30 @@ class Features:
         h = _out_ptr()
         L.mph_features_create(X.data_ptr(), X.shape[0], X.shape[1], X.stride(0), tau_bp, force_mode,
                               stream_ptr(stream), C.byref(h))
+        self._attach(h, X.shape[0], X.shape[1])
+
+    def _attach(self, h, N: int, F: int):
         self.h = h
-        self.N, self.F = X.shape
+        self.N, self.F = N, F
         nnz, mode, binary = C.c_int64(), C.c_int32(), C.c_int32()
         L.mph_features_info(h, C.byref(nnz), C.byref(mode), C.byref(binary))
         self.nnz, self.mode, self.is_binary = nnz.value, mode.value, bool(binary.value)
+
+    @classmethod
+    def from_csr(cls, ptr: np.ndarray, idx: np.ndarray, val: np.ndarray, shape, tau_bp: int = 8000,
+                 force_mode: int = -1, stream=None) -> "Features":
+        """a1 from a host CSR matrix (mph_features_create_csr): NELL-sized X never densified."""
+        p = np.ascontiguousarray(ptr, dtype=np.int64)
+        i = np.ascontiguousarray(idx, dtype=np.int32)
+        v = np.ascontiguousarray(val, dtype=np.float32)
+        N, F = int(shape[0]), int(shape[1])
+        assert p.shape == (N + 1,) and i.shape == v.shape
+        h = _out_ptr()
+        L.mph_features_create_csr(p.ctypes.data, i.ctypes.data, v.ctypes.data, N, F, tau_bp, force_mode,
+                                  stream_ptr(stream), C.byref(h))
+        self = cls.__new__(cls)
+        self._attach(h, N, F)
+        return self
 
     def csr(self):
         p, i, v = C.c_void_p(), C.c_void_p(), C.c_void_p()

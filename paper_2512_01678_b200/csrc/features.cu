@@ -94,6 +94,74 @@ __global__ void k_pad_copy(const float* X, int32_t N, int32_t F, int32_t ld, flo
   }
 }
 
+// X_csc from X_csr (sort of (col << 32 | row) keys, values carried along), then the per-column
+// segments of <= kSegNnz nonzeros used by the sparse dW kernel.  Synchronises.
+static int csc_from_csr(mph_features* f, cudaStream_t s) {
+  const int64_t nnz = f->nnz;
+  const int32_t N = f->N, F = f->F;
+  uint64_t *keys = nullptr, *keys2 = nullptr;
+  void* tmp = nullptr;
+  int rc = MPH_OK;
+  auto done = [&](int code) {
+    dev_free(keys);
+    dev_free(keys2);
+    dev_free(tmp);
+    return code;
+  };
+  cudaError_t e = cudaSuccess;
+  if (nnz > 0) {
+    if ((rc = dev_alloc(&keys, (size_t)nnz)) || (rc = dev_alloc(&keys2, (size_t)nnz))) return done(rc);
+    const unsigned warps_grid = (unsigned)std::min<int64_t>(ceil_div((int64_t)N * 32, 256), 148 * 32);
+    k_csc_keys<<<warps_grid, 256, 0, s>>>(f->csr_ptr, f->csr_idx, N, keys);
+    count_launch();
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, keys2, f->csr_val, f->csc_val, nnz, 0, 64, s);
+    if ((rc = dev_alloc((char**)&tmp, tb))) return done(rc);
+    e = cub::DeviceRadixSort::SortPairs(tmp, tb, keys, keys2, f->csr_val, f->csc_val, nnz, 0, 64, s);
+    count_launch();
+    if (e != cudaSuccess) return done(fail(MPH_ECUDA, "csc sort: %s", cudaGetErrorString(e)));
+    k_csc_split<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), 4096), 256, 0, s>>>(keys2, nnz, f->csc_idx);
+    count_launch();
+  }
+  k_col_ptr<<<(unsigned)ceil_div((int64_t)F + 1, 256), 256, 0, s>>>(keys2 ? keys2 : keys, nnz, F, f->csc_ptr);
+  count_launch();
+  e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return done(fail(MPH_ECUDA, "csc build: %s", cudaGetErrorString(e)));
+  std::vector<int64_t> cptr((size_t)F + 1);
+  e = cudaMemcpy(cptr.data(), f->csc_ptr, cptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return done(fail(MPH_ECUDA, "segments: %s", cudaGetErrorString(e)));
+  std::vector<int32_t> sc;
+  std::vector<int64_t> sb, c0((size_t)F + 1);
+  for (int32_t k = 0; k < F; ++k) {
+    c0[k] = (int64_t)sc.size();
+    for (int64_t b = cptr[k]; b < cptr[k + 1]; b += kSegNnz) {
+      sc.push_back(k);
+      sb.push_back(b);
+    }
+  }
+  c0[F] = (int64_t)sc.size();
+  f->n_seg = (int64_t)sc.size();
+  if ((rc = dev_alloc(&f->col_seg0, (size_t)F + 1)) || (rc = dev_alloc(&f->seg_col, sc.size())) ||
+      (rc = dev_alloc(&f->seg_begin, sb.size())))
+    return done(rc);
+  e = cudaMemcpy(f->col_seg0, c0.data(), c0.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !sc.empty())
+    e = cudaMemcpy(f->seg_col, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !sb.empty())
+    e = cudaMemcpy(f->seg_begin, sb.data(), sb.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return done(fail(MPH_ECUDA, "segments upload: %s", cudaGetErrorString(e)));
+  return done(MPH_OK);
+}
+
+// Dense padded copy from CSR: warp per row scatters its entries.
+__global__ void k_csr_scatter(const int64_t* ptr, const int32_t* idx, const float* val, int32_t N, float* X, int32_t P) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nwarps)
+    for (int64_t e = ptr[i] + lane; e < ptr[i + 1]; e += 32) X[i * P + idx[e]] = val[e];
+}
+
 static void features_free(mph_features* f) {
   if (!f) return;
   dev_free(f->X);
@@ -126,17 +194,12 @@ extern "C" int mph_features_create(const float* X_d, int32_t N, int32_t F, int32
   f->N = N;
   f->F = F;
   int64_t *row_nnz = nullptr, *row_nu = nullptr, *sums = nullptr;
-  uint64_t *keys = nullptr, *keys2 = nullptr;
-  float* vals2 = nullptr;
   void* tmp = nullptr;
   int rc = MPH_OK;
   auto cleanup = [&]() {
     dev_free(row_nnz);
     dev_free(row_nu);
     dev_free(sums);
-    dev_free(keys);
-    dev_free(keys2);
-    dev_free(vals2);
     dev_free(tmp);
   };
   auto bail = [&](int code) {
@@ -152,7 +215,7 @@ extern "C" int mph_features_create(const float* X_d, int32_t N, int32_t F, int32
   const unsigned warps_grid = (unsigned)std::min<int64_t>(ceil_div((int64_t)N * 32, 256), 148 * 32);
   k_row_counts<<<warps_grid, 256, 0, s>>>(X_d, N, F, ld, row_nnz, row_nu);
   count_launch();
-  size_t tb = 0, tb2 = 0, tb3 = 0;
+  size_t tb = 0, tb2 = 0;
   cub::DeviceReduce::Sum(nullptr, tb, row_nnz, sums, N, s);
   cub::DeviceScan::ExclusiveSum(nullptr, tb2, row_nnz, row_nnz, N, s);
   if ((rc = dev_alloc((char**)&tmp, std::max(tb, tb2)))) return bail(rc);
@@ -186,54 +249,125 @@ extern "C" int mph_features_create(const float* X_d, int32_t N, int32_t F, int32
     if (e != cudaSuccess) return cuda_bail(e, "scan");
     k_fill_csr<<<warps_grid, 256, 0, s>>>(X_d, N, F, ld, f->csr_ptr, f->csr_idx, f->csr_val);
     count_launch();
-    if (nnz > 0) {
-      if ((rc = dev_alloc(&keys, (size_t)nnz)) || (rc = dev_alloc(&keys2, (size_t)nnz)) ||
-          (rc = dev_alloc(&vals2, (size_t)nnz)))
-        return bail(rc);
-      k_csc_keys<<<warps_grid, 256, 0, s>>>(f->csr_ptr, f->csr_idx, N, keys);
-      count_launch();
-      cub::DeviceRadixSort::SortPairs(nullptr, tb3, keys, keys2, f->csr_val, f->csc_val, nnz, 0, 64, s);
-      dev_free(tmp);
-      tmp = nullptr;
-      if ((rc = dev_alloc((char**)&tmp, tb3))) return bail(rc);
-      e = cub::DeviceRadixSort::SortPairs(tmp, tb3, keys, keys2, f->csr_val, f->csc_val, nnz, 0, 64, s);
-      count_launch();
-      if (e != cudaSuccess) return cuda_bail(e, "csc sort");
-      k_csc_split<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), 4096), 256, 0, s>>>(keys2, nnz, f->csc_idx);
-      count_launch();
-    }
-    k_col_ptr<<<(unsigned)ceil_div((int64_t)F + 1, 256), 256, 0, s>>>(keys2 ? keys2 : keys, nnz, F, f->csc_ptr);
-    count_launch();
+    if ((rc = csc_from_csr(f, s))) return bail(rc);
   }
   e = cudaStreamSynchronize(s);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_bail(e, "build");
-  if (f->mode == 1) {  // segments of <= kSegNnz nonzeros per CSC column (parallel, ordered dW reduction)
-    std::vector<int64_t> cptr((size_t)F + 1);
-    e = cudaMemcpy(cptr.data(), f->csc_ptr, cptr.size() * sizeof(int64_t), cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return cuda_bail(e, "segments");
-    std::vector<int32_t> sc;
-    std::vector<int64_t> sb, c0((size_t)F + 1);
-    for (int32_t k = 0; k < F; ++k) {
-      c0[k] = (int64_t)sc.size();
-      for (int64_t b = cptr[k]; b < cptr[k + 1]; b += kSegNnz) {
-        sc.push_back(k);
-        sb.push_back(b);
+  cleanup();
+  *out = f;
+  return MPH_OK;
+}
+
+extern "C" int mph_features_create_csr(const int64_t* ptr_h, const int32_t* idx_h, const float* val_h, int32_t N,
+                                       int32_t F, int32_t tau_bp, int32_t force_mode, void* stream,
+                                       mph_features** out) {
+  if (!out) return fail(MPH_EINVAL, "null out");
+  *out = nullptr;
+  if (N <= 0 || F <= 0) return fail(MPH_EDEGENERATE, "N*F = 0");
+  if (!ptr_h || tau_bp < 0 || tau_bp > 10000 || force_mode < -1 || force_mode > 1)
+    return fail(MPH_EINVAL, "features_create_csr arguments");
+  const int64_t m = ptr_h[N];
+  if (ptr_h[0] != 0 || m < 0 || (m > 0 && (!idx_h || !val_h))) return fail(MPH_EINVAL, "features_create_csr: bad row_ptr");
+  // Host validation (S3: columns strictly ascending within a row) and the S1 count of nonzeros:
+  // explicit zeros in val are not entries of X_csr, so they are dropped.
+  int64_t nnz = 0, nonunit = 0;
+  bool has_zeros = false;
+  for (int32_t i = 0; i < N; ++i) {
+    if (ptr_h[i + 1] < ptr_h[i]) return fail(MPH_EINVAL, "features_create_csr: row_ptr not monotone at %d", i);
+    for (int64_t e = ptr_h[i]; e < ptr_h[i + 1]; ++e) {
+      if (idx_h[e] < 0 || idx_h[e] >= F || (e > ptr_h[i] && idx_h[e] <= idx_h[e - 1]))
+        return fail(MPH_EINVAL, "features_create_csr: column index out of range or not ascending in row %d", i);
+      const float x = val_h[e];
+      if (x != 0.0f) {
+        ++nnz;
+        nonunit += (x != 1.0f);
+      } else {
+        has_zeros = true;
       }
     }
-    c0[F] = (int64_t)sc.size();
-    f->n_seg = (int64_t)sc.size();
-    if ((rc = dev_alloc(&f->col_seg0, (size_t)F + 1)) || (rc = dev_alloc(&f->seg_col, sc.size())) ||
-        (rc = dev_alloc(&f->seg_begin, sb.size())))
-      return bail(rc);
-    e = cudaMemcpy(f->col_seg0, c0.data(), c0.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !sc.empty())
-      e = cudaMemcpy(f->seg_col, sc.data(), sc.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !sb.empty())
-      e = cudaMemcpy(f->seg_begin, sb.data(), sb.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_bail(e, "segments upload");
   }
-  cleanup();
+  std::vector<int64_t> p2;
+  std::vector<int32_t> i2;
+  std::vector<float> v2;
+  const int64_t* P_h = ptr_h;
+  const int32_t* I_h = idx_h;
+  const float* V_h = val_h;
+  if (has_zeros) {
+    p2.resize((size_t)N + 1);
+    i2.reserve((size_t)nnz);
+    v2.reserve((size_t)nnz);
+    p2[0] = 0;
+    for (int32_t i = 0; i < N; ++i) {
+      for (int64_t e = ptr_h[i]; e < ptr_h[i + 1]; ++e)
+        if (val_h[e] != 0.0f) {
+          i2.push_back(idx_h[e]);
+          v2.push_back(val_h[e]);
+        }
+      p2[(size_t)i + 1] = (int64_t)i2.size();
+    }
+    P_h = p2.data();
+    I_h = i2.data();
+    V_h = v2.data();
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  mph_features* f = new mph_features();
+  f->N = N;
+  f->F = F;
+  f->nnz = nnz;
+  f->is_binary = (nonunit == 0);
+  const __int128 lhs = (__int128)10000 * nnz, rhs = (__int128)(10000 - tau_bp) * N * F;
+  f->mode = force_mode >= 0 ? force_mode : (lhs <= rhs ? 1 : 0);  // S2, as in mph_features_create
+  int rc = MPH_OK;
+  int64_t* tptr = nullptr;
+  int32_t* tidx = nullptr;
+  float* tval = nullptr;
+  auto bail = [&](int code) {
+    dev_free(tptr);
+    dev_free(tidx);
+    dev_free(tval);
+    features_free(f);
+    return code;
+  };
+  if (f->mode == 1) {
+    if ((rc = dev_alloc(&f->csr_ptr, (size_t)N + 1)) || (rc = dev_alloc(&f->csr_idx, (size_t)nnz)) ||
+        (rc = dev_alloc(&f->csr_val, (size_t)nnz)) || (rc = dev_alloc(&f->csc_ptr, (size_t)F + 1)) ||
+        (rc = dev_alloc(&f->csc_idx, (size_t)nnz)) || (rc = dev_alloc(&f->csc_val, (size_t)nnz)))
+      return bail(rc);
+    tptr = f->csr_ptr;
+    tidx = f->csr_idx;
+    tval = f->csr_val;
+  } else {
+    f->P = pad_width(F);
+    if ((rc = dev_alloc(&f->X, (size_t)N * f->P)) || (rc = dev_alloc(&tptr, (size_t)N + 1)) ||
+        (rc = dev_alloc(&tidx, (size_t)nnz)) || (rc = dev_alloc(&tval, (size_t)nnz)))
+      return bail(rc);
+  }
+  cudaError_t e = cudaMemcpyAsync(tptr, P_h, ((size_t)N + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(tidx, I_h, (size_t)nnz * sizeof(int32_t), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && nnz > 0) e = cudaMemcpyAsync(tval, V_h, (size_t)nnz * sizeof(float), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    if (f->mode == 1) tptr = nullptr, tidx = nullptr, tval = nullptr;
+    return bail(fail(MPH_ECUDA, "features_create_csr upload: %s", cudaGetErrorString(e)));
+  }
+  if (f->mode == 1) {
+    tptr = nullptr;  // owned by f from here on
+    tidx = nullptr;
+    tval = nullptr;
+    if ((rc = csc_from_csr(f, s))) return bail(rc);
+  } else {
+    e = cudaMemsetAsync(f->X, 0, (size_t)N * f->P * sizeof(float), s);
+    if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "features_create_csr memset: %s", cudaGetErrorString(e)));
+    const unsigned warps_grid = (unsigned)std::min<int64_t>(ceil_div((int64_t)N * 32, 256), 148 * 32);
+    k_csr_scatter<<<warps_grid, 256, 0, s>>>(tptr, tidx, tval, N, f->X, f->P);
+    count_launch();
+  }
+  e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "features_create_csr build: %s", cudaGetErrorString(e)));
+  dev_free(tptr);
+  dev_free(tidx);
+  dev_free(tval);
   *out = f;
   return MPH_OK;
 }

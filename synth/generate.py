@@ -199,11 +199,41 @@ def make_features(n: int, f: int, y: np.ndarray, c: int, kind: str, density: flo
     return np.where(mask, vals, np.float32(0.0)).astype(np.float32)
 
 
+def make_features_csr(n: int, f: int, y: np.ndarray, c: int, density: float, seed: int):
+    """Binary sparse features generated directly in CSR form (same mask recipe as
+    make_features, for shapes whose dense matrix would not fit host memory, e.g. NELL's
+    65,755 x 61,278).  Returns (ptr int64[n+1], idx int32 ascending per row, val f32 == 1)."""
+    rng = np.random.Generator(np.random.PCG64(seed + 7919))
+    p_hi = max(0.05, 2.0 * density)
+    p_lo = max(0.0, (density - p_hi / c) / (1.0 - 1.0 / c))
+    hot_cols = np.array([(f - 1 - yy) // c + 1 for yy in range(c)])     # columns k < f with k % c == y
+    n_hot = rng.binomial(hot_cols[y], p_hi)
+    n_cold = rng.binomial(f, p_lo, size=n)
+    rows_h = np.repeat(np.arange(n, dtype=np.int64), n_hot)
+    cols_h = y[rows_h].astype(np.int64) + c * (rng.random(rows_h.size) * hot_cols[y[rows_h]]).astype(np.int64)
+    rows_c = np.repeat(np.arange(n, dtype=np.int64), n_cold)
+    cols_c = rng.integers(0, f, size=rows_c.size, dtype=np.int64)
+    keys = _sorted_unique(np.concatenate([rows_h * f + cols_h, rows_c * f + cols_c]))
+    rows = keys // f
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=ptr[1:])
+    return ptr, (keys % f).astype(np.int32), np.ones(keys.size, dtype=np.float32)
+
+
+# NELL (the paper's headline sparse-feature dataset, Table P:635 and P:690: 65,755 nodes,
+# 251,550 edges, 61,278 features, 186 classes, feature sparsity 99.21 %) with the paper's model
+# (3 layers, hidden 32, P:655).  SURVEY §8(f) NEXT-2.  Features are produced as CSR.
+CONFIGS["nell"] = WorkloadConfig("nell", 65755, 251550, (61278, 32, 32, 186), "binary_csr", 0.0079, 2.5, 0.2, 6)
+
+
 def make_workload(name: str, feature_dtype=np.float32):
-    """Return dict(src, dst, X, y, cfg) for one of CONFIGS."""
+    """Return dict(src, dst, X, y, cfg) for one of CONFIGS (X_csr instead of X for CSR kinds)."""
     cfg = CONFIGS[name]
     y = make_labels(cfg.num_nodes, cfg.num_classes)
     src, dst = make_graph(cfg.num_nodes, cfg.nnz_a, cfg.num_classes, cfg.alpha, cfg.mu, cfg.seed)
+    if cfg.feature_kind == "binary_csr":
+        csr = make_features_csr(cfg.num_nodes, cfg.num_features, y, cfg.num_classes, cfg.density, cfg.seed)
+        return {"src": src, "dst": dst, "X": None, "X_csr": csr, "y": y, "cfg": cfg}
     x = make_features(cfg.num_nodes, cfg.num_features, y, cfg.num_classes, cfg.feature_kind, cfg.density, cfg.seed)
     return {"src": src, "dst": dst, "X": x.astype(feature_dtype, copy=False), "y": y, "cfg": cfg}
 

@@ -1,0 +1,113 @@
+"""a1 from a host CSR matrix (mph_features_create_csr) and the paper's headline sparse case:
+NELL-shaped X (65,755 x 61,278, s = 99.21%) that is never densified.
+
+* the CSR entry point gives the same mode / nnz / is_binary / X_csr / X_csc as the dense entry
+  point on the densified matrix (explicit zeros dropped, S1) — bit-exact (integer work);
+* malformed CSR is rejected with MPH_EINVAL;
+* at NELL's full size, X_csr / X_csc are bit-exact against the oracle's analysis and 10 epochs
+  of training follow the oracle's loss trajectory within 1e-3 (Q24).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+import oracle
+from synth.generate import make_workload
+from tests.gpu_helpers import cuda
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2512_01678_b200 as P
+    from paper_2512_01678_b200 import _lib as L
+    L.mph_device_check(C.byref(C.c_int32()))
+    return P
+
+
+def _random_csr(n, f, density, seed, zeros=True, binary=False):
+    rng = np.random.default_rng(seed)
+    X = (rng.random((n, f)) < density).astype(np.float32)
+    if not binary:
+        X *= rng.integers(1, 4, (n, f)).astype(np.float32)
+    M = sp.csr_matrix(X)
+    M.sort_indices()
+    ptr, idx, val = M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data.astype(np.float32)
+    if zeros:  # explicit zeros in every 7th stored entry: must not count (S1)
+        val = val.copy()
+        val[::7] = 0.0
+        X = sp.csr_matrix((val, idx, ptr), shape=(n, f)).toarray()
+    return X, ptr, idx, val
+
+
+@pytest.mark.parametrize("n,f,density,force", [(1000, 300, 0.05, -1), (700, 129, 0.3, -1), (500, 77, 0.02, 0),
+                                                (333, 1000, 0.01, 1)])
+def test_csr_entry_equals_dense_entry(P, n, f, density, force):
+    X, ptr, idx, val = _random_csr(n, f, density, seed=n + f)
+    a = P.Features(cuda(X), force_mode=force)
+    b = P.Features.from_csr(ptr, idx, val, (n, f), force_mode=force)
+    assert (a.nnz, a.mode, a.is_binary) == (b.nnz, b.mode, b.is_binary)
+    ref = oracle.analyze_features(X, 8000)
+    assert b.nnz == ref.nnz and (force >= 0 or b.mode == ref.mode)
+    if b.mode == 1:
+        for u, v in zip(a.csr() + a.csc(), b.csr() + b.csc()):
+            assert torch.equal(u, v)
+        for u, v in zip(b.csr() + b.csc(), oracle.analyze_features(X, 0).csr + oracle.analyze_features(X, 0).csc):
+            assert np.array_equal(u.cpu().numpy(), np.asarray(v).astype(u.cpu().numpy().dtype))
+    else:
+        assert torch.equal(a.dense(), b.dense())
+        assert np.array_equal(b.dense()[:, :f].cpu().numpy(), X)
+
+
+def test_csr_entry_rejects_malformed(P):
+    from paper_2512_01678_b200 import _lib as L
+    _, ptr, idx, val = _random_csr(50, 40, 0.2, seed=1, zeros=False)
+    bad_order = idx.copy()
+    r = int(np.argmax(np.diff(ptr) >= 2))
+    bad_order[ptr[r]], bad_order[ptr[r] + 1] = bad_order[ptr[r] + 1], bad_order[ptr[r]]
+    bad_range = idx.copy()
+    bad_range[0] = 40
+    bad_ptr = ptr.copy()
+    bad_ptr[5] = bad_ptr[6] + 1
+    for p, i in ((ptr, bad_order), (ptr, bad_range), (bad_ptr, idx)):
+        with pytest.raises(L.MorphlingError) as e:
+            P.Features.from_csr(p, i, val, (50, 40))
+        assert e.value.code == -1  # MPH_EINVAL
+
+
+@pytest.fixture(scope="module")
+def nell():
+    return make_workload("nell")
+
+
+def test_nell_full_size_csr_csc_bit_exact(P, nell):
+    ptr, idx, val = nell["X_csr"]
+    cfg = nell["cfg"]
+    f = P.Features.from_csr(ptr, idx, val, (cfg.num_nodes, cfg.num_features))
+    ref = oracle.analyze_features(sp.csr_matrix((val, idx, ptr), shape=(cfg.num_nodes, cfg.num_features)), 8000)
+    assert f.mode == 1 and ref.mode == 1 and f.is_binary and f.nnz == ref.nnz == val.size
+    for got, exp in zip(f.csr() + f.csc(), ref.csr + ref.csc):
+        got = got.cpu().numpy()
+        assert np.array_equal(got, np.asarray(exp).astype(got.dtype))
+
+
+def test_nell_loss_trajectory(P, nell):
+    ptr, idx, val = nell["X_csr"]
+    cfg = nell["cfg"]
+    dims = cfg.dims
+    g = P.Graph(nell["src"], nell["dst"], cfg.num_nodes)
+    f = P.Features.from_csr(ptr, idx, val, (cfg.num_nodes, cfg.num_features))
+    m = P.GCN(g, f, dims)
+    m.init_xavier(42)
+    m.set_labels(cuda(nell["y"].astype(np.int32)))
+    got = [m.train_epoch(t).item() for t in range(1, 11)]
+    rg = oracle.graph_build(nell["src"], nell["dst"], cfg.num_nodes)
+    X = sp.csr_matrix((val, idx, ptr), shape=(cfg.num_nodes, cfg.num_features))
+    ref, _ = oracle.train(rg, X, nell["y"], dims, epochs=10, seed=42)
+    for t, (a, b) in enumerate(zip(got, ref), 1):
+        assert abs(a - b) <= 1e-3 * max(1.0, abs(b)), f"epoch {t}: gpu {a} vs oracle {b}"
+    assert got[-1] < got[0]
