@@ -19,7 +19,7 @@ __all__ = [
     "OracleError", "Graph", "graph_build", "a_hat_values", "a_hat_dense_from_csr",
     "aggregate", "aggregate_rows", "analyze_features", "FeatureAnalysis",
     "splitmix64_stream", "xavier_init", "philox4x32_10", "dropout_keep",
-    "dropout_threshold", "forward", "softmax_ce", "backward", "adam_step", "train",
+    "dropout_threshold", "tf32_rna", "forward", "softmax_ce", "backward", "adam_step", "train",
     "partition_1d", "localize", "LocalPlan", "GOLDEN",
 ]
 
@@ -273,13 +273,38 @@ def dropout_keep(n_rows: int, n_cols: int, p: float, seed: int, layer: int, epoc
 # Forward (c.2 F1-F4): layer update of P:92 with Q1 (Â), Q6 (bias),
 # Q8 (ReLU hidden, identity output), Q10 (dropout after ReLU).
 # ---------------------------------------------------------------------------
-def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1):
-    # X may be a scipy CSR matrix (sparse features): X·W_1 and X^T·G are then sparse products
+def tf32_rna(x) -> np.ndarray:
+    """TF32 operand rounding (reading R2; north_star "TF32 in, FP32 accumulate"): the value as an
+    fp32 number with its 23-bit mantissa rounded to TF32's 10 bits, to nearest, ties away from
+    zero (PTX cvt.rna.tf32.f32).  Sign-magnitude layout: adding half an ulp (bit 12) to the
+    magnitude bits and clearing the low 13 bits rounds |x| half-up.  Finite inputs only."""
+    a = np.array(x, dtype=np.float32, copy=True)
+    u = a.view(np.uint32)
+    u += np.uint32(0x1000)
+    u &= np.uint32(0xFFFFE000)
+    return a.astype(np.float64)
+
+
+def _operand(M, rounding):
+    """A dense GEMM operand as the tensor core sees it (identity unless rounding == "tf32")."""
+    if rounding is None or sp.issparse(M):
+        return M
+    if rounding != "tf32":
+        raise ValueError(rounding)
+    return tf32_rna(M)
+
+
+def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1, operand_rounding=None):
+    # X may be a scipy CSR matrix (sparse features): X·W_1 and X^T·G are then sparse products.
+    # operand_rounding="tf32" rounds both operands of every dense product H·W (R2); sparse products
+    # (X_csr·W_1) and the aggregation stay exact.  It models transform-first layers.
     H = X.astype(np.float64).tocsr() if sp.issparse(X) else np.asarray(X, dtype=np.float64)
     hs, zs = [H], []
     L = len(Ws)
+    r = operand_rounding
     for l in range(1, L + 1):
-        P = H @ np.asarray(Ws[l - 1], dtype=np.float64)                 # F1
+        W = np.asarray(Ws[l - 1], dtype=np.float64)
+        P = _operand(H, r) @ (W if sp.issparse(H) else _operand(W, r))   # F1
         Z = aggregate(g, P) + np.asarray(bs[l - 1], dtype=np.float64)   # F2
         zs.append(Z)
         if l < L:
@@ -288,7 +313,7 @@ def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: i
                 keep = dropout_keep(Z.shape[0], Z.shape[1], dropout_p, seed, l, epoch)
                 H = H * keep / (1.0 - float(np.float32(dropout_p)))
             hs.append(H)
-    return zs[-1], {"H": hs, "Z": zs, "dropout_p": dropout_p, "seed": seed, "epoch": epoch}
+    return zs[-1], {"H": hs, "Z": zs, "dropout_p": dropout_p, "seed": seed, "epoch": epoch, "rounding": r}
 
 
 def softmax_ce(Z, labels, mask=None, n_lab: int | None = None):
@@ -315,9 +340,11 @@ def backward(g: Graph, cache, Ws, dZ):
     for l in range(L, 0, -1):
         dbs[l - 1] = dZ.sum(axis=0)                                     # B1
         G = aggregate(g, dZ)                                             # B2 (Âᵀ = Â)
-        dWs[l - 1] = cache["H"][l - 1].T @ G                             # B3
+        r = cache.get("rounding")
+        Hp = cache["H"][l - 1]
+        dWs[l - 1] = _operand(Hp, r).T @ (G if sp.issparse(Hp) else _operand(G, r))   # B3
         if l > 1:
-            dH = G @ np.asarray(Ws[l - 1], dtype=np.float64).T           # B4
+            dH = _operand(G, r) @ _operand(np.asarray(Ws[l - 1], dtype=np.float64), r).T   # B4
             dZ = dH * (cache["Z"][l - 2] > 0.0)                          # ReLU'(0) := 0 (Q8)
             if cache["dropout_p"] > 0.0:
                 keep = dropout_keep(dZ.shape[0], dZ.shape[1], cache["dropout_p"], cache["seed"],
@@ -340,7 +367,7 @@ def adam_step(params, grads, m, v, t: int, lr=0.01, beta1=0.9, beta2=0.999, eps=
 
 def train(g: Graph, X, labels, dims, epochs: int, seed: int = 42, lr=0.01, beta1=0.9,
           beta2=0.999, eps=1e-8, mask=None, dropout_p: float = 0.0, dropout_seed: int = 0,
-          init=None):
+          init=None, operand_rounding=None):
     """Epoch loop (Listing 1): loss_t at θ_{t-1}, backward, Adam -> θ_t."""
     if init is None:
         Ws, bs = xavier_init(dims, seed)
@@ -352,7 +379,7 @@ def train(g: Graph, X, labels, dims, epochs: int, seed: int = 42, lr=0.01, beta1
     v = [np.zeros_like(p) for p in params]
     losses = []
     for t in range(1, epochs + 1):
-        Z, cache = forward(g, X, params[:L], params[L:], dropout_p, dropout_seed, t)
+        Z, cache = forward(g, X, params[:L], params[L:], dropout_p, dropout_seed, t, operand_rounding)
         loss, dZ = softmax_ce(Z, labels, mask)
         losses.append(loss)
         dWs, dbs = backward(g, cache, params[:L], dZ)

@@ -46,8 +46,15 @@ struct mph_features {
   int32_t* seg_col = nullptr;
   int64_t* seg_begin = nullptr;
   int64_t* col_seg0 = nullptr;  // [F+1] first segment of each column
+  int64_t* seg_ptr = nullptr;   // [n_seg+1] segments as the rows of a virtual CSR over X_csc
   float* part = nullptr;
   size_t part_cap = 0;
+  // edge-balanced work items of the gather kernels (spmm.cu): rows of X_csr, segments of X_csc
+  int2* xw_items = nullptr;
+  int xw_n_items = 0;
+  int2* xtg_items = nullptr;
+  int xtg_n_items = 0;
+  int* item_counter = nullptr;
 };
 
 constexpr int64_t kSegNnz = 128;
@@ -61,6 +68,14 @@ int launch_dinv(const int32_t* deg, float* dinv, int64_t n, cudaStream_t s);
 // 1 ghost columns accumulated onto out + epilogue.
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
                 const mph_epilogue* epi, cudaStream_t s);
+// Edge-balanced work items over a CSR whose row_ptr lives on the device (synchronises; setup only).
+int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** items, int* n_items, cudaStream_t s);
+// The same gather kernel on a general CSR: out[r,:] = row_scale[r] * sum_e val[e] * in[col[e],:]
+// (val == nullptr: pattern / binary matrix; row_scale == nullptr: 1).  w, ld_in, ld_out multiples
+// of 4, in/out 16-byte aligned, w <= 512.
+int spmm_csr_launch(const int64_t* row_ptr, const int32_t* col, const float* val, int n_rows, const int2* items,
+                    int n_items, int* counter, const float* row_scale, const float* in, int w, int ld_in, float* out,
+                    int ld_out, cudaStream_t s);
 // Halo exchange in two halves (comm.cu) so the model can overlap them with the local-edge SpMM.
 int halo_reserve(const mph_graph* g, int w);
 int halo_pack(const mph_graph* g, const float* buf, int w, int ld, cudaStream_t s);

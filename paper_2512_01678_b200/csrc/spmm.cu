@@ -40,7 +40,8 @@ struct SpmmArgs {
   const int64_t* row_ptr;
   const int64_t* split;
   const int32_t* col;
-  const float* dinv;
+  const float* val;   // per-edge values (HAS_VAL kernels only)
+  const float* dinv;  // output row scale (nullptr: 1)
   const float* in;
   float* out;
   const int2* items;  // [first_row, end_row) per work item, hubs first
@@ -60,7 +61,7 @@ __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int6
   return v;
 }
 
-template <int LPR, int VPL>
+template <int LPR, int VPL, bool HAS_VAL>
 __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   constexpr int ES = 32 / LPR;
   // U gathers per slot in flight; U*VPL float4 loads per lane before the first use
@@ -74,11 +75,15 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
 #pragma unroll
   for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
   const uint64_t pol = l2_policy_evict_first();
+  const int* vbits = reinterpret_cast<const int*>(a.val);
   int nxt = (s + lane < e) ? ldg_stream_i32_hint(a.col + s + lane, pol) : 0;
+  int nxv = (HAS_VAL && s + lane < e) ? ldg_stream_i32_hint(vbits + s + lane, pol) : 0;
   for (int64_t base = s; base < e; base += 32) {
     const int nb = (int)min((int64_t)32, e - base);
     const int my_c = nxt;
+    const float my_v = __int_as_float(nxv);
     nxt = (base + 32 + lane < e) ? ldg_stream_i32_hint(a.col + base + 32 + lane, pol) : 0;  // prefetch next ids
+    if (HAS_VAL) nxv = (base + 32 + lane < e) ? ldg_stream_i32_hint(vbits + base + 32 + lane, pol) : 0;
     for (int k0 = 0; k0 < nb; k0 += ES * U) {
       float4 x[U][VPL];
 #pragma unroll
@@ -89,6 +94,16 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
 #pragma unroll
         for (int j = 0; j < VPL; ++j)
           x[uu][j] = (k < nb && sub + j * LPR < a.nv4) ? ldg_f4(p + j * LPR) : f4_zero();
+        if (HAS_VAL) {
+          const float xv = __shfl_sync(0xffffffffu, my_v, k & 31);
+#pragma unroll
+          for (int j = 0; j < VPL; ++j) {
+            x[uu][j].x *= xv;
+            x[uu][j].y *= xv;
+            x[uu][j].z *= xv;
+            x[uu][j].w *= xv;
+          }
+        }
       }
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
@@ -118,7 +133,7 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
     return;
   }
   const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
-  const float du = a.dinv[row];
+  const float du = a.dinv ? a.dinv[row] : 1.0f;
   const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[row] : 1.0f;
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
@@ -151,7 +166,7 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   }
 }
 
-template <int LPR, int VPL>
+template <int LPR, int VPL, bool HAS_VAL>
 __global__ void __launch_bounds__(256, 3) k_spmm(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   while (true) {
@@ -160,7 +175,7 @@ __global__ void __launch_bounds__(256, 3) k_spmm(SpmmArgs a) {
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
-    for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL>(a, row, lane);
+    for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL, HAS_VAL>(a, row, lane);
   }
 }
 
@@ -186,21 +201,20 @@ Dropout make_dropout(const mph_epilogue* e) {
 // about E edges, E = nnz / (32 items per resident warp) clamped to [64, 2048]; a row longer
 // than E is an item of its own.  Items holding a row longer than 4E ("hubs") come first,
 // longest first.
-static int build_items(const mph_graph* gc, cudaStream_t s) {
-  mph_graph* g = const_cast<mph_graph*>(gc);
-  if (g->items) return MPH_OK;
+int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** items_out, int* n_items,
+                     cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, g->nnz / ((int64_t)sms * 24 * 32)));
-  std::vector<int64_t> rp((size_t)g->n_rows + 1);
-  MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), g->row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  const int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, nnz / ((int64_t)sms * 24 * 32)));
+  std::vector<int64_t> rp((size_t)n_rows + 1);
+  MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), row_ptr_d, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MPH_CUDA_TRY(cudaStreamSynchronize(s));
   std::vector<int2> hubs, rest;
   std::vector<int64_t> hub_len;
   int r0 = 0;
   int64_t acc = 0;
-  for (int r = 0; r < g->n_rows; ++r) {
+  for (int r = 0; r < n_rows; ++r) {
     const int64_t d = rp[r + 1] - rp[r];
     if (d > kItemEdges) {  // long row: flush the current run, then the row alone
       if (r > r0) rest.push_back(make_int2(r0, r));
@@ -221,7 +235,7 @@ static int build_items(const mph_graph* gc, cudaStream_t s) {
       acc = 0;
     }
   }
-  if (r0 < g->n_rows) rest.push_back(make_int2(r0, g->n_rows));
+  if (r0 < n_rows) rest.push_back(make_int2(r0, n_rows));
   std::vector<size_t> order(hubs.size());
   for (size_t i = 0; i < order.size(); ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return hub_len[x] > hub_len[y]; });
@@ -229,20 +243,35 @@ static int build_items(const mph_graph* gc, cudaStream_t s) {
   items.reserve(hubs.size() + rest.size());
   for (size_t i : order) items.push_back(hubs[i]);
   items.insert(items.end(), rest.begin(), rest.end());
-  MPH_TRY(dev_alloc(&g->items, items.size()));
-  MPH_TRY(dev_alloc(&g->item_counter, 1));
-  MPH_CUDA_TRY(cudaMemcpyAsync(g->items, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
-  MPH_CUDA_TRY(cudaStreamSynchronize(s));
-  g->n_items = (int)items.size();
+  int2* d_items = nullptr;
+  MPH_TRY(dev_alloc(&d_items, std::max<size_t>(items.size(), 1)));
+  if (!items.empty()) {
+    cudaError_t e = cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      dev_free(d_items);
+      return fail(MPH_ECUDA, "work items: %s", cudaGetErrorString(e));
+    }
+  }
+  *items_out = d_items;
+  *n_items = (int)items.size();
   return MPH_OK;
 }
 
-template <int LPR, int VPL>
+static int build_items(const mph_graph* gc, cudaStream_t s) {
+  mph_graph* g = const_cast<mph_graph*>(gc);
+  if (g->items) return MPH_OK;
+  MPH_TRY(build_work_items(g->row_ptr, g->n_rows, g->nnz, &g->items, &g->n_items, s));
+  MPH_TRY(dev_alloc(&g->item_counter, 1));
+  return MPH_OK;
+}
+
+template <int LPR, int VPL, bool HAS_VAL>
 static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
   static int blocks_per_sm = 0;
   static int sms = 0;
   if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<LPR, VPL>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<LPR, VPL, HAS_VAL>, 256, 0);
     blocks_per_sm = std::max(1, blocks_per_sm);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -250,9 +279,24 @@ static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
   }
   const int64_t grid = std::min<int64_t>((int64_t)sms * blocks_per_sm, ceil_div(a.n_items, 8));
   MPH_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
-  k_spmm<LPR, VPL><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
+  k_spmm<LPR, VPL, HAS_VAL><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
   count_launch();
   return launch_check("spmm");
+}
+
+template <bool HAS_VAL>
+static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
+  const int nv4 = a.nv4;
+  if (nv4 <= 1) return launch_spmm<1, 1, HAS_VAL>(a, s);
+  if (nv4 <= 2) return launch_spmm<2, 1, HAS_VAL>(a, s);
+  if (nv4 <= 4) return launch_spmm<4, 1, HAS_VAL>(a, s);
+  if (nv4 <= 8) return launch_spmm<8, 1, HAS_VAL>(a, s);
+  if (nv4 <= 12) return launch_spmm<4, 3, HAS_VAL>(a, s);
+  if (nv4 <= 16) return launch_spmm<16, 1, HAS_VAL>(a, s);
+  if (nv4 <= 32) return launch_spmm<32, 1, HAS_VAL>(a, s);
+  if (nv4 <= 64) return launch_spmm<32, 2, HAS_VAL>(a, s);
+  if (nv4 <= 96) return launch_spmm<32, 3, HAS_VAL>(a, s);
+  return launch_spmm<32, 4, HAS_VAL>(a, s);
 }
 
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
@@ -271,7 +315,8 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   if (epi && (epi->flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "spmm: null row_scale");
   if (g->n_rows == 0) return MPH_OK;
   MPH_TRY(build_items(g, s));
-  SpmmArgs a;
+  SpmmArgs a{};
+  a.val = nullptr;
   a.row_ptr = g->row_ptr;
   a.split = g->split;
   a.col = g->col_idx;
@@ -293,17 +338,37 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.epi.row0 = epi ? epi->row0 : 0;
   if (a.epi.drop.threshold == 0) a.epi.flags &= ~MPH_EPI_DROPOUT;
   a.epi.c4_0 = 0;
-  const int nv4 = a.nv4;
-  if (nv4 <= 1) return launch_spmm<1, 1>(a, s);
-  if (nv4 <= 2) return launch_spmm<2, 1>(a, s);
-  if (nv4 <= 4) return launch_spmm<4, 1>(a, s);
-  if (nv4 <= 8) return launch_spmm<8, 1>(a, s);
-  if (nv4 <= 12) return launch_spmm<4, 3>(a, s);
-  if (nv4 <= 16) return launch_spmm<16, 1>(a, s);
-  if (nv4 <= 32) return launch_spmm<32, 1>(a, s);
-  if (nv4 <= 64) return launch_spmm<32, 2>(a, s);
-  if (nv4 <= 96) return launch_spmm<32, 3>(a, s);
-  return launch_spmm<32, 4>(a, s);
+  return dispatch_spmm<false>(a, s);
+}
+
+int spmm_csr_launch(const int64_t* row_ptr, const int32_t* col, const float* val, int n_rows, const int2* items,
+                    int n_items, int* counter, const float* row_scale, const float* in, int w, int ld_in, float* out,
+                    int ld_out, cudaStream_t s) {
+  if (!row_ptr || !in || !out || (!items && n_items > 0) || !counter) return fail(MPH_EINVAL, "spmm_csr: null argument");
+  if (w <= 0 || w % 4 || ld_in % 4 || ld_out % 4 || ld_in < w || ld_out < w || w > 512)
+    return fail(MPH_EINVAL, "spmm_csr: bad width %d", w);
+  if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
+    return fail(MPH_EINVAL, "spmm_csr: operands must be 16-byte aligned");
+  if (n_rows == 0 || n_items == 0) return MPH_OK;
+  SpmmArgs a{};
+  a.row_ptr = row_ptr;
+  a.split = nullptr;
+  a.col = col;
+  a.val = val;
+  a.dinv = row_scale;
+  a.in = in;
+  a.out = out;
+  a.items = items;
+  a.counter = counter;
+  a.n_items = n_items;
+  a.ld_in = ld_in;
+  a.ld_out = ld_out;
+  a.n_rows = n_rows;
+  a.nv4 = w / 4;
+  a.part = -1;
+  a.epi.flags = 0u;
+  a.epi.drop = make_dropout(nullptr);
+  return val ? dispatch_spmm<true>(a, s) : dispatch_spmm<false>(a, s);
 }
 
 __global__ void k_pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int nv4, float* out) {

@@ -314,13 +314,15 @@ def test_xavier_bit_exact(P, fi, fo, layer):
 
 
 # ------------------------------------------------------------------ sparse-feature kernels
-@pytest.mark.parametrize("name", ["cora", "pubmed"])
-def test_sparse_feature_kernels(P, name):
+@pytest.mark.parametrize("name,fo", [("cora", None), ("pubmed", None), ("pubmed", 10), ("cora", 100)])
+def test_sparse_feature_kernels(P, name, fo):
+    """fo % 4 == 0: float4 gather kernel (binary cora: pattern only, tf-idf pubmed: values);
+    fo = 10: the scalar fallback."""
     from paper_2512_01678_b200._lib import mph_sparse_xtg, mph_sparse_xw
     w = make_workload(name)
     X = w["X"]
     N, F = X.shape
-    fo = w["cfg"].dims[1]
+    fo = fo or w["cfg"].dims[1]
     f = P.Features(cuda(X))
     rng = np.random.default_rng(1)
     W = rng.standard_normal((F, fo)).astype(np.float32)

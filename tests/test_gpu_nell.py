@@ -105,9 +105,50 @@ def test_nell_loss_trajectory(P, nell):
     m.init_xavier(42)
     m.set_labels(cuda(nell["y"].astype(np.int32)))
     got = [m.train_epoch(t).item() for t in range(1, 11)]
+    print("gpu", np.round(got, 5))
     rg = oracle.graph_build(nell["src"], nell["dst"], cfg.num_nodes)
     X = sp.csr_matrix((val, idx, ptr), shape=(cfg.num_nodes, cfg.num_features))
-    ref, _ = oracle.train(rg, X, nell["y"], dims, epochs=10, seed=42)
+    # Reading R4: at lr = 0.01 this configuration is in a regime where Adam's normalisation turns
+    # tiny absolute gradient differences into lr-sized steps (the loss rises at epoch 3), so the
+    # TF32 operand rounding the north_star allows moves the exact-arithmetic trajectory by ~2e-2
+    # from epoch 4 on.  Epochs 1-3 are held to the exact oracle; all ten to the oracle with TF32
+    # operands on its dense products (oracle.tf32_rna, pinned in test_oracle_sparse).
+    ref, _ = oracle.train(rg, X, nell["y"], dims, epochs=3, seed=42)
     for t, (a, b) in enumerate(zip(got, ref), 1):
         assert abs(a - b) <= 1e-3 * max(1.0, abs(b)), f"epoch {t}: gpu {a} vs oracle {b}"
+    ref_tf, _ = oracle.train(rg, X, nell["y"], dims, epochs=10, seed=42, operand_rounding="tf32")
+    print("oracle tf32", np.round(ref_tf, 5))
+    for t, (a, b) in enumerate(zip(got, ref_tf), 1):
+        assert abs(a - b) <= 1e-3 * max(1.0, abs(b)), f"epoch {t}: gpu {a} vs oracle(tf32) {b}"
     assert got[-1] < got[0]
+
+
+def test_nell_first_epoch_layers_and_gradients(P, nell):
+    """Epoch 1 on NELL against the oracle: sampled rows of T1 = X·W1 (sparse, FP32 bound), the loss,
+    and every gradient normwise (TF32 GEMMs on layers 2-3: 2e-3)."""
+    ptr, idx, val = nell["X_csr"]
+    cfg = nell["cfg"]
+    dims = cfg.dims
+    g = P.Graph(nell["src"], nell["dst"], cfg.num_nodes)
+    f = P.Features.from_csr(ptr, idx, val, (cfg.num_nodes, cfg.num_features))
+    m = P.GCN(g, f, dims)
+    m.init_xavier(42)
+    m.set_labels(cuda(nell["y"].astype(np.int32)))
+    assert m.order == [0, 0, 0]
+    m.forward(1)
+    lg = m.loss().item()
+    m.backward()
+    torch.cuda.synchronize()
+    rg = oracle.graph_build(nell["src"], nell["dst"], cfg.num_nodes)
+    X = sp.csr_matrix((val, idx, ptr), shape=(cfg.num_nodes, cfg.num_features))
+    Ws, bs = oracle.xavier_init(dims, 42)
+    Z, cache = oracle.forward(rg, X, Ws, bs)
+    lr, dZ = oracle.softmax_ce(Z, nell["y"])
+    dWs, dbs = oracle.backward(rg, cache, Ws, dZ)
+    assert abs(lg - lr) <= 1e-5 * abs(lr)
+    for l, (dWg, dbg) in enumerate(m.grads()):
+        for name, got, exp in (("dW", dWg, dWs[l]), ("db", dbg, dbs[l])):
+            got = got.cpu().numpy().astype(np.float64)
+            rel = np.linalg.norm(got - exp) / max(np.linalg.norm(exp), 1e-30)
+            print(f"layer {l + 1} {name} rel {rel:.3g}")
+            assert rel <= 2e-3, f"layer {l + 1} {name} rel err {rel:.3g}"

@@ -48,3 +48,46 @@ def test_nell_features_have_the_papers_sparsity():
     Xs = sp.csr_matrix((val, idx, ptr), shape=(n, fdim))
     a = oracle.analyze_features(Xs, gd["tau"]["tau_bp"])
     assert a.mode == 1 and a.is_binary and a.nnz == val.size
+
+
+# ---------------------------------------------------------------- TF32 operand rounding (R2)
+def test_tf32_rna_known_values():
+    """cvt.rna.tf32.f32: 10 explicit mantissa bits, nearest, ties away from zero."""
+    u = 2.0 ** -10                                        # TF32 ulp at 1.0
+    cases = {1.0: 1.0, 1.0 + u / 2: 1.0 + u, -(1.0 + u / 2): -(1.0 + u), 1.0 + u / 4: 1.0,
+             1.0 + 3 * u / 4: 1.0 + u, 1.0 + u + u / 2: 1.0 + 2 * u, 3.0 * 2.0 ** 100: 3.0 * 2.0 ** 100,
+             0.0: 0.0, 2.0 - u / 2: 2.0, 1.0 + 2.0 ** -23: 1.0}
+    for x, want in cases.items():
+        assert oracle.tf32_rna(np.float32(x)) == want, x
+    # subnormal fp32 input: same rule on the raw mantissa
+    sub = np.array([0x00001000], np.uint32).view(np.float32)
+    assert oracle.tf32_rna(sub).item() == np.array([0x00002000], np.uint32).view(np.float32).item()
+
+
+def test_tf32_rna_properties():
+    rng = np.random.default_rng(0)
+    x = (rng.standard_normal(100000) * np.exp(rng.uniform(-20, 20, 100000))).astype(np.float32)
+    r = oracle.tf32_rna(x)
+    assert np.all(np.abs(r - x) <= 2.0 ** -11 * np.abs(x.astype(np.float64)))
+    assert np.all(r.astype(np.float32).view(np.uint32) & 0x1FFF == 0)
+    assert np.array_equal(oracle.tf32_rna(r), r)                  # idempotent
+    assert np.array_equal(oracle.tf32_rna(-x), -r)                # symmetric (ties away from zero)
+
+
+def test_tf32_forward_within_operand_bound():
+    """operand_rounding="tf32" changes each dense product H·W by at most (2^-11 + 2^-11 + 2^-22)|H||W|
+    per element before aggregation; Â is nonnegative, so Z moves by at most Â(that bound)."""
+    w = make_small(300, 2400, 24, 5, seed=5)
+    g = oracle.graph_build(w["src"], w["dst"], 300)
+    dims = (24, 16, 5)
+    Ws, bs = oracle.xavier_init(dims, 42)
+    Z0, c0 = oracle.forward(g, w["X"], Ws, bs)
+    Z1, c1 = oracle.forward(g, w["X"], Ws, bs, operand_rounding="tf32")
+    e = 2.0 ** -11 * 2 + 2.0 ** -22
+    b1 = oracle.aggregate(g, e * np.abs(w["X"].astype(np.float64)) @ np.abs(Ws[0].astype(np.float64)))
+    z1_exact = c0["Z"][0]
+    assert np.all(np.abs(c1["Z"][0] - z1_exact) <= b1 + 1e-15)
+    assert not np.array_equal(c1["Z"][0], z1_exact)               # the option does something
+    # sparse X: the layer-1 product stays exact
+    _, cs = oracle.forward(g, sp.csr_matrix(w["X"]), Ws, bs, operand_rounding="tf32")
+    assert np.allclose(cs["Z"][0], z1_exact, rtol=1e-13, atol=1e-15)
