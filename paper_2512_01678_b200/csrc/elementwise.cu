@@ -382,6 +382,10 @@ int sparse_xw_launch(const mph_features* f, const float* W, int F_out, int ldw, 
   if (!f || !W || !T || F_out <= 0 || ldw < F_out || ldt < F_out) return fail(MPH_EINVAL, "sparse_xw: bad arguments");
   if (f->mode != 1) return fail(MPH_ESTATE, "sparse_xw: features are in dense mode");
   if (F_out > 256) return fail(MPH_ENOTSUP, "sparse_xw: F_out > 256");
+  if (F_out % 4 == 0 && ldw % 4 == 0 && ldt % 4 == 0 &&
+      !((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(T)) & 15))  // float4 gather kernel
+    return spmm_csr_launch(f->csr_ptr, f->csr_idx, f->is_binary ? nullptr : f->csr_val, f->N, f->xw_items,
+                           f->xw_n_items, f->item_counter, row_scale, W, F_out, ldw, T, ldt, s);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(f->N, 8), 148 * 16));
   k_sparse_xw<<<grid, 256, 0, s>>>(f->csr_ptr, f->csr_idx, f->csr_val, f->N, W, F_out, ldw, row_scale, T, ldt);
   count_launch();
@@ -402,14 +406,21 @@ int sparse_xtg_launch(const mph_features* fc, const float* G, int F_out, int ldg
     f->part_cap = need;
   }
   if (f->n_seg > 0) {
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(f->n_seg, 8), 148 * 16));
-    k_sparse_xtg_seg<<<grid, 256, 0, s>>>(f->seg_col, f->seg_begin, f->csc_ptr, f->csc_idx, f->csc_val, f->n_seg, G,
-                                          F_out, ldg, f->part);
+    if (F_out % 4 == 0 && ldg % 4 == 0 && !(reinterpret_cast<uintptr_t>(G) & 15)) {  // float4 gather kernel
+      MPH_TRY(spmm_csr_launch(f->seg_ptr, f->csc_idx, f->is_binary ? nullptr : f->csc_val, (int)f->n_seg,
+                              f->xtg_items, f->xtg_n_items, f->item_counter, nullptr, G, F_out, ldg, f->part, F_out,
+                              s));
+    } else {
+      const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(f->n_seg, 8), 148 * 16));
+      k_sparse_xtg_seg<<<grid, 256, 0, s>>>(f->seg_col, f->seg_begin, f->csc_ptr, f->csc_idx, f->csc_val, f->n_seg,
+                                            G, F_out, ldg, f->part);
+      count_launch();
+    }
   }
   const int64_t total = (int64_t)f->F * F_out;
   k_sparse_xtg_sum<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 148 * 16)), 256, 0, s>>>(
       f->col_seg0, f->F, f->part, F_out, dW, lddw);
-  count_launch(2);
+  count_launch();
   return launch_check("sparse_xtg");
 }
 

@@ -151,6 +151,16 @@ static int csc_from_csr(mph_features* f, cudaStream_t s) {
   if (e == cudaSuccess && !sb.empty())
     e = cudaMemcpy(f->seg_begin, sb.data(), sb.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return done(fail(MPH_ECUDA, "segments upload: %s", cudaGetErrorString(e)));
+  // segments are contiguous runs of X_csc in order, so their begins (+ nnz) form the row_ptr of a
+  // virtual CSR whose rows are the segments: the dW gather runs on it like any SpMM
+  sb.push_back(nnz);
+  if ((rc = dev_alloc(&f->seg_ptr, sb.size()))) return done(rc);
+  e = cudaMemcpy(f->seg_ptr, sb.data(), sb.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return done(fail(MPH_ECUDA, "segments upload: %s", cudaGetErrorString(e)));
+  if ((rc = build_work_items(f->csr_ptr, N, nnz, &f->xw_items, &f->xw_n_items, s)) ||
+      (rc = build_work_items(f->seg_ptr, (int)f->n_seg, nnz, &f->xtg_items, &f->xtg_n_items, s)) ||
+      (rc = dev_alloc(&f->item_counter, 1)))
+    return done(rc);
   return done(MPH_OK);
 }
 
@@ -174,6 +184,10 @@ static void features_free(mph_features* f) {
   dev_free(f->seg_col);
   dev_free(f->seg_begin);
   dev_free(f->col_seg0);
+  dev_free(f->seg_ptr);
+  dev_free(f->xw_items);
+  dev_free(f->xtg_items);
+  dev_free(f->item_counter);
   dev_free(f->part);
   delete f;
 }
