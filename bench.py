@@ -29,7 +29,7 @@ METRIC = "GCN ms/epoch (fwd+bwd+Adam) at 1/2/4/8 B200; SpMM HBM GB/s vs peak"
 UNIT = "ms/epoch"
 FALLBACK_HBM_GBS = 6650.0
 # CPU-oracle sample: the same generator recipe at 1/k scale (same mean degree, widths, classes)
-SAMPLE_SCALE = {"cora": 1, "pubmed": 1, "arxiv": 4, "reddit": 16, "products": 32}
+SAMPLE_SCALE = {"cora": 1, "pubmed": 1, "arxiv": 4, "reddit": 16, "products": 32, "nell": 2}
 PROF_KINDS = {0: "spmm", 1: "gemm_nt", 2: "gemm_tn", 3: "softmax_ce", 4: "adam", 5: "sparse_feat", 6: "halo"}
 
 
@@ -98,14 +98,19 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------- oracle sample
 def _oracle_sample(name: str, seed_offset: int = 0):
     """The same workload recipe at 1/k scale, for the CPU oracle (bounded sample)."""
-    from synth.generate import CONFIGS, make_features, make_graph, make_labels
+    from synth.generate import CONFIGS, make_features, make_features_csr, make_graph, make_labels
     cfg = CONFIGS[name]
     k = SAMPLE_SCALE[name]
     n = max(64, cfg.num_nodes // k)
     nnz = cfg.nnz_a // k
     y = make_labels(n, cfg.num_classes)
     src, dst = make_graph(n, nnz, cfg.num_classes, cfg.alpha, cfg.mu, cfg.seed + seed_offset)
-    X = make_features(n, cfg.num_features, y, cfg.num_classes, cfg.feature_kind, cfg.density, cfg.seed)
+    if cfg.feature_kind == "binary_csr":
+        import scipy.sparse as sp
+        ptr, idx, val = make_features_csr(n, cfg.num_features, y, cfg.num_classes, cfg.density, cfg.seed)
+        X = sp.csr_matrix((val, idx, ptr), shape=(n, cfg.num_features))
+    else:
+        X = make_features(n, cfg.num_features, y, cfg.num_classes, cfg.feature_kind, cfg.density, cfg.seed)
     return {"src": src, "dst": dst, "X": X, "y": y, "n": n, "nnz_a": nnz, "k": k, "cfg": cfg}
 
 
@@ -164,9 +169,17 @@ def _build_model(P, torch, w, world, rank, comm):
     cfg = w["cfg"]
     n = cfg.num_nodes
     X = w["X"]
+
+    def features(r0, r1):
+        if X is not None:
+            return P.Features(torch.from_numpy(np.ascontiguousarray(X[r0:r1])).cuda())
+        ptr, idx, val = w["X_csr"]   # CSR features (NELL): rows r0..r1 of the host CSR, never densified
+        b, e = int(ptr[r0]), int(ptr[r1])
+        return P.Features.from_csr(ptr[r0:r1 + 1] - b, idx[b:e], val[b:e], (r1 - r0, cfg.num_features))
+
     if world == 1:
         g = P.Graph(w["src"], w["dst"], n)
-        f = P.Features(torch.from_numpy(X).cuda())
+        f = features(0, n)
         m = P.GCN(g, f, cfg.dims)
         y = torch.from_numpy(w["y"]).cuda()
         own = (0, n)
@@ -180,7 +193,7 @@ def _build_model(P, torch, w, world, rank, comm):
         del rp, ci
         g = P.Graph.from_plan(plan)
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-        f = P.Features(torch.from_numpy(np.ascontiguousarray(X[r0:r1])).cuda())
+        f = features(r0, r1)
         m = P.GCN(g, f, cfg.dims, comm=comm)
         y = torch.from_numpy(np.ascontiguousarray(w["y"][r0:r1])).cuda()
         own = (r0, r1)
@@ -254,11 +267,14 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     # ---------------- end-to-end through the public API with host buffers
     e2e = None
     if full and not args.no_e2e:
-        X = w["X"][own[0]:own[1]]
-        Pw = P.pad_width(X.shape[1])
-        Xh = torch.zeros((X.shape[0], Pw), dtype=torch.float32).pin_memory()   # padded pinned host rows
-        Xh[:, :X.shape[1]] = torch.from_numpy(X)
         upload = f.mode == 0   # sparse-mode features are analysed once at load (Alg. 1); labels still move
+        if upload:
+            X = w["X"][own[0]:own[1]]
+            Pw = P.pad_width(X.shape[1])
+            Xh = torch.zeros((X.shape[0], Pw), dtype=torch.float32).pin_memory()   # padded pinned host rows
+            Xh[:, :X.shape[1]] = torch.from_numpy(X)
+        else:
+            Xh, Pw = torch.zeros(0), 0
         yh = torch.from_numpy(np.ascontiguousarray(w["y"][own[0]:own[1]])).pin_memory()
         lh = torch.zeros(1, dtype=torch.float64).pin_memory()
         steps_e2e = max(3, args.steps // 2)
@@ -287,7 +303,8 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
 
     # ---------------- roofline of the dominant kernel
     peak, peak_kind = _peaks()
-    dom = max((k for k in ("spmm", "gemm_nt", "gemm_tn") if k in kernels), key=lambda k: kernels[k]["ms_per_epoch"],
+    dom = max((k for k in ("spmm", "gemm_nt", "gemm_tn", "sparse_feat") if k in kernels),
+              key=lambda k: kernels[k]["ms_per_epoch"],
               default=None)
     roofline = None
     if dom is not None:
@@ -300,7 +317,10 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": peak, "unit": "GB/s",
                     "frac": kd["algorithmic_GBps"] / peak, "traffic": traffic,
                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                    "algorithmic_bytes": "SURVEY 8(d) d.3 no-reuse count: per edge 4 + 4*w B, per row 12 + 4*w B",
+                    "algorithmic_bytes": ("SURVEY 8(d) d.3 no-reuse count: per edge 4 + 4*w B, per row 12 + 4*w B"
+                                          if dom == "spmm" else
+                                          "no-reuse count: per nonzero of X 8 + 4*w B, per row/column 8 + 4*w B"
+                                          if dom == "sparse_feat" else "A + B + C bytes once"),
                     "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_ms": kd["avg_launch_ms"],
                     "share_of_epoch": kd["ms_per_epoch"] / ms}
 
@@ -414,7 +434,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="reddit", choices=["cora", "pubmed", "arxiv", "reddit", "products"])
+    ap.add_argument("--config", default="reddit", choices=["cora", "pubmed", "arxiv", "reddit", "products", "nell"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

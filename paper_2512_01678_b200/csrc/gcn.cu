@@ -196,7 +196,9 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
   if (l.order == 0) {
     // a2/a4: T' = dinv ⊙ (H_{l-1} · W_l)
     if (li == 0 && m->f->mode == 1) {
-      prof::Scope sc(MPH_PROF_SPARSE, s, 8.0 * m->f->nnz + 4.0 * g->n_rows * l.pout, 2.0 * m->f->nnz * l.pout);
+      // no-reuse count (as for the SpMM): per nonzero 8 B (col, val) + a W row; per row ptr + T row
+      prof::Scope sc(MPH_PROF_SPARSE, s, (8.0 + 4.0 * l.pout) * m->f->nnz + (8.0 + 4.0 * l.pout) * g->n_rows,
+                     2.0 * m->f->nnz * l.pout);
       MPH_TRY(sparse_xw_launch(m->f, m->params + l.off_w, l.pout, l.pout, g->dinv, l.T, l.pout, s));
     } else {
       const float* A = li == 0 ? m->Xr : m->layers[li - 1].out;
@@ -254,7 +256,9 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       Gsrc = l.G;
       // a7: dW = H^T·G  (sparse layer 1: X_csc^T·G)
       if (li == 0 && m->f->mode == 1) {
-        prof::Scope sc(MPH_PROF_SPARSE, s, 8.0 * m->f->nnz + 4.0 * m->f->nnz * l.pout, 2.0 * m->f->nnz * l.pout);
+        // per nonzero 8 B + a G row; per column ptr + dW row (segment partials not counted)
+        prof::Scope sc(MPH_PROF_SPARSE, s, (8.0 + 4.0 * l.pout) * m->f->nnz + (8.0 + 4.0 * l.pout) * m->f->F,
+                       2.0 * m->f->nnz * l.pout);
         MPH_TRY(sparse_xtg_launch(m->f, l.G, l.pout, l.pout, m->grads + l.off_w, l.pout, s));
       } else {
         MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, Hin, ld_in, l.G, l.pout, m->grads + l.off_w, l.pout, m->ws,
