@@ -24,6 +24,13 @@ Parity status of each function (pins live in tests/test_oracle_*.py):
   adam_step .......... pinned (first step -lr*sign(g), zero grad, torch.optim.Adam)
   train .............. pinned (monotone loss on the separable SBM toy)
   partition_1d / localize ... pinned (brute-force recount, union = global set)
+  tf32_rna ........... pinned (known values incl. ties away from zero, bounds, idempotence)
+  aggregate_scheme (sum/mean) ... pinned (brute force over neighbour sets from the raw edge list,
+                                  dense adjoints, Ã·1 = d̃, mean of a constant, torch autograd)
+  aggregate_max / _backward ..... pinned (brute force with ties -> smallest id, hand star case,
+                                  central differences, routed-mass conservation)
+  forward/backward (sum/mean/max) pinned (central finite differences of the whole loss)
+  sgd_step / adamw_step ......... pinned (closed forms; torch.optim.SGD / AdamW traces)
   absolute model quality vs the paper ... parity unpinned (the paper prints no loss
                                            or accuracy value)
 """

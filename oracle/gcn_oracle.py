@@ -20,6 +20,8 @@ __all__ = [
     "aggregate", "aggregate_rows", "analyze_features", "FeatureAnalysis",
     "splitmix64_stream", "xavier_init", "philox4x32_10", "dropout_keep",
     "dropout_threshold", "tf32_rna", "forward", "softmax_ce", "backward", "adam_step", "train",
+    "AGGREGATORS", "aggregate_scheme", "aggregate_max", "aggregate_max_backward",
+    "OPTIMIZERS", "sgd_step", "adamw_step",
     "partition_1d", "localize", "LocalPlan", "GOLDEN",
 ]
 
@@ -120,6 +122,63 @@ def aggregate_rows(g: Graph, P: np.ndarray, rows) -> np.ndarray:
         w = 1.0 / np.sqrt(d[u] * d[cols])
         out[i] = w @ np.asarray(P[cols], dtype=np.float64)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Other aggregation schemes: "GCN uses normalized mean aggregation ...
+# GIN employs sum aggregation"; "multiple aggregation schemes (mean, max, sum)";
+# Listing 1's SAGE "Max".  Readings R6-R8: every scheme aggregates over
+# Ñ(u) = N(u) ∪ {u}, the same Ã = A + I the GCN uses (Q2); max is taken before the transform
+# (P:92 applies W to AGGREGATE(h)); ties go to the smallest node id.
+# ---------------------------------------------------------------------------
+AGGREGATORS = ("gcn", "sum", "mean", "max")
+
+
+def _a_tilde_csr(g: Graph) -> sp.csr_matrix:
+    """Ã = A + I as a 0/1 CSR (the graph's pattern, diagonal included)."""
+    return sp.csr_matrix((np.ones(g.nnz), g.col_idx.astype(np.int64), g.row_ptr),
+                         shape=(g.num_nodes, g.num_nodes))
+
+
+def aggregate_scheme(g: Graph, P: np.ndarray, scheme: str, transpose: bool = False) -> np.ndarray:
+    """Linear aggregations in FP64: gcn Â·P; sum Ã·P; mean D̃^{-1}Ã·P.  transpose=True applies
+    the adjoint used by the backward pass (Âᵀ = Â, Ãᵀ = Ã, (D̃^{-1}Ã)ᵀ = Ã·D̃^{-1})."""
+    P = np.asarray(P, dtype=np.float64)
+    if scheme == "gcn":
+        return aggregate(g, P)
+    At = _a_tilde_csr(g)
+    if scheme == "sum":
+        return np.asarray(At @ P)
+    if scheme == "mean":
+        d = g.deg.astype(np.float64)[:, None]
+        return np.asarray(At @ (P / d)) if transpose else np.asarray(At @ P) / d
+    raise ValueError(f"not a linear aggregation scheme: {scheme}")
+
+
+def aggregate_max(g: Graph, P: np.ndarray):
+    """Y[u,c] = max over v in Ñ(u) of P[v,c]; arg[u,c] = the smallest such v (ties, R7).
+    Plain per-row loop: the row's neighbour ids are ascending, so np.argmax's first maximum is
+    the smallest id."""
+    P = np.asarray(P, dtype=np.float64)
+    n, f = P.shape
+    Y = np.empty((n, f), dtype=np.float64)
+    arg = np.empty((n, f), dtype=np.int64)
+    cols_f = np.arange(f)
+    for u in range(n):
+        nb = g.col_idx[g.row_ptr[u]:g.row_ptr[u + 1]].astype(np.int64)
+        block = P[nb]
+        k = np.argmax(block, axis=0)
+        Y[u] = block[k, cols_f]
+        arg[u] = nb[k]
+    return Y, arg
+
+
+def aggregate_max_backward(dY: np.ndarray, arg: np.ndarray, num_nodes: int) -> np.ndarray:
+    """Adjoint of aggregate_max: every dY[u,c] is routed to its argmax node arg[u,c]."""
+    dY = np.asarray(dY, dtype=np.float64)
+    dH = np.zeros((num_nodes, dY.shape[1]), dtype=np.float64)
+    np.add.at(dH, (arg, np.broadcast_to(np.arange(dY.shape[1]), arg.shape)), dY)
+    return dH
 
 
 # ---------------------------------------------------------------------------
@@ -294,18 +353,29 @@ def _operand(M, rounding):
     return tf32_rna(M)
 
 
-def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1, operand_rounding=None):
+def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1, operand_rounding=None,
+            aggregator: str = "gcn"):
     # X may be a scipy CSR matrix (sparse features): X·W_1 and X^T·G are then sparse products.
     # operand_rounding="tf32" rounds both operands of every dense product H·W (R2); sparse products
     # (X_csr·W_1) and the aggregation stay exact.  It models transform-first layers.
+    # aggregator: "gcn" (Â, the north star), "sum", "mean" (linear: Z = AGG(H·W) + b) or "max"
+    # (Z = MAX(H)·W + b, R7); see aggregate_scheme / aggregate_max.
+    if aggregator not in AGGREGATORS:
+        raise ValueError(aggregator)
     H = X.astype(np.float64).tocsr() if sp.issparse(X) else np.asarray(X, dtype=np.float64)
-    hs, zs = [H], []
+    hs, zs, ys, args = [H], [], [], []
     L = len(Ws)
     r = operand_rounding
     for l in range(1, L + 1):
         W = np.asarray(Ws[l - 1], dtype=np.float64)
-        P = _operand(H, r) @ (W if sp.issparse(H) else _operand(W, r))   # F1
-        Z = aggregate(g, P) + np.asarray(bs[l - 1], dtype=np.float64)   # F2
+        if aggregator == "max":
+            Y, arg = aggregate_max(g, H.toarray() if sp.issparse(H) else H)   # F2 before F1 (R7)
+            ys.append(Y)
+            args.append(arg)
+            Z = _operand(Y, r) @ _operand(W, r) + np.asarray(bs[l - 1], dtype=np.float64)
+        else:
+            P = _operand(H, r) @ (W if sp.issparse(H) else _operand(W, r))   # F1
+            Z = aggregate_scheme(g, P, aggregator) + np.asarray(bs[l - 1], dtype=np.float64)   # F2
         zs.append(Z)
         if l < L:
             H = np.maximum(Z, 0.0)                                       # F3
@@ -313,7 +383,8 @@ def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: i
                 keep = dropout_keep(Z.shape[0], Z.shape[1], dropout_p, seed, l, epoch)
                 H = H * keep / (1.0 - float(np.float32(dropout_p)))
             hs.append(H)
-    return zs[-1], {"H": hs, "Z": zs, "dropout_p": dropout_p, "seed": seed, "epoch": epoch, "rounding": r}
+    return zs[-1], {"H": hs, "Z": zs, "dropout_p": dropout_p, "seed": seed, "epoch": epoch, "rounding": r,
+                    "aggregator": aggregator, "Y": ys, "arg": args}
 
 
 def softmax_ce(Z, labels, mask=None, n_lab: int | None = None):
@@ -337,14 +408,23 @@ def backward(g: Graph, cache, Ws, dZ):
     """B1-B4: returns (dWs, dbs)."""
     L = len(Ws)
     dWs, dbs = [None] * L, [None] * L
+    agg = cache.get("aggregator", "gcn")
     for l in range(L, 0, -1):
         dbs[l - 1] = dZ.sum(axis=0)                                     # B1
-        G = aggregate(g, dZ)                                             # B2 (Âᵀ = Â)
         r = cache.get("rounding")
-        Hp = cache["H"][l - 1]
-        dWs[l - 1] = _operand(Hp, r).T @ (G if sp.issparse(Hp) else _operand(G, r))   # B3
+        W = np.asarray(Ws[l - 1], dtype=np.float64)
+        if agg == "max":                                                 # Z = Y·W + b, Y = MAX(H)
+            dWs[l - 1] = _operand(cache["Y"][l - 1], r).T @ _operand(dZ, r)
+            if l > 1:
+                dY = _operand(dZ, r) @ _operand(W, r).T
+                dH = aggregate_max_backward(dY, cache["arg"][l - 1], g.num_nodes)
+        else:
+            G = aggregate_scheme(g, dZ, agg, transpose=True)             # B2 (Âᵀ = Â)
+            Hp = cache["H"][l - 1]
+            dWs[l - 1] = _operand(Hp, r).T @ (G if sp.issparse(Hp) else _operand(G, r))   # B3
+            if l > 1:
+                dH = _operand(G, r) @ _operand(W, r).T                   # B4
         if l > 1:
-            dH = _operand(G, r) @ _operand(np.asarray(Ws[l - 1], dtype=np.float64), r).T   # B4
             dZ = dH * (cache["Z"][l - 2] > 0.0)                          # ReLU'(0) := 0 (Q8)
             if cache["dropout_p"] > 0.0:
                 keep = dropout_keep(dZ.shape[0], dZ.shape[1], cache["dropout_p"], cache["seed"],
@@ -365,10 +445,38 @@ def adam_step(params, grads, m, v, t: int, lr=0.01, beta1=0.9, beta2=0.999, eps=
         p -= lr * mhat / (np.sqrt(vhat) + eps)
 
 
+def sgd_step(params, grads, vel, lr=0.01, momentum=0.0, weight_decay=0.0):
+    """SGD (reading R8, the common definition): g' = g + wd·p; with momentum μ > 0 the
+    velocity is v = μ·v + g' (v = g' at the first step, i.e. v starts at zero); p -= lr·v
+    (p -= lr·g' when μ = 0).  In place."""
+    for p, gr, vv in zip(params, grads, vel):
+        d = gr + weight_decay * p if weight_decay != 0.0 else gr
+        if momentum != 0.0:
+            vv *= momentum
+            vv += d
+            d = vv
+        p -= lr * d
+
+
+def adamw_step(params, grads, m, v, t: int, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01):
+    """AdamW (P:140; S:375 "applies decoupled weight decay before the Adam update"):
+    p ← p − lr·wd·p, then adam_step.  In place."""
+    for p in params:
+        p -= lr * weight_decay * p
+    adam_step(params, grads, m, v, t, lr, beta1, beta2, eps)
+
+
+OPTIMIZERS = ("adam", "sgd", "adamw")
+
+
 def train(g: Graph, X, labels, dims, epochs: int, seed: int = 42, lr=0.01, beta1=0.9,
           beta2=0.999, eps=1e-8, mask=None, dropout_p: float = 0.0, dropout_seed: int = 0,
-          init=None, operand_rounding=None):
-    """Epoch loop (Listing 1): loss_t at θ_{t-1}, backward, Adam -> θ_t."""
+          init=None, operand_rounding=None, aggregator: str = "gcn", optimizer: str = "adam",
+          weight_decay: float = 0.0, momentum: float = 0.0):
+    """Epoch loop (Listing 1): loss_t at θ_{t-1}, backward, optimizer -> θ_t
+    (Adam by default; SGD / AdamW)."""
+    if optimizer not in OPTIMIZERS:
+        raise ValueError(optimizer)
     if init is None:
         Ws, bs = xavier_init(dims, seed)
     else:
@@ -379,11 +487,16 @@ def train(g: Graph, X, labels, dims, epochs: int, seed: int = 42, lr=0.01, beta1
     v = [np.zeros_like(p) for p in params]
     losses = []
     for t in range(1, epochs + 1):
-        Z, cache = forward(g, X, params[:L], params[L:], dropout_p, dropout_seed, t, operand_rounding)
+        Z, cache = forward(g, X, params[:L], params[L:], dropout_p, dropout_seed, t, operand_rounding, aggregator)
         loss, dZ = softmax_ce(Z, labels, mask)
         losses.append(loss)
         dWs, dbs = backward(g, cache, params[:L], dZ)
-        adam_step(params, dWs + dbs, m, v, t, lr, beta1, beta2, eps)
+        if optimizer == "adam":
+            adam_step(params, dWs + dbs, m, v, t, lr, beta1, beta2, eps)
+        elif optimizer == "adamw":
+            adamw_step(params, dWs + dbs, m, v, t, lr, beta1, beta2, eps, weight_decay)
+        else:
+            sgd_step(params, dWs + dbs, m, lr, momentum, weight_decay)
     return losses, params
 
 
