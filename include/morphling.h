@@ -156,6 +156,39 @@ int mph_spmm(const mph_graph* g, const float* in_d, int32_t w, int32_t ld_in, fl
 int mph_spmm_part(const mph_graph* g, int32_t part, const float* in_d, int32_t w, int32_t ld_in, float* out_d,
                   int32_t ld_out, const mph_epilogue* epi, void* stream);
 
+/* Other aggregation schemes: "GCN uses normalized mean aggregation ...
+ * GIN employs sum aggregation", "multiple aggregation schemes (mean, max, sum)",
+ * Listing 1's SAGE "Max".  Reading R6: every scheme aggregates over Ñ(u) = N(u) ∪ {u}
+ * (the graph's CSR, diagonal included).  A linear scheme is AGG = diag(post)·Ã·diag(pre):
+ *   GCN  pre = post = D̃^{-1/2} (both directions)      SUM  none
+ *   MEAN forward post = D̃^{-1}; adjoint (transpose = 1, Ã·D̃^{-1}) pre = D̃^{-1}
+ * mph_graph_agg_scales returns the device arrays (n_cols floats; NULL = 1, borrowed).
+ * mph_aggregate: out[u,:] = post[u] · Σ_{v∈Ñ(u)} in[v,:] then the epilogue (BIAS, RELU,
+ * DROPOUT, ROWSCALE, TF32 as mph_spmm) — `in` must already carry the pre-scale (the producer
+ * applies it, as for the GCN's dinv).  Constraints and errors as mph_spmm. */
+#define MPH_AGG_GCN 0
+#define MPH_AGG_SUM 1
+#define MPH_AGG_MEAN 2
+#define MPH_AGG_MAX 3
+int mph_graph_agg_scales(const mph_graph* g, int32_t scheme, int32_t transpose, const float** pre_d,
+                         const float** post_d);
+int mph_aggregate(const mph_graph* g, int32_t scheme, int32_t transpose, const float* in_d, int32_t w, int32_t ld_in,
+                  float* out_d, int32_t ld_out, const mph_epilogue* epi, void* stream);
+/* Max aggregation (reading R7: applied before the transform; ties to the smallest
+ * neighbour id):  out[u,c] = max_{v∈Ñ(u)} in[v,c],  arg[u,c] = smallest v attaining it
+ * (arg_d nullable: not recorded).  Epilogue: TF32 only.  Values are compared exactly (no
+ * rounding before the comparison), so out and arg are bit-exact given the same input.
+ * w, ld_in, ld_out, ld_arg multiples of 4, 16-byte aligned, w <= 512.  Single GPU: MPH_ENOTSUP
+ * on a localized graph with world > 1 (arg holds local ids). */
+int mph_aggregate_max(const mph_graph* g, const float* in_d, int32_t w, int32_t ld_in, float* out_d, int32_t ld_out,
+                      int32_t* arg_d, int32_t ld_arg, const mph_epilogue* epi, void* stream);
+/* Its adjoint, the routing of every dY[u,c] to arg[u,c], computed as a gather over Ñ(v)
+ * (Ã symmetric; deterministic, no atomics):  dH[v,c] = Σ_{u∈Ñ(v)} [arg[u,c] = v]·dY[u,c],
+ * then the epilogue MASK (· (mask_src[v,c] > 0 ? mask_scale : 0): ReLU' and dropout of
+ * H_{l-1}) and TF32.  Other flags: MPH_EINVAL. */
+int mph_aggregate_max_backward(const mph_graph* g, const float* dY_d, int32_t w, int32_t ld_dy, const int32_t* arg_d,
+                               int32_t ld_arg, float* dH_d, int32_t ld_out, const mph_epilogue* epi, void* stream);
+
 /* a2/a4/a8 — dense transform on tcgen05 tensor cores (TF32 in, FP32 accumulate in TMEM):
  *   C[M, N] = epi( A[M, K] · Bt[N, K]^T )    A row-major (lda), Bt row-major (ldb)
  * TMA-fed, 128-row tiles, N <= 256 per tile.  Columns of C in [N, round_up(N,16)) are not
@@ -201,6 +234,22 @@ typedef struct {
 } mph_adam_cfg;
 int mph_adam(float* params_d, const float* grads_d, float* m_d, float* v_d, int64_t n, const mph_adam_cfg* cfg,
              int32_t t, void* stream);
+/* Optimizers of P:140 ("SGD, Adam, AdamW"; reading R8), one launch over a
+ * flat buffer:
+ *   ADAM   as mph_adam (weight_decay, momentum ignored)
+ *   SGD    d = g + wd·p;  momentum μ > 0: m = μ·m + d, d = m  (m_d: velocity, starts at 0);
+ *          p -= lr·d      (v_d unused, may be NULL)
+ *   ADAMW  p -= lr·wd·p (decoupled, before the update), then the Adam update
+ * t is 1-based (Adam / AdamW bias corrections). */
+#define MPH_OPT_ADAM 0
+#define MPH_OPT_SGD 1
+#define MPH_OPT_ADAMW 2
+typedef struct {
+  int32_t kind;
+  float lr, beta1, beta2, eps, weight_decay, momentum;
+} mph_optim_cfg;
+int mph_optim_step(float* params_d, const float* grads_d, float* m_d, float* v_d, int64_t n,
+                   const mph_optim_cfg* cfg, int32_t t, void* stream);
 
 /* Xavier-uniform fill ("xaviers", Listing 1; bound S:322; stream of reading Q16):
  *   W[i*ld + j] = (float)(a * (2*(x_{i*f_out+j} >> 40)/2^24 - 1)), a = sqrt(6/(f_in+f_out)),
@@ -278,6 +327,9 @@ typedef struct {
   float dropout_p;       /* 0 disables (default); inverted dropout after hidden ReLU (Q10) */
   uint64_t dropout_seed;
   int32_t order_policy;  /* 0 auto (Q7), 1 force transform-first everywhere */
+  int32_t aggregator;    /* MPH_AGG_GCN (default, the north star), _SUM, _MEAN (linear: the layer
+                            order of Q7 applies) or _MAX (Z = MAX(H)·W + b on every layer, R7;
+                            dense-mode features and a single GPU only, else MPH_ENOTSUP) */
 } mph_gcn_desc;
 
 /* graph may be global (comm NULL) or localized (comm non-NULL, world > 1); features hold the
@@ -305,6 +357,9 @@ int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream);
 /* One epoch a2..a11: forward, loss (written to loss_d, global sum over ranks), backward,
  * gradient all-reduce (P > 1), Adam step t.  Capturable in a CUDA graph when comm == NULL. */
 int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* loss_d, void* stream);
+/* The same with any optimizer of mph_optim_step (the Adam moments double as SGD velocity). */
+int mph_gcn_optim_step(mph_gcn* m, const mph_optim_cfg* cfg, int32_t t, void* stream);
+int mph_gcn_train_epoch_opt(mph_gcn* m, int32_t t, const mph_optim_cfg* cfg, double* loss_d, void* stream);
 /* CUDA-graph replay of whole epochs (single GPU; launch-bound configs).  mph_gcn_graph_capture
  * records one epoch (step-counter advance, forward, loss, backward, Adam with cfg) after at
  * least one eager mph_gcn_train_epoch (MPH_ESTATE otherwise); the next replay runs epoch
@@ -312,6 +367,7 @@ int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* 
  * device memory (mph_gcn_graph_state).  Replayed epochs are bitwise identical to eager ones.
  * Synchronises `stream` before capturing.  MPH_ENOTSUP for P > 1. */
 int mph_gcn_graph_capture(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t_next, void* stream);
+int mph_gcn_graph_capture_opt(mph_gcn* m, const mph_optim_cfg* cfg, int32_t t_next, void* stream);
 int mph_gcn_graph_replay(mph_gcn* m, void* stream);
 int mph_gcn_graph_state(const mph_gcn* m, int32_t** t_d, double** loss_d);
 /* Borrowed views of activations for tests: kind 0 = layer input H_{l-1} (l=1 is X),

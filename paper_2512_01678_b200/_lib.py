@@ -17,7 +17,9 @@ LIB_PATH = os.path.join(_HERE, "lib", "libmorphling.so")
 STATUS = {0: "MPH_OK", -1: "MPH_EINVAL", -2: "MPH_ERANGE", -3: "MPH_EDEGENERATE", -4: "MPH_ESTATE",
           -5: "MPH_ENOMEM", -6: "MPH_ECUDA", -7: "MPH_ENCCL", -8: "MPH_EDIVERGED", -9: "MPH_ENOTSUP"}
 
-EPI_BIAS, EPI_RELU, EPI_ROWSCALE, EPI_MASK, EPI_DROPOUT, EPI_COLSUM = 1, 2, 4, 8, 16, 32
+EPI_BIAS, EPI_RELU, EPI_ROWSCALE, EPI_MASK, EPI_DROPOUT, EPI_COLSUM, EPI_TF32 = 1, 2, 4, 8, 16, 32, 64
+AGG = {"gcn": 0, "sum": 1, "mean": 2, "max": 3}            # MPH_AGG_*
+OPT = {"adam": 0, "sgd": 1, "adamw": 2}                    # MPH_OPT_*
 
 
 class MorphlingError(RuntimeError):
@@ -38,9 +40,14 @@ class AdamCfg(C.Structure):
     _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
 
 
+class OptimCfg(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float), ("momentum", C.c_float)]
+
+
 class GcnDesc(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("dims_h", C.POINTER(C.c_int32)), ("dropout_p", C.c_float),
-                ("dropout_seed", C.c_uint64), ("order_policy", C.c_int32)]
+                ("dropout_seed", C.c_uint64), ("order_policy", C.c_int32), ("aggregator", C.c_int32)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -69,6 +76,10 @@ _SIGS = {
     "mph_features_destroy": [P],
     "mph_spmm": [P, P, i32, i32, P, i32, C.POINTER(Epilogue), P],
     "mph_spmm_part": [P, i32, P, i32, i32, P, i32, C.POINTER(Epilogue), P],
+    "mph_graph_agg_scales": [P, i32, i32, PP, PP],
+    "mph_aggregate": [P, i32, i32, P, i32, i32, P, i32, C.POINTER(Epilogue), P],
+    "mph_aggregate_max": [P, P, i32, i32, P, i32, P, i32, C.POINTER(Epilogue), P],
+    "mph_aggregate_max_backward": [P, P, i32, i32, P, i32, P, i32, C.POINTER(Epilogue), P],
     "mph_gemm_nt": [i32, i32, i32, P, i32, P, i32, P, i32, C.POINTER(Epilogue), P],
     "mph_gemm_tn_workspace": [i32, i32, i32, C.POINTER(sz)],
     "mph_gemm_tn": [i32, i32, i32, P, i32, P, i32, P, i32, P, sz, P],
@@ -78,6 +89,7 @@ _SIGS = {
     "mph_softmax_ce_workspace": [i32, i32, C.POINTER(sz)],
     "mph_softmax_ce": [P, i32, i32, i32, P, P, i64, P, P, i32, P, P, P, sz, P],
     "mph_adam": [P, P, P, P, i64, C.POINTER(AdamCfg), i32, P],
+    "mph_optim_step": [P, P, P, P, i64, C.POINTER(OptimCfg), i32, P],
     "mph_xavier_fill": [P, i32, i32, i32, u64, i32, P],
     "mph_partition_1d": [P, i32, i32, P],
     "mph_plan_create": [P, P, i32, P, i32, i32, PP],
@@ -107,6 +119,9 @@ _SIGS = {
     "mph_gcn_adam": [P, C.POINTER(AdamCfg), i32, P],
     "mph_gcn_train_epoch": [P, i32, C.POINTER(AdamCfg), P, P],
     "mph_gcn_graph_capture": [P, C.POINTER(AdamCfg), i32, P],
+    "mph_gcn_optim_step": [P, C.POINTER(OptimCfg), i32, P],
+    "mph_gcn_train_epoch_opt": [P, i32, C.POINTER(OptimCfg), P, P],
+    "mph_gcn_graph_capture_opt": [P, C.POINTER(OptimCfg), i32, P],
     "mph_gcn_graph_replay": [P, P],
     "mph_gcn_graph_state": [P, PP, PP],
     "mph_gcn_tensor": [P, i32, i32, PP, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],

@@ -16,9 +16,15 @@ import numpy as np
 import torch
 
 from . import _lib as L
-from ._lib import AdamCfg, Epilogue, GcnDesc, MorphlingError  # noqa: F401
+from ._lib import AdamCfg, Epilogue, GcnDesc, MorphlingError, OptimCfg  # noqa: F401
 
 DEFAULT_ADAM = (0.01, 0.9, 0.999, 1e-8)  # Listing 1; eps reading Q15
+
+
+def optimizer(kind: str = "adam", lr: float = 0.01, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+              weight_decay: float = 0.0, momentum: float = 0.0) -> OptimCfg:
+    """mph_optim_cfg for "adam" | "sgd" | "adamw" (reading R8)."""
+    return OptimCfg(L.OPT[kind], lr, beta1, beta2, eps, weight_decay, momentum)
 
 
 def pad_width(w: int) -> int:
@@ -244,12 +250,13 @@ class GCN:
     """The L-layer GCN training step (initializeLayers / forwardPass / backPropagation / optimizer)."""
 
     def __init__(self, graph: Graph, features: Features, dims, dropout_p: float = 0.0, dropout_seed: int = 0,
-                 order_policy: int = 0, comm: Comm | None = None, stream=None):
+                 order_policy: int = 0, comm: Comm | None = None, stream=None, aggregator: str = "gcn"):
         self.graph, self.features, self.comm = graph, features, comm
         self.dims = tuple(int(d) for d in dims)
         self.L = len(self.dims) - 1
+        self.aggregator = aggregator
         arr = (C.c_int32 * len(self.dims))(*self.dims)
-        desc = GcnDesc(self.L, arr, float(dropout_p), int(dropout_seed), int(order_policy))
+        desc = GcnDesc(self.L, arr, float(dropout_p), int(dropout_seed), int(order_policy), L.AGG[aggregator])
         h = _out_ptr()
         L.mph_gcn_create(graph.h, features.h, C.byref(desc), comm.h if comm is not None else None,
                          stream_ptr(stream), C.byref(h))
@@ -319,14 +326,24 @@ class GCN:
     def adam(self, t: int, cfg=DEFAULT_ADAM, stream=None):
         L.mph_gcn_adam(self.h, C.byref(AdamCfg(*cfg)), int(t), stream_ptr(stream))
 
+    def optim_step(self, t: int, cfg: OptimCfg, stream=None):
+        L.mph_gcn_optim_step(self.h, C.byref(cfg), int(t), stream_ptr(stream))
+
     def train_epoch(self, t: int, cfg=DEFAULT_ADAM, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """cfg: an Adam tuple (lr, b1, b2, eps) or an OptimCfg from optimizer(...)."""
         out = self.loss_buf if out is None else out
-        L.mph_gcn_train_epoch(self.h, int(t), C.byref(AdamCfg(*cfg)), out.data_ptr(), stream_ptr(stream))
+        if isinstance(cfg, OptimCfg):
+            L.mph_gcn_train_epoch_opt(self.h, int(t), C.byref(cfg), out.data_ptr(), stream_ptr(stream))
+        else:
+            L.mph_gcn_train_epoch(self.h, int(t), C.byref(AdamCfg(*cfg)), out.data_ptr(), stream_ptr(stream))
         return out
 
     def graph_capture(self, t_next: int, cfg=DEFAULT_ADAM, stream=None):
         """Record one whole epoch as a CUDA graph; each replay() then runs the next epoch."""
-        L.mph_gcn_graph_capture(self.h, C.byref(AdamCfg(*cfg)), int(t_next), stream_ptr(stream))
+        if isinstance(cfg, OptimCfg):
+            L.mph_gcn_graph_capture_opt(self.h, C.byref(cfg), int(t_next), stream_ptr(stream))
+        else:
+            L.mph_gcn_graph_capture(self.h, C.byref(AdamCfg(*cfg)), int(t_next), stream_ptr(stream))
         t, loss = C.c_void_p(), C.c_void_p()
         L.mph_gcn_graph_state(self.h, C.byref(t), C.byref(loss))
         self.graph_step = device_view(t.value, (1,), torch.int32)

@@ -22,7 +22,8 @@ static int ce_grid(int N) { return (int)std::max<int64_t>(1, std::min<int64_t>(c
 template <int NJ>
 __global__ void __launch_bounds__(kCeThreads) k_softmax_ce(const float* Z, int N, int C, int ld, const int32_t* labels,
                                                            const uint8_t* mask, float inv_nlab, const float* row_scale,
-                                                           float* dZ, int ld_dz, double* part_loss, float* part_db) {
+                                                           float* dZ, int ld_dz, double* part_loss, float* part_db,
+                                                           int round_tf32) {
   constexpr int R = NJ <= 2 ? 4 : (NJ <= 4 ? 2 : 1);
   __shared__ double s_loss[kCeThreads / 32];
   __shared__ float s_db[kCeThreads / 32][kCeMaxC];
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kCeThreads) k_softmax_ce(const float* Z, int N
           if (c == y) zy = zv[r][j];
           const float g = (expf(zv[r][j] - lse) - (c == y ? 1.0f : 0.0f)) * inv_nlab;
           dbacc[j] += g;
-          dz[c] = g * rsv[r];
+          dz[c] = round_tf32 ? tf32_rna(g * rsv[r]) : g * rsv[r];
         }
       }
 #pragma unroll
@@ -145,7 +146,7 @@ size_t softmax_ce_ws_bytes(int N, int C) {
 
 int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* labels, const uint8_t* mask, int64_t n_lab,
                       const float* row_scale, float* dZ, int ld_dz, float* db, double* loss, void* ws, size_t ws_bytes,
-                      cudaStream_t s) {
+                      cudaStream_t s, int round_tf32) {
   if (!Z || !labels || !dZ || !loss || N < 0 || C <= 0 || ld < C || ld_dz < C || n_lab <= 0)
     return fail(MPH_EINVAL, "softmax_ce: bad arguments");
   if (C > kCeMaxC) return fail(MPH_ENOTSUP, "softmax_ce: C=%d > %d", C, kCeMaxC);
@@ -158,7 +159,7 @@ int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* label
 #define CE_CASE(NJ)                                                                                              \
   case NJ:                                                                                                       \
     k_softmax_ce<NJ><<<g, kCeThreads, 0, s>>>(Z, N, C, ld, labels, mask, inv, row_scale, dZ, ld_dz, part_loss, \
-                                              part_db);                                                          \
+                                              part_db, round_tf32);                                              \
     break;
     CE_CASE(1) CE_CASE(2) CE_CASE(3) CE_CASE(4) CE_CASE(5) CE_CASE(6) CE_CASE(7) CE_CASE(8)
 #undef CE_CASE
@@ -171,29 +172,56 @@ int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* label
 // ------------------------------------------------------------------ a9 Adam
 // Bias corrections are computed on the device from t (host value, or device counter during a
 // CUDA-graph replay), so eager and graph epochs are bitwise identical.
-__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
-                       int64_t n, float lr, float b1, float b2, float eps, int t_host, const int32_t* t_dev) {
+__global__ void k_optim(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                        float* __restrict__ v, int64_t n, int kind, float lr, float b1, float b2, float eps, float wd,
+                        float mu, int t_host, const int32_t* t_dev) {
   const int t = t_dev ? *t_dev : t_host;
-  const float bc1 = (float)(1.0 - pow((double)b1, (double)t));
-  const float bc2 = (float)(1.0 - pow((double)b2, (double)t));
+  float bc1 = 1.0f, bc2 = 1.0f;
+  if (kind != MPH_OPT_SGD) {
+    bc1 = (float)(1.0 - pow((double)b1, (double)t));
+    bc2 = (float)(1.0 - pow((double)b2, (double)t));
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
+    if (kind == MPH_OPT_SGD) {  // d = g + wd·p; m = μ·m + d (μ > 0); p -= lr·d   (R8)
+      float d = wd != 0.0f ? gi + wd * p[i] : gi;
+      if (mu != 0.0f) {
+        d = mu * m[i] + d;
+        m[i] = d;
+      }
+      p[i] -= lr * d;
+      continue;
+    }
+    float pi = p[i];
+    if (kind == MPH_OPT_ADAMW) pi -= lr * wd * pi;  // decoupled weight decay before the update
     const float mi = b1 * m[i] + (1.0f - b1) * gi;
     const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
     m[i] = mi;
     v[i] = vi;
-    p[i] -= lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    p[i] = pi - lr * (mi / bc1) / (sqrtf(vi / bc2) + eps);
   }
+}
+
+int optim_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_optim_cfg* cfg, int t,
+                 cudaStream_t s, const int32_t* t_dev) {
+  if (!p || !g || !cfg || n < 0 || (t < 1 && !t_dev) || cfg->kind < MPH_OPT_ADAM || cfg->kind > MPH_OPT_ADAMW)
+    return fail(MPH_EINVAL, "optim: bad arguments");
+  if (cfg->kind != MPH_OPT_SGD && (!m || !v)) return fail(MPH_EINVAL, "optim: Adam/AdamW need m and v");
+  if (cfg->kind == MPH_OPT_SGD && cfg->momentum != 0.0f && !m) return fail(MPH_EINVAL, "optim: momentum needs m");
+  if (n == 0) return MPH_OK;
+  const float wd = cfg->kind == MPH_OPT_ADAM ? 0.0f : cfg->weight_decay;
+  const float mu = cfg->kind == MPH_OPT_SGD ? cfg->momentum : 0.0f;
+  k_optim<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(
+      p, g, m, v, n, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, wd, mu, t, t_dev);
+  count_launch();
+  return launch_check("optim");
 }
 
 int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s,
                 const int32_t* t_dev) {
-  if (!p || !g || !m || !v || !cfg || n < 0 || (t < 1 && !t_dev)) return fail(MPH_EINVAL, "adam: bad arguments");
-  if (n == 0) return MPH_OK;
-  k_adam<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(p, g, m, v, n, cfg->lr, cfg->beta1,
-                                                                                 cfg->beta2, cfg->eps, t, t_dev);
-  count_launch();
-  return launch_check("adam");
+  if (!cfg) return fail(MPH_EINVAL, "adam: bad arguments");
+  const mph_optim_cfg o{MPH_OPT_ADAM, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, 0.0f, 0.0f};
+  return optim_launch(p, g, m, v, n, &o, t, s, t_dev);
 }
 
 // ------------------------------------------------------------------ Xavier (Q16)
@@ -444,6 +472,11 @@ extern "C" int mph_softmax_ce(const float* Z_d, int32_t N, int32_t C, int32_t ld
 extern "C" int mph_adam(float* params_d, const float* grads_d, float* m_d, float* v_d, int64_t n, const mph_adam_cfg* cfg,
                         int32_t t, void* stream) {
   return adam_launch(params_d, grads_d, m_d, v_d, n, cfg, t, (cudaStream_t)stream);
+}
+
+extern "C" int mph_optim_step(float* params_d, const float* grads_d, float* m_d, float* v_d, int64_t n,
+                              const mph_optim_cfg* cfg, int32_t t, void* stream) {
+  return optim_launch(params_d, grads_d, m_d, v_d, n, cfg, t, (cudaStream_t)stream);
 }
 
 extern "C" int mph_xavier_fill(float* W_d, int32_t f_in, int32_t f_out, int32_t ld, uint64_t seed, int32_t layer,

@@ -31,8 +31,10 @@ struct Layer {
   float* out = nullptr;
   float* dZ = nullptr;
   float* G = nullptr;
-  float* Y = nullptr;
+  float* Y = nullptr;     // aggregate-first input (AF layer 1; every layer under max)
   float* colsum = nullptr;
+  int32_t* arg = nullptr;  // max aggregation: argmax of Y (layers > 1)
+  float* dY = nullptr;     // max aggregation: dZ·Wᵀ, the gradient routed back through arg
 };
 
 }  // namespace
@@ -43,6 +45,10 @@ struct mph_gcn {
   mph_comm* comm = nullptr;
   int world = 1;
   int L = 0;
+  int agg = MPH_AGG_GCN;  // aggregation scheme (NEXT-4)
+  // diagonal scales of a linear scheme: forward AGG = diag(fpost)·Ã·diag(fpre), adjoint
+  // diag(bpost)·Ã·diag(bpre); nullptr = 1 (aggregate.cu)
+  const float *fpre = nullptr, *fpost = nullptr, *bpre = nullptr, *bpost = nullptr;
   std::vector<Layer> layers;
   float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *wt = nullptr;
   float* wr = nullptr;  // TF32-rounded copy of the W segments (B operand of the dH GEMM)
@@ -68,7 +74,7 @@ struct mph_gcn {
   bool warm = false;        // one eager epoch done (lazy setup finished)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
-  mph_adam_cfg graph_cfg{};
+  mph_optim_cfg graph_cfg{};
 };
 
 namespace mph {
@@ -84,6 +90,8 @@ static void gcn_free(mph_gcn* m) {
     dev_free(l.G);
     dev_free(l.Y);
     dev_free(l.colsum);
+    dev_free(l.arg);
+    dev_free(l.dY);
   }
   dev_free(m->params);
   dev_free(m->grads);
@@ -118,18 +126,19 @@ static double spmm_bytes(const mph_graph* g, int w) {
   return 8.0 * (rows + 1) + 4.0 * nnz + 4.0 * rows + 4.0 * nnz * w + 4.0 * rows * w;
 }
 static int spmm_p(const mph_graph* g, const float* in, int w, int ld_in, float* out, int ld_out, const mph_epilogue* e,
-                  cudaStream_t s) {
+                  const float* post, cudaStream_t s) {
   prof::Scope sc(MPH_PROF_SPMM, s, spmm_bytes(g, w), 2.0 * (double)g->nnz * w);
-  return spmm_launch(g, -1, in, w, ld_in, out, ld_out, e, s);
+  return spmm_launch(g, -1, in, w, ld_in, out, ld_out, e, post, s);
 }
 
 // a10 + a3/a6: aggregation whose input's ghost rows come from their owners.  With P > 1 the
 // pack runs on the compute stream, the grouped send/recv on the comm stream, and the
 // local-edge part of the SpMM overlaps the transfer; the ghost-edge part and the fused
 // epilogue run once the halo has landed (overlap P:765).
-static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogue* e, cudaStream_t s) {
+static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogue* e, const float* post,
+                     cudaStream_t s) {
   const mph_graph* g = m->g;
-  if (m->world == 1) return spmm_p(g, in, w, w, out, w, e, s);
+  if (m->world == 1) return spmm_p(g, in, w, w, out, w, e, post, s);
   MPH_TRY(halo_pack(g, in, w, w, s));
   MPH_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
   MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_pack, 0));
@@ -139,9 +148,9 @@ static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogu
   }
   MPH_CUDA_TRY(cudaEventRecord(m->ev_halo, m->cs));
   prof::Scope sc(MPH_PROF_SPMM, s, spmm_bytes(g, w), 2.0 * (double)g->nnz * w);
-  MPH_TRY(spmm_launch(g, 0, in, w, w, out, w, nullptr, s));
+  MPH_TRY(spmm_launch(g, 0, in, w, w, out, w, nullptr, post, s));
   MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_halo, 0));
-  return spmm_launch(g, 1, in, w, w, out, w, e, s);
+  return spmm_launch(g, 1, in, w, w, out, w, e, post, s);
 }
 
 // a11: all-reduce one layer's [dW_l | b_l] gradient segment on the comm stream as soon as it is
@@ -175,6 +184,27 @@ static mph_epilogue epi_none() {
 
 static float dropout_scale(float p) { return p > 0.0f ? (float)(1.0 / (1.0 - (double)p)) : 1.0f; }
 
+// max aggregation (aggregate.cu): per edge 4 B id + 4·w gathered, per row ptr + Y (+ arg) rows
+static int aggmax_p(const mph_graph* g, const float* in, int w, int ld_in, float* Y, int32_t* arg, cudaStream_t s) {
+  prof::Scope sc(MPH_PROF_SPMM, s, 8.0 * (g->n_rows + 1) + (4.0 + 4.0 * w) * g->nnz + (arg ? 8.0 : 4.0) * w * g->n_rows,
+                 (double)g->nnz * w);
+  mph_epilogue en = epi_none();
+  en.flags = MPH_EPI_TF32;  // Y only feeds the GEMMs
+  return aggregate_max_launch(g, in, w, ld_in, Y, w, arg, w, &en, s);
+}
+// ... and its adjoint: per edge 4 B id + 8·w (dY and arg rows), per row ptr + mask read + dH write
+static int aggmax_bwd_p(const mph_graph* g, const float* dY, const int32_t* arg, int w, float* dH, const float* mask,
+                        float mask_scale, cudaStream_t s) {
+  prof::Scope sc(MPH_PROF_SPMM, s, 8.0 * (g->n_rows + 1) + (4.0 + 8.0 * w) * g->nnz + 8.0 * w * g->n_rows,
+                 (double)g->nnz * w);
+  mph_epilogue e = epi_none();
+  e.flags = MPH_EPI_MASK | MPH_EPI_TF32;  // dZ_{l-1} feeds the dW and dY GEMMs
+  e.mask_src = mask;
+  e.ld_mask = w;
+  e.mask_scale = mask_scale;
+  return aggregate_max_backward_launch(g, dY, w, w, arg, w, dH, w, &e, s);
+}
+
 static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
   Layer& l = m->layers[li];
   const mph_graph* g = m->g;
@@ -193,28 +223,33 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
     eo.dropout_epoch_d = m->graph_mode ? m->t_dev : nullptr;
     eo.row0 = g->row0;
   }
+  if (m->agg == MPH_AGG_MAX) {
+    // R7: Y_l = MAX(H_{l-1}) (with argmax; Y_1 = MAX(X) is prepared once), Z_l = Y_l·W_l + b
+    if (li > 0) MPH_TRY(aggmax_p(g, m->layers[li - 1].out, l.pin, l.pin, l.Y, l.arg, s));
+    return gemm_nt_p(g->n_rows, l.pout, l.pin, l.Y, l.pin, m->wt + l.off_wt, l.pin, l.out, l.pout, &eo, s);
+  }
   if (l.order == 0) {
-    // a2/a4: T' = dinv ⊙ (H_{l-1} · W_l)
+    // a2/a4: T' = pre ⊙ (H_{l-1} · W_l)   (pre = dinv for the GCN)
     if (li == 0 && m->f->mode == 1) {
       // no-reuse count (as for the SpMM): per nonzero 8 B (col, val) + a W row; per row ptr + T row
       prof::Scope sc(MPH_PROF_SPARSE, s, (8.0 + 4.0 * l.pout) * m->f->nnz + (8.0 + 4.0 * l.pout) * g->n_rows,
                      2.0 * m->f->nnz * l.pout);
-      MPH_TRY(sparse_xw_launch(m->f, m->params + l.off_w, l.pout, l.pout, g->dinv, l.T, l.pout, s));
+      MPH_TRY(sparse_xw_launch(m->f, m->params + l.off_w, l.pout, l.pout, m->fpre, l.T, l.pout, s));
     } else {
       const float* A = li == 0 ? m->Xr : m->layers[li - 1].out;
       const int lda = li == 0 ? m->f->P : m->layers[li - 1].pout;
       mph_epilogue et = epi_none();
-      et.flags = MPH_EPI_ROWSCALE;
-      et.row_scale = g->dinv;
+      et.flags = m->fpre ? MPH_EPI_ROWSCALE : 0u;
+      et.row_scale = m->fpre;
       MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, A, lda, m->wt + l.off_wt, l.pin, l.T, l.pout, &et, s));
     }
     // a10 + a3: ghost rows of T' from their owners; Z = Â·T + b, ReLU (dropout) fused
-    MPH_TRY(spmm_halo(m, l.T, l.pout, l.out, &eo, s));
+    MPH_TRY(spmm_halo(m, l.T, l.pout, l.out, &eo, m->fpost, s));
   } else {
     // aggregate-first layer 1: Y = Â·X (on dinv ⊙ X), Z = Y·W + b with the epilogue fused in the GEMM
     mph_epilogue en = epi_none();
     en.flags = MPH_EPI_TF32;  // Y only feeds the GEMMs
-    MPH_TRY(spmm_p(g, m->Xs, l.pin, l.pin, l.Y, l.pin, &en, s));
+    MPH_TRY(spmm_p(g, m->Xs, l.pin, l.pin, l.Y, l.pin, &en, m->fpost, s));
     MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, l.Y, l.pin, m->wt + l.off_wt, l.pin, l.out, l.pout, &eo, s));
   }
   return MPH_OK;
@@ -233,9 +268,11 @@ static int do_loss(mph_gcn* m, double* loss_d, cudaStream_t s) {
   if (!m->labels) return fail(MPH_ESTATE, "labels not set");
   Layer& l = m->layers[m->L - 1];
   prof::Scope sc(MPH_PROF_LOSS, s, 8.0 * m->g->n_rows * l.pout + 4.0 * m->g->n_rows, 0.0);
+  // TF: dZ' = bpre ⊙ dZ feeds the backward aggregation (FP32); max: dZ feeds the GEMMs (TF32)
+  const bool max_agg = m->agg == MPH_AGG_MAX;
   MPH_TRY(softmax_ce_launch(l.out, m->g->n_rows, l.fout, l.pout, m->labels, m->mask, m->n_lab,
-                            l.order == 0 ? m->g->dinv : nullptr, l.dZ, l.pout, m->grads + l.off_b, loss_d, m->ws,
-                            m->ws_bytes, s));
+                            (l.order == 0 && !max_agg) ? m->bpre : nullptr, l.dZ, l.pout, m->grads + l.off_b, loss_d,
+                            m->ws, m->ws_bytes, s, max_agg ? 1 : 0));
   m->loss_done = true;
   return MPH_OK;
 }
@@ -243,16 +280,29 @@ static int do_loss(mph_gcn* m, double* loss_d, cudaStream_t s) {
 static int do_backward(mph_gcn* m, cudaStream_t s) {
   if (!m->loss_done) return fail(MPH_ESTATE, "backward without a matching forward+loss (S:353)");
   const mph_graph* g = m->g;
-  for (int li = m->L - 1; li >= 0; --li) {
+  for (int li = m->L - 1; li >= 0 && m->agg == MPH_AGG_MAX; --li) {
+    // R7: Z = Y·W + b:  dW = Yᵀ·dZ;  dY = dZ·Wᵀ;  dZ_{l-1} = route(dY, arg) ⊙ ReLU'(H_{l-1}) (/(1-p))
+    Layer& l = m->layers[li];
+    MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, l.Y, l.pin, l.dZ, l.pout, m->grads + l.off_w, l.pout, m->ws,
+                      m->ws_bytes, s));
+    if (li > 0) {
+      Layer& pl = m->layers[li - 1];
+      MPH_TRY(gemm_nt_p(g->n_rows, l.pin, l.pout, l.dZ, l.pout, m->wr + l.off_w, l.pout, l.dY, l.pin, nullptr, s));
+      MPH_TRY(aggmax_bwd_p(g, l.dY, l.arg, l.pin, pl.dZ, pl.out, dropout_scale(m->dropout_p), s));
+      MPH_TRY(colsum_chunks_launch(pl.dZ, g->n_rows, pl.pout, pl.pout, pl.colsum, s));
+      MPH_TRY(reduce_rows_launch(pl.colsum, (int)ceil_div(g->n_rows, 128), pl.pout, pl.pout, m->grads + pl.off_b, 0, s));
+    }
+  }
+  for (int li = m->L - 1; li >= 0 && m->agg != MPH_AGG_MAX; --li) {
     Layer& l = m->layers[li];
     const float* Hin = li == 0 ? m->Xr : m->layers[li - 1].out;
     const int ld_in = li == 0 ? m->f->P : m->layers[li - 1].pout;
     const float* Gsrc;  // gradient w.r.t. the transform output (TF) or Z (AF)
     if (l.order == 0) {
-      // a10 + a6: G = Â·dZ (Â symmetric, same kernel as forward)
+      // a10 + a6: G = AGGᵀ·dZ = bpost ⊙ Ã·dZ' (Â symmetric: the forward kernel)
       mph_epilogue en = epi_none();
       en.flags = MPH_EPI_TF32;  // G only feeds the dW and dH GEMMs
-      MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, s));
+      MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, m->bpost, s));
       Gsrc = l.G;
       // a7: dW = H^T·G  (sparse layer 1: X_csc^T·G)
       if (li == 0 && m->f->mode == 1) {
@@ -279,12 +329,13 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       Layer& pl = m->layers[li - 1];
       mph_epilogue ed = epi_none();
       // TF: dZ' feeds the FP32 SpMM (keep FP32); AF: dZ_1 feeds only the dW GEMM (TF32)
-      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM | (pl.order == 0 ? MPH_EPI_ROWSCALE : MPH_EPI_TF32);
+      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM |
+                 (pl.order == 0 ? (m->bpre ? MPH_EPI_ROWSCALE : 0u) : MPH_EPI_TF32);
       ed.mask_src = pl.out;
       ed.ld_mask = pl.pout;
       ed.mask_scale = dropout_scale(m->dropout_p);
       ed.colsum_out = pl.colsum;
-      ed.row_scale = g->dinv;
+      ed.row_scale = m->bpre;
       MPH_TRY(gemm_nt_p(g->n_rows, pl.pout, l.pout, Gsrc, l.pout, m->wr + l.off_w, l.pout, pl.dZ, pl.pout, &ed,
                         s));
       MPH_TRY(reduce_rows_launch(pl.colsum, (int)ceil_div(g->n_rows, 128), pl.pout, pl.pout, m->grads + pl.off_b, 0, s));
@@ -310,9 +361,14 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   if (f->N != g->n_rows) return fail(MPH_EINVAL, "features rows (%d) != graph rows (%d)", f->N, g->n_rows);
   if (desc->dims_h[0] != f->F) return fail(MPH_EINVAL, "dims[0]=%d != feature width %d", desc->dims_h[0], f->F);
   if (desc->dropout_p < 0.0f || desc->dropout_p >= 1.0f) return fail(MPH_EINVAL, "dropout_p must be in [0,1)");
+  if (desc->aggregator < MPH_AGG_GCN || desc->aggregator > MPH_AGG_MAX)
+    return fail(MPH_EINVAL, "unknown aggregator %d", desc->aggregator);
   int world = 1;
   if (comm) MPH_TRY(mph_comm_info(comm, &world, nullptr));
   if (world > 1 && !g->local) return fail(MPH_EINVAL, "distributed model needs a localized graph");
+  const bool max_agg = desc->aggregator == MPH_AGG_MAX;
+  if (max_agg && (world > 1 || f->mode != 0))
+    return fail(MPH_ENOTSUP, "max aggregation: single GPU, dense-mode features only");
   for (int i = 0; i <= desc->num_layers; ++i)
     if (desc->dims_h[i] <= 0 || pad_width(desc->dims_h[i]) > 256 + (i == 0 ? 1 << 20 : 0))
       return fail(MPH_ENOTSUP, "layer width %d outside (0, 256]", desc->dims_h[i]);
@@ -325,6 +381,11 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   m->L = desc->num_layers;
   m->dropout_p = desc->dropout_p;
   m->dropout_seed = desc->dropout_seed;
+  m->agg = desc->aggregator;
+  if (!max_agg) {
+    MPH_TRY(agg_scales(g, m->agg, 0, &m->fpre, &m->fpost));
+    MPH_TRY(agg_scales(g, m->agg, 1, &m->bpre, &m->bpost));
+  }
   m->layers.resize(m->L);
   int64_t off = 0, offt = 0;
   for (int li = 0; li < m->L; ++li) {
@@ -335,6 +396,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     l.pout = pad_width(l.fout);
     // reading Q7: TF iff F_out <= F_in, or layer 1 in Sparse mode; AF only ever needed on layer 1
     l.order = (desc->order_policy == 1 || l.fout <= l.fin || (li == 0 && f->mode == 1) || li > 0) ? 0 : 1;
+    if (max_agg) l.order = 1;  // max is taken before the transform on every layer (R7)
     l.off_w = off;
     off = align16(off + (int64_t)l.pin * l.pout);
     l.off_b = off;
@@ -359,7 +421,11 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     if ((rc = dev_alloc(&l.out, (size_t)nr * l.pout))) return bail(rc);
     if ((rc = dev_alloc(&l.dZ, (size_t)(l.order == 0 ? nc : nr) * l.pout))) return bail(rc);
     if ((rc = dev_alloc(&l.colsum, (size_t)ceil_div(nr, 128) * l.pout))) return bail(rc);
-    if (l.order == 0) {
+    if (max_agg) {
+      if ((rc = dev_alloc(&l.Y, (size_t)nr * l.pin))) return bail(rc);
+      if (li > 0 && ((rc = dev_alloc(&l.arg, (size_t)nr * l.pin)) || (rc = dev_alloc(&l.dY, (size_t)nr * l.pin))))
+        return bail(rc);
+    } else if (l.order == 0) {
       if ((rc = dev_alloc(&l.T, (size_t)nc * l.pout))) return bail(rc);
       if ((rc = dev_alloc(&l.G, (size_t)nr * l.pout))) return bail(rc);
     } else {
@@ -377,6 +443,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     if (e == cudaSuccess && l.T) e = cudaMemsetAsync(l.T, 0, (size_t)nc * l.pout * 4, s);
     if (e == cudaSuccess && l.G) e = cudaMemsetAsync(l.G, 0, (size_t)nr * l.pout * 4, s);
     if (e == cudaSuccess && l.Y) e = cudaMemsetAsync(l.Y, 0, (size_t)nr * l.pin * 4, s);
+    if (e == cudaSuccess && l.dY) e = cudaMemsetAsync(l.dY, 0, (size_t)nr * l.pin * 4, s);
   }
   if (e == cudaSuccess) e = cudaMemsetAsync(m->params, 0, off * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(m->grads, 0, off * 4, s);
@@ -385,13 +452,19 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   if (e == cudaSuccess) e = cudaMemsetAsync(m->wt, 0, offt * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(m->wr, 0, off * 4, s);
   if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create memset: %s", cudaGetErrorString(e)));
-  if (m->layers[0].order == 1) {
-    // X is constant input data: its dinv pre-scale (and, distributed, its ghost rows) are set up once.
+  if (max_agg) {
+    // X is constant input data: Y_1 = MAX(X) is computed once (its argmax is never needed)
+    const Layer& l = m->layers[0];
+    mph_epilogue en = epi_none();
+    en.flags = MPH_EPI_TF32;  // Y_1 only feeds the GEMMs
+    if ((rc = aggregate_max_launch(g, f->X, l.pin, f->P, l.Y, l.pin, nullptr, 0, &en, s))) return bail(rc);
+  } else if (m->layers[0].order == 1) {
+    // X is constant input data: its pre-scale (and, distributed, its ghost rows) are set up once.
     const Layer& l = m->layers[0];
     if ((rc = dev_alloc(&m->Xs, (size_t)nc * l.pin))) return bail(rc);
     e = cudaMemsetAsync(m->Xs, 0, (size_t)nc * l.pin * 4, s);
     if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "memset: %s", cudaGetErrorString(e)));
-    if ((rc = rowscale_launch(f->X, f->P, g->dinv, (int)nr, l.pin, m->Xs, l.pin, 0, s))) return bail(rc);
+    if ((rc = rowscale_launch(f->X, f->P, m->fpre, (int)nr, l.pin, m->Xs, l.pin, 0, s))) return bail(rc);
     if (world > 1 && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
   }
   if (world > 1) {
@@ -403,7 +476,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     for (const auto& l : m->layers) wmax = std::max(wmax, l.pout);
     if ((rc = halo_reserve(g, wmax))) return bail(rc);  // no reallocation while sends are in flight
   }
-  if (m->layers[0].order == 0 && f->mode == 0) {
+  if (m->layers[0].order == 0 && f->mode == 0 && !max_agg) {
     // TF32-rounded copy of X: the A operand of the layer-1 transform and of its dW GEMM
     if ((rc = dev_alloc(&m->Xr, (size_t)nr * f->P))) return bail(rc);
     if ((rc = rowscale_launch(f->X, f->P, nullptr, (int)nr, f->P, m->Xr, f->P, 1, s))) return bail(rc);
@@ -464,9 +537,14 @@ extern "C" int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_
   else
     MPH_CUDA_TRY(cudaMemcpy2DAsync(f->X, (size_t)f->P * 4, X_h, (size_t)ld_h * 4, (size_t)f->F * 4, (size_t)f->N,
                                    cudaMemcpyHostToDevice, s));
-  if (m->layers[0].order == 1) {
+  if (m->agg == MPH_AGG_MAX) {
     const Layer& l = m->layers[0];
-    MPH_TRY(rowscale_launch(f->X, f->P, m->g->dinv, m->g->n_rows, l.pin, m->Xs, l.pin, 0, s));
+    mph_epilogue en = epi_none();
+    en.flags = MPH_EPI_TF32;
+    MPH_TRY(aggregate_max_launch(m->g, f->X, l.pin, f->P, l.Y, l.pin, nullptr, 0, &en, s));
+  } else if (m->layers[0].order == 1) {
+    const Layer& l = m->layers[0];
+    MPH_TRY(rowscale_launch(f->X, f->P, m->fpre, m->g->n_rows, l.pin, m->Xs, l.pin, 0, s));
     if (m->world > 1) MPH_TRY(mph_halo_exchange(m->g, m->comm, m->Xs, l.pin, l.pin, s));
   } else {
     MPH_TRY(rowscale_launch(f->X, f->P, nullptr, m->g->n_rows, f->P, m->Xr, f->P, 1, s));
@@ -507,22 +585,38 @@ extern "C" int mph_gcn_backward(mph_gcn* m, void* stream) {
   return do_backward(m, (cudaStream_t)stream);
 }
 
-extern "C" int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream) {
-  if (!m || !cfg) return fail(MPH_EINVAL, "gcn_adam arguments");
+static mph_optim_cfg as_optim(const mph_adam_cfg* c) {
+  return mph_optim_cfg{MPH_OPT_ADAM, c->lr, c->beta1, c->beta2, c->eps, 0.0f, 0.0f};
+}
+
+extern "C" int mph_gcn_optim_step(mph_gcn* m, const mph_optim_cfg* cfg, int32_t t, void* stream) {
+  if (!m || !cfg) return fail(MPH_EINVAL, "gcn_optim_step arguments");
   cudaStream_t s = (cudaStream_t)stream;
-  prof::Scope sc(MPH_PROF_ADAM, s, 28.0 * m->n_params, 0.0);
-  MPH_TRY(adam_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s, m->graph_mode ? m->t_dev : nullptr));
+  prof::Scope sc(MPH_PROF_ADAM, s, (cfg->kind == MPH_OPT_SGD ? 20.0 : 28.0) * m->n_params, 0.0);
+  MPH_TRY(optim_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s, m->graph_mode ? m->t_dev : nullptr));
   return refresh_wt(m, s);
 }
 
-extern "C" int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* loss_d, void* stream) {
+extern "C" int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream) {
+  if (!m || !cfg) return fail(MPH_EINVAL, "gcn_adam arguments");
+  const mph_optim_cfg o = as_optim(cfg);
+  return mph_gcn_optim_step(m, &o, t, stream);
+}
+
+extern "C" int mph_gcn_train_epoch_opt(mph_gcn* m, int32_t t, const mph_optim_cfg* cfg, double* loss_d, void* stream) {
   if (!m || !cfg || !loss_d || t < 1) return fail(MPH_EINVAL, "train_epoch arguments");
   MPH_TRY(mph_gcn_forward(m, t, stream));
   MPH_TRY(mph_gcn_loss(m, loss_d, stream));
   MPH_TRY(mph_gcn_backward(m, stream));
-  MPH_TRY(mph_gcn_adam(m, cfg, t, stream));
+  MPH_TRY(mph_gcn_optim_step(m, cfg, t, stream));
   m->warm = true;
   return MPH_OK;
+}
+
+extern "C" int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* loss_d, void* stream) {
+  if (!m || !cfg) return fail(MPH_EINVAL, "train_epoch arguments");
+  const mph_optim_cfg o = as_optim(cfg);
+  return mph_gcn_train_epoch_opt(m, t, &o, loss_d, stream);
 }
 
 namespace mph {
@@ -534,6 +628,12 @@ __global__ void k_step_advance(int32_t* t) { *t += 1; }
 // corrections and the dropout counter read it there.  Eager and replayed epochs run the same
 // kernels with the same arguments, so they are bitwise identical.
 extern "C" int mph_gcn_graph_capture(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t_next, void* stream) {
+  if (!m || !cfg) return fail(MPH_EINVAL, "graph_capture arguments");
+  const mph_optim_cfg o = as_optim(cfg);
+  return mph_gcn_graph_capture_opt(m, &o, t_next, stream);
+}
+
+extern "C" int mph_gcn_graph_capture_opt(mph_gcn* m, const mph_optim_cfg* cfg, int32_t t_next, void* stream) {
   if (!m || !cfg || t_next < 1) return fail(MPH_EINVAL, "graph_capture arguments");
   if (m->world > 1) return fail(MPH_ENOTSUP, "graph capture is single-GPU (NCCL p2p is issued eagerly)");
   if (!m->warm) return fail(MPH_ESTATE, "run one eager mph_gcn_train_epoch before capturing (lazy setup)");
@@ -563,7 +663,7 @@ extern "C" int mph_gcn_graph_capture(mph_gcn* m, const mph_adam_cfg* cfg, int32_
     rc = do_forward(m, t_next, cap);
     if (rc == MPH_OK) rc = do_loss(m, m->loss_dev, cap);
     if (rc == MPH_OK) rc = do_backward(m, cap);
-    if (rc == MPH_OK) rc = mph_gcn_adam(m, &m->graph_cfg, t_next, cap);
+    if (rc == MPH_OK) rc = mph_gcn_optim_step(m, &m->graph_cfg, t_next, cap);
     cudaGraph_t gph = nullptr;
     cudaError_t e2 = cudaStreamEndCapture(cap, &gph);
     if (rc == MPH_OK && e2 != cudaSuccess) rc = fail(MPH_ECUDA, "EndCapture: %s", cudaGetErrorString(e2));

@@ -69,16 +69,17 @@ __global__ void k_degrees(const int64_t* row_ptr, int32_t n, int32_t* deg) {
     deg[u] = (int32_t)(row_ptr[u + 1] - row_ptr[u]);  // G5
 }
 
-__global__ void k_dinv(const int32_t* deg, float* dinv, int64_t n) {
+__global__ void k_dinv(const int32_t* deg, float* dinv, float* dinv1, int64_t n) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
     double d = (double)deg[u];
     dinv[u] = __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(d)));  // G6
+    dinv1[u] = __double2float_rn(__ddiv_rn(1.0, d));             // mean aggregation (R6)
   }
 }
 
-int launch_dinv(const int32_t* deg, float* dinv, int64_t n, cudaStream_t s) {
+int launch_dinv(const int32_t* deg, float* dinv, float* dinv1, int64_t n, cudaStream_t s) {
   if (n == 0) return MPH_OK;
-  k_dinv<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4096), 256, 0, s>>>(deg, dinv, n);
+  k_dinv<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 4096), 256, 0, s>>>(deg, dinv, dinv1, n);
   count_launch();
   return launch_check("dinv");
 }
@@ -93,6 +94,7 @@ static void graph_free(mph_graph* g) {
   dev_free(g->col_idx);
   dev_free(g->deg);
   dev_free(g->dinv);
+  dev_free(g->dinv1);
   dev_free(g->split);
   dev_free(g->send_ids);
   dev_free(g->send_buf);
@@ -223,12 +225,13 @@ extern "C" int mph_graph_build(const int32_t* src_h, const int32_t* dst_h, int64
   GB_TRY(dev_alloc(&g->col_idx, (size_t)nnz));
   GB_TRY(dev_alloc(&g->deg, (size_t)n));
   GB_TRY(dev_alloc(&g->dinv, (size_t)n));
+  GB_TRY(dev_alloc(&g->dinv1, (size_t)n));
   k_split_keys<<<grid_for(nnz), 256, 0, s>>>(keys, nnz, g->col_idx);
   k_lower_bound_hi<<<grid_for(n + 1), 256, 0, s>>>(keys, nnz, (int32_t)n, g->row_ptr);
   k_degrees<<<grid_for(n), 256, 0, s>>>(g->row_ptr, (int32_t)n, g->deg);
   count_launch(3);
   GB_CUDA(cudaGetLastError());
-  GB_TRY(launch_dinv(g->deg, g->dinv, n, s));
+  GB_TRY(launch_dinv(g->deg, g->dinv, g->dinv1, n, s));
   GB_TRY(max_degree(g, s, &g->max_deg));
   cleanup();
 #undef GB_TRY
@@ -438,6 +441,7 @@ extern "C" int mph_graph_from_plan(const mph_plan* p, void* stream, mph_graph** 
   if ((rc = dev_alloc(&g->col_idx, (size_t)g->nnz)) != MPH_OK) return bail(rc);
   if ((rc = dev_alloc(&g->deg, (size_t)g->n_cols)) != MPH_OK) return bail(rc);
   if ((rc = dev_alloc(&g->dinv, (size_t)g->n_cols)) != MPH_OK) return bail(rc);
+  if ((rc = dev_alloc(&g->dinv1, (size_t)g->n_cols)) != MPH_OK) return bail(rc);
   if ((rc = dev_alloc(&g->split, (size_t)g->n_rows)) != MPH_OK) return bail(rc);
   if ((rc = dev_alloc(&split_count, (size_t)g->n_rows)) != MPH_OK) return bail(rc);
   if ((rc = dev_alloc(&g->send_ids, (size_t)g->n_send)) != MPH_OK) return bail(rc);
@@ -456,7 +460,7 @@ extern "C" int mph_graph_from_plan(const mph_plan* p, void* stream, mph_graph** 
     k_split_abs<<<grid_for(g->n_rows), 256, 0, s>>>(g->row_ptr, split_count, g->n_rows, g->split);
     count_launch();
   }
-  if ((rc = launch_dinv(g->deg, g->dinv, g->n_cols, s)) != MPH_OK) return bail(rc);
+  if ((rc = launch_dinv(g->deg, g->dinv, g->dinv1, g->n_cols, s)) != MPH_OK) return bail(rc);
   if ((rc = max_degree(g, s, &g->max_deg)) != MPH_OK) return bail(rc);  // synchronises
   dev_free(split_count);
   *out = g;

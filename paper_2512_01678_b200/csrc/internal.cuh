@@ -13,7 +13,8 @@ struct mph_graph {
   int64_t* row_ptr = nullptr;  // [n_rows+1]
   int32_t* col_idx = nullptr;  // [nnz] (local ids for a localized graph)
   int32_t* deg = nullptr;      // [n_cols] global degree d~
-  float* dinv = nullptr;       // [n_cols]
+  float* dinv = nullptr;       // [n_cols] D̃^{-1/2} (G6)
+  float* dinv1 = nullptr;      // [n_cols] D̃^{-1} (mean aggregation, R6)
   // localized graphs only (D2-D4)
   bool local = false;
   int32_t world = 1, rank = 0;
@@ -62,12 +63,21 @@ constexpr int64_t kSegNnz = 128;
 namespace mph {
 
 // dinv[u] = (float)(1.0 / sqrt((double)deg[u]))  (G6)
-int launch_dinv(const int32_t* deg, float* dinv, int64_t n, cudaStream_t s);
+int launch_dinv(const int32_t* deg, float* dinv, float* dinv1, int64_t n, cudaStream_t s);
 
 // SpMM driver (spmm.cu). part: -1 whole row, 0 owned columns (raw sums, no epilogue),
 // 1 ghost columns accumulated onto out + epilogue.
+// post: the output row scale (D̃^{-1/2} for the GCN's Â, D̃^{-1} for mean, nullptr for sum).
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
-                const mph_epilogue* epi, cudaStream_t s);
+                const mph_epilogue* epi, const float* post, cudaStream_t s);
+int ensure_graph_items(const mph_graph* g, cudaStream_t s);
+// aggregate.cu (NEXT-4): scheme scales, max aggregation and its adjoint, chunked column sums
+int agg_scales(const mph_graph* g, int scheme, int transpose, const float** pre, const float** post);
+int aggregate_max_launch(const mph_graph* g, const float* in, int w, int ld_in, float* out, int ld_out, int32_t* arg,
+                         int ld_arg, const mph_epilogue* epi, cudaStream_t s);
+int aggregate_max_backward_launch(const mph_graph* g, const float* dY, int w, int ld_dy, const int32_t* arg, int ld_arg,
+                                  float* dH, int ld_out, const mph_epilogue* epi, cudaStream_t s);
+int colsum_chunks_launch(const float* in, int rows, int cols, int ld, float* part, cudaStream_t s);
 // Edge-balanced work items over a CSR whose row_ptr lives on the device (synchronises; setup only).
 int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** items, int* n_items, cudaStream_t s);
 // The same gather kernel on a general CSR: out[r,:] = row_scale[r] * sum_e val[e] * in[col[e],:]
@@ -93,9 +103,11 @@ int reduce_rows_launch(const float* in, int rows, int cols, int ld, float* out, 
 size_t softmax_ce_ws_bytes(int N, int C);
 int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* labels, const uint8_t* mask, int64_t n_lab,
                       const float* row_scale, float* dZ, int ld_dz, float* db, double* loss, void* ws, size_t ws_bytes,
-                      cudaStream_t s);
+                      cudaStream_t s, int round_tf32 = 0);
 int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s,
                 const int32_t* t_dev = nullptr);
+int optim_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_optim_cfg* cfg, int t,
+                 cudaStream_t s, const int32_t* t_dev = nullptr);
 int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int layer, cudaStream_t s);
 // dst_t[j*ld_t + i] = tf32(src[i*ld_src + j]), dst_r[i*ld_r + j] = tf32(src[i*ld_src + j]) (dst_r nullable)
 int weight_copies_launch(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,

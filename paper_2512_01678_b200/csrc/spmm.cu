@@ -258,7 +258,7 @@ int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** i
   return MPH_OK;
 }
 
-static int build_items(const mph_graph* gc, cudaStream_t s) {
+int ensure_graph_items(const mph_graph* gc, cudaStream_t s) {
   mph_graph* g = const_cast<mph_graph*>(gc);
   if (g->items) return MPH_OK;
   MPH_TRY(build_work_items(g->row_ptr, g->n_rows, g->nnz, &g->items, &g->n_items, s));
@@ -300,7 +300,7 @@ static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
 }
 
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
-                const mph_epilogue* epi, cudaStream_t s) {
+                const mph_epilogue* epi, const float* post, cudaStream_t s) {
   if (!g || !in || !out) return fail(MPH_EINVAL, "spmm: null argument");
   if (w <= 0 || w % 4 || ld_in % 4 || ld_out % 4 || ld_in < w || ld_out < w)
     return fail(MPH_EINVAL, "spmm: w, ld_in, ld_out must be multiples of 4 with ld >= w (w=%d)", w);
@@ -314,13 +314,13 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
     return fail(MPH_EINVAL, "spmm: bias must be non-null and 16-byte aligned");
   if (epi && (epi->flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "spmm: null row_scale");
   if (g->n_rows == 0) return MPH_OK;
-  MPH_TRY(build_items(g, s));
+  MPH_TRY(ensure_graph_items(g, s));
   SpmmArgs a{};
   a.val = nullptr;
   a.row_ptr = g->row_ptr;
   a.split = g->split;
   a.col = g->col_idx;
-  a.dinv = g->dinv;
+  a.dinv = post;
   a.in = in;
   a.out = out;
   a.items = g->items;
@@ -393,11 +393,13 @@ int pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int w, fl
 
 extern "C" int mph_spmm(const mph_graph* g, const float* in_d, int32_t w, int32_t ld_in, float* out_d, int32_t ld_out,
                         const mph_epilogue* epi, void* stream) {
-  return mph::spmm_launch(g, -1, in_d, w, ld_in, out_d, ld_out, epi, (cudaStream_t)stream);
+  if (!g) return mph::fail(MPH_EINVAL, "spmm: null argument");
+  return mph::spmm_launch(g, -1, in_d, w, ld_in, out_d, ld_out, epi, g->dinv, (cudaStream_t)stream);
 }
 
 extern "C" int mph_spmm_part(const mph_graph* g, int32_t part, const float* in_d, int32_t w, int32_t ld_in, float* out_d,
                              int32_t ld_out, const mph_epilogue* epi, void* stream) {
   if (part < -1 || part > 1) return mph::fail(MPH_EINVAL, "spmm_part: part must be -1, 0 or 1");
-  return mph::spmm_launch(g, part, in_d, w, ld_in, out_d, ld_out, epi, (cudaStream_t)stream);
+  if (!g) return mph::fail(MPH_EINVAL, "spmm: null argument");
+  return mph::spmm_launch(g, part, in_d, w, ld_in, out_d, ld_out, epi, g->dinv, (cudaStream_t)stream);
 }

@@ -1,0 +1,216 @@
+"""Parity of the other aggregation schemes and optimizers through the C-ABI
+against the FP64 oracle (pins in tests/test_oracle_aggregators.py).
+
+* mph_aggregate (sum / mean, forward and adjoint): FP32 aggregation bound 1e-5·(|AGG|·|P|);
+* mph_aggregate_max: Y and arg bit-exact (max is exact; ties -> smallest id), incl. a wide
+  (column-slab) case; mph_aggregate_max_backward: FP32 bound on the routed sums, MASK epilogue;
+* mph_optim_step SGD / AdamW: against the oracle steps;
+* the whole training step with aggregator = sum / mean / max and optimizer = sgd / adamw: the
+  10-epoch loss trajectory within 1e-3 (Q24) and first-epoch gradients.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth.generate import make_small, make_workload
+from tests.gpu_helpers import cuda, padded
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2512_01678_b200 as P
+    from paper_2512_01678_b200 import _lib as L
+    L.mph_device_check(C.byref(C.c_int32()))
+    return P
+
+
+@pytest.fixture(scope="module")
+def graph_case():
+    w = make_small(3001, 40000, 8, 4, seed=11)
+    return w, oracle.graph_build(w["src"], w["dst"], 3001)
+
+
+def _scale(ptr, n):
+    if not ptr:
+        return np.ones(n, np.float32)
+    from paper_2512_01678_b200.api import device_view
+    return device_view(ptr, (n,), torch.float32).cpu().numpy()
+
+
+@pytest.mark.parametrize("scheme", ["sum", "mean", "gcn"])
+@pytest.mark.parametrize("transpose", [0, 1])
+@pytest.mark.parametrize("w_", [4, 16, 48, 128, 256])
+def test_linear_aggregate(P, graph_case, scheme, transpose, w_):
+    from paper_2512_01678_b200 import _lib as L
+    w, ref = graph_case
+    n = ref.num_nodes
+    g = P.Graph(w["src"], w["dst"], n)
+    pre, post = C.c_void_p(), C.c_void_p()
+    L.mph_graph_agg_scales(g.h, L.AGG[scheme], transpose, C.byref(pre), C.byref(post))
+    X = np.random.default_rng(w_).standard_normal((n, w_)).astype(np.float32)
+    Xin = (X * _scale(pre.value, n)[:, None]).astype(np.float32)       # the producer's pre-scale
+    out = torch.zeros((n, w_), device="cuda")
+    L.mph_aggregate(g.h, L.AGG[scheme], transpose, cuda(Xin).data_ptr(), w_, w_, out.data_ptr(), w_, None,
+                    torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    exp = oracle.aggregate_scheme(ref, X, scheme, transpose=bool(transpose))
+    bound = oracle.aggregate_scheme(ref, np.abs(X.astype(np.float64)), scheme, transpose=bool(transpose))
+    err = np.abs(out.cpu().numpy() - exp)
+    assert float((err / (1e-5 * bound + 1e-30)).max()) <= 1.0
+
+
+@pytest.mark.parametrize("w_,ties", [(4, True), (16, True), (48, False), (128, True), (256, False), (1000, True)])
+def test_max_aggregate_bit_exact(P, graph_case, w_, ties):
+    from paper_2512_01678_b200 import _lib as L
+    w, ref = graph_case
+    n = ref.num_nodes
+    g = P.Graph(w["src"], w["dst"], n)
+    rng = np.random.default_rng(w_)
+    X = (rng.integers(0, 4, (n, w_)) if ties else rng.standard_normal((n, w_))).astype(np.float32)
+    X[::7] = np.maximum(X[::7], 0)                                        # post-ReLU-like rows with zero ties
+    Y = torch.full((n, w_), 7.0, device="cuda")
+    arg = torch.full((n, w_), -5, dtype=torch.int32, device="cuda")
+    L.mph_aggregate_max(g.h, cuda(X).data_ptr(), w_, w_, Y.data_ptr(), w_, arg.data_ptr(), w_, None,
+                        torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    Yr, ar = oracle.aggregate_max(ref, X)
+    assert np.array_equal(Y.cpu().numpy(), Yr.astype(np.float32))
+    assert np.array_equal(arg.cpu().numpy(), ar.astype(np.int32))
+
+
+@pytest.mark.parametrize("w_,masked", [(8, False), (48, True), (128, True), (256, False)])
+def test_max_backward(P, graph_case, w_, masked):
+    from paper_2512_01678_b200 import _lib as L
+    w, ref = graph_case
+    n = ref.num_nodes
+    g = P.Graph(w["src"], w["dst"], n)
+    rng = np.random.default_rng(w_ + 1)
+    H = np.maximum(rng.standard_normal((n, w_)), 0).astype(np.float32)
+    _, arg = oracle.aggregate_max(ref, H)
+    dY = rng.standard_normal((n, w_)).astype(np.float32)
+    dH = torch.zeros((n, w_), device="cuda")
+    e = L.Epilogue()
+    e.mask_scale = 1.0
+    if masked:
+        e.flags = L.EPI_MASK
+        th = cuda(H)
+        e.mask_src, e.ld_mask, e.mask_scale = th.data_ptr(), w_, 1.25
+    L.mph_aggregate_max_backward(g.h, cuda(dY).data_ptr(), w_, w_, cuda(arg.astype(np.int32)).data_ptr(), w_,
+                                 dH.data_ptr(), w_, C.byref(e), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    exp = oracle.aggregate_max_backward(dY, arg, n)
+    bound = oracle.aggregate_max_backward(np.abs(dY.astype(np.float64)), arg, n)
+    if masked:
+        keep = (H > 0) * 1.25
+        exp, bound = exp * keep, bound * keep
+    err = np.abs(dH.cpu().numpy() - exp)
+    assert float((err / (1e-5 * bound + 1e-30)).max()) <= 1.0
+
+
+@pytest.mark.parametrize("kind,kw", [("sgd", {}), ("sgd", {"momentum": 0.9}), ("sgd", {"momentum": 0.9, "weight_decay": 0.01}),
+                                     ("adamw", {"weight_decay": 0.05})])
+def test_optimizers_match_oracle(P, kind, kw):
+    from paper_2512_01678_b200 import _lib as L
+    n = 100003
+    rng = np.random.default_rng(2)
+    p0 = rng.standard_normal(n).astype(np.float32)
+    p, m, v = cuda(p0), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    rp, rm, rv = [p0.astype(np.float64)], [np.zeros(n)], [np.zeros(n)]
+    cfg = P.optimizer(kind, lr=0.01, **kw)
+    s = torch.cuda.current_stream().cuda_stream
+    for t in range(1, 6):
+        gr = rng.standard_normal(n).astype(np.float32)
+        L.mph_optim_step(p.data_ptr(), cuda(gr).data_ptr(), m.data_ptr(), v.data_ptr(), n, C.byref(cfg), t, s)
+        if kind == "sgd":
+            oracle.sgd_step(rp, [gr.astype(np.float64)], rm, lr=0.01, **kw)
+        else:
+            oracle.adamw_step(rp, [gr.astype(np.float64)], rm, rv, t, lr=0.01, **kw)
+    torch.cuda.synchronize()
+    assert np.allclose(p.cpu().numpy(), rp[0], rtol=0, atol=3e-6)
+
+
+# ---------------------------------------------------------------- the training step
+def _model(P, w, dims, agg, force_mode=-1, dropout_p=0.0):
+    n = w["X"].shape[0]
+    g = P.Graph(w["src"], w["dst"], n)
+    f = P.Features(cuda(w["X"]), force_mode=force_mode)
+    m = P.GCN(g, f, dims, aggregator=agg, dropout_p=dropout_p, dropout_seed=5)
+    m.init_xavier(42)
+    m.set_labels(cuda(w["y"].astype(np.int32)))
+    return g, f, m
+
+
+@pytest.mark.parametrize("agg,opt,kw", [("sum", "adam", {}), ("mean", "adam", {}), ("max", "adam", {}),
+                                        ("gcn", "sgd", {"lr": 0.05, "momentum": 0.9}),
+                                        ("mean", "adamw", {"weight_decay": 0.01}),
+                                        ("max", "sgd", {"lr": 0.05, "momentum": 0.9})])
+def test_training_trajectory(P, agg, opt, kw):
+    w = make_small(2000, 16000, 24, 5, seed=4)
+    dims = (24, 32, 16, 5)
+    _, _, m = _model(P, w, dims, agg)
+    cfg = P.optimizer(opt, **kw)
+    got = [m.train_epoch(t, cfg).item() for t in range(1, 11)]
+    ref_g = oracle.graph_build(w["src"], w["dst"], 2000)
+    okw = dict(kw)
+    lr = okw.pop("lr", 0.01)
+    ref, _ = oracle.train(ref_g, w["X"], w["y"], dims, epochs=10, seed=42, aggregator=agg, optimizer=opt, lr=lr, **okw)
+    for t, (a, b) in enumerate(zip(got, ref), 1):
+        assert abs(a - b) <= 1e-3 * max(1.0, abs(b)), f"{agg}/{opt} epoch {t}: gpu {a} vs oracle {b}"
+    assert got[-1] < got[0]
+
+
+@pytest.mark.parametrize("name,agg,mode", [("cora", "mean", -1), ("cora", "sum", -1), ("pubmed", "max", 0),
+                                           ("arxiv", "mean", -1)])
+def test_first_epoch_gradients_workloads(P, name, agg, mode):
+    """Sparse-mode layer 1 (cora), a forced-dense max model (pubmed), an aggregate-first layer 1
+    (arxiv, mean): loss and every gradient against the oracle with TF32 GEMM operands (R4)."""
+    w = make_workload(name)
+    dims = w["cfg"].dims
+    _, f, m = _model(P, w, dims, agg, force_mode=mode)
+    m.forward(1)
+    lg = m.loss().item()
+    m.backward()
+    torch.cuda.synchronize()
+    ref_g = oracle.graph_build(w["src"], w["dst"], w["X"].shape[0])
+    Ws, bs = oracle.xavier_init(dims, 42)
+    Z, _ = oracle.forward(ref_g, w["X"], Ws, bs, aggregator=agg)
+    lr, _ = oracle.softmax_ce(Z, w["y"])
+    assert abs(lg - lr) <= 1e-4 * abs(lr)
+    af = m.order[0] == 1 and agg != "max"
+    rounding = None if af else "tf32"      # the oracle's TF32 option models transform-first / max layers
+    Zt, ct = oracle.forward(ref_g, w["X"], Ws, bs, aggregator=agg, operand_rounding=rounding)
+    _, dZt = oracle.softmax_ce(Zt, w["y"])
+    dWs, dbs = oracle.backward(ref_g, ct, Ws, dZt)
+    for l, (dWg, dbg) in enumerate(m.grads()):
+        for got, exp in ((dWg, dWs[l]), (dbg, dbs[l])):
+            got = got.cpu().numpy().astype(np.float64)
+            rel = np.linalg.norm(got - exp) / max(np.linalg.norm(exp), 1e-30)
+            assert rel <= 2e-3, f"{name}/{agg} layer {l + 1}: gradient rel err {rel:.3g}"
+
+
+def test_max_rejects_sparse_features(P):
+    from paper_2512_01678_b200._lib import MorphlingError
+    w = make_workload("cora")
+    with pytest.raises(MorphlingError) as e:
+        _model(P, w, w["cfg"].dims, "max")
+    assert e.value.name == "MPH_ENOTSUP"
+
+
+@pytest.mark.parametrize("agg,opt", [("max", "sgd"), ("mean", "adamw")])
+def test_graph_replay_bitwise_equals_eager_other_schemes(P, agg, opt):
+    w = make_small(1500, 12000, 16, 4, seed=9)
+    dims = (16, 24, 4)
+    cfg = P.optimizer(opt, lr=0.02, momentum=0.9 if opt == "sgd" else 0.0, weight_decay=0.01)
+    _, _, a = _model(P, w, dims, agg, dropout_p=0.3)
+    _, _, b = _model(P, w, dims, agg, dropout_p=0.3)
+    la = [a.train_epoch(t, cfg).item() for t in range(1, 7)]
+    lb = [b.train_epoch(1, cfg).item()]
+    b.graph_capture(2, cfg)
+    lb += [b.replay().item() for _ in range(5)]
+    assert la == lb
+    assert torch.equal(a.params_flat, b.params_flat)
