@@ -6,7 +6,8 @@ Importing this package fails if the shared library has not been built — there 
 no CPU fallback.
 """
 from . import _lib  # noqa: F401  (raises ImportError when the library is missing)
-from .api import (Comm, Features, GCN, Graph, Plan, device_view, pad_width,  # noqa: F401
+from .api import (Comm, Features, GCN, Graph, Plan, device_view, optimizer, pad_width,  # noqa: F401
                   partition_1d, stream_ptr)
 
-__all__ = ["Comm", "Features", "GCN", "Graph", "Plan", "device_view", "pad_width", "partition_1d", "stream_ptr"]
+__all__ = ["Comm", "Features", "GCN", "Graph", "Plan", "device_view", "optimizer", "pad_width", "partition_1d",
+           "stream_ptr"]

@@ -16,7 +16,7 @@ import torch
 
 import oracle
 from synth.generate import make_small, make_workload
-from tests.gpu_helpers import cuda, padded
+from tests.gpu_helpers import cuda
 
 pytestmark = pytest.mark.gpu
 
@@ -55,7 +55,8 @@ def test_linear_aggregate(P, graph_case, scheme, transpose, w_):
     X = np.random.default_rng(w_).standard_normal((n, w_)).astype(np.float32)
     Xin = (X * _scale(pre.value, n)[:, None]).astype(np.float32)       # the producer's pre-scale
     out = torch.zeros((n, w_), device="cuda")
-    L.mph_aggregate(g.h, L.AGG[scheme], transpose, cuda(Xin).data_ptr(), w_, w_, out.data_ptr(), w_, None,
+    tin = cuda(Xin)                       # keep every device input referenced until the kernel ran
+    L.mph_aggregate(g.h, L.AGG[scheme], transpose, tin.data_ptr(), w_, w_, out.data_ptr(), w_, None,
                     torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     exp = oracle.aggregate_scheme(ref, X, scheme, transpose=bool(transpose))
@@ -75,7 +76,8 @@ def test_max_aggregate_bit_exact(P, graph_case, w_, ties):
     X[::7] = np.maximum(X[::7], 0)                                        # post-ReLU-like rows with zero ties
     Y = torch.full((n, w_), 7.0, device="cuda")
     arg = torch.full((n, w_), -5, dtype=torch.int32, device="cuda")
-    L.mph_aggregate_max(g.h, cuda(X).data_ptr(), w_, w_, Y.data_ptr(), w_, arg.data_ptr(), w_, None,
+    tx = cuda(X)
+    L.mph_aggregate_max(g.h, tx.data_ptr(), w_, w_, Y.data_ptr(), w_, arg.data_ptr(), w_, None,
                         torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     Yr, ar = oracle.aggregate_max(ref, X)
@@ -100,7 +102,8 @@ def test_max_backward(P, graph_case, w_, masked):
         e.flags = L.EPI_MASK
         th = cuda(H)
         e.mask_src, e.ld_mask, e.mask_scale = th.data_ptr(), w_, 1.25
-    L.mph_aggregate_max_backward(g.h, cuda(dY).data_ptr(), w_, w_, cuda(arg.astype(np.int32)).data_ptr(), w_,
+    tdy, targ = cuda(dY), cuda(arg.astype(np.int32))
+    L.mph_aggregate_max_backward(g.h, tdy.data_ptr(), w_, w_, targ.data_ptr(), w_,
                                  dH.data_ptr(), w_, C.byref(e), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     exp = oracle.aggregate_max_backward(dY, arg, n)
@@ -125,7 +128,8 @@ def test_optimizers_match_oracle(P, kind, kw):
     s = torch.cuda.current_stream().cuda_stream
     for t in range(1, 6):
         gr = rng.standard_normal(n).astype(np.float32)
-        L.mph_optim_step(p.data_ptr(), cuda(gr).data_ptr(), m.data_ptr(), v.data_ptr(), n, C.byref(cfg), t, s)
+        tg = cuda(gr)
+        L.mph_optim_step(p.data_ptr(), tg.data_ptr(), m.data_ptr(), v.data_ptr(), n, C.byref(cfg), t, s)
         if kind == "sgd":
             oracle.sgd_step(rp, [gr.astype(np.float64)], rm, lr=0.01, **kw)
         else:

@@ -290,7 +290,8 @@ def test_adam_matches_oracle(P):
     for t in range(1, 6):
         g = rng.standard_normal(n).astype(np.float32)
         g[:10] = 0.0
-        mph_adam(p.data_ptr(), cuda(g).data_ptr(), m.data_ptr(), v.data_ptr(), n, C.byref(cfg), t, s)
+        tg = cuda(g)   # referenced until the launch is enqueued (no caching-allocator reuse)
+        mph_adam(p.data_ptr(), tg.data_ptr(), m.data_ptr(), v.data_ptr(), n, C.byref(cfg), t, s)
         oracle.adam_step(rp, [g.astype(np.float64)], rm, rv, t)
     torch.cuda.synchronize()
     got = p.cpu().numpy()
