@@ -369,7 +369,9 @@ def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: i
     for l in range(1, L + 1):
         W = np.asarray(Ws[l - 1], dtype=np.float64)
         if aggregator == "max":
-            Y, arg = aggregate_max(g, H.toarray() if sp.issparse(H) else H)   # F2 before F1 (R7)
+            # F2 before F1 (R7).  With operand_rounding the max is taken on the operand as the
+            # kernel stores it (TF32): an argmax is decided in the kernel's precision
+            Y, arg = aggregate_max(g, _operand(H.toarray() if sp.issparse(H) else H, r))
             ys.append(Y)
             args.append(arg)
             Z = _operand(Y, r) @ _operand(W, r) + np.asarray(bs[l - 1], dtype=np.float64)
