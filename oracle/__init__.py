@@ -31,6 +31,10 @@ Parity status of each function (pins live in tests/test_oracle_*.py):
                                   central differences, routed-mass conservation)
   forward/backward (sum/mean/max) pinned (central finite differences of the whole loss)
   sgd_step / adamw_step ......... pinned (closed forms; torch.optim.SGD / AdamW traces)
+  partition_greedy / _components / relabel / partition_stats ... pinned (hand-worked star and
+                                  component cases, scipy connected components, the greedy's
+                                  list-scheduling bound, brute-force recounts, permutation
+                                  invariance of training under relabelling)
   absolute model quality vs the paper ... parity unpinned (the paper prints no loss
                                            or accuracy value)
 """

@@ -21,6 +21,8 @@ __all__ = [
     "splitmix64_stream", "xavier_init", "philox4x32_10", "dropout_keep",
     "dropout_threshold", "tf32_rna", "forward", "softmax_ce", "backward", "adam_step", "train",
     "AGGREGATORS", "aggregate_scheme", "aggregate_max", "aggregate_max_backward",
+    "connected_components", "partition_components", "partition_greedy", "partition_hierarchical", "relabel",
+    "partition_stats",
     "OPTIMIZERS", "sgd_step", "adamw_step",
     "partition_1d", "localize", "LocalPlan", "GOLDEN",
 ]
@@ -518,6 +520,105 @@ def partition_1d(row_ptr, world: int) -> np.ndarray:
             u += 1
         bounds[r] = u
     return bounds
+
+
+# ---------------------------------------------------------------------------
+# Alg. 4: Phase II component bin packing and Phase III
+# load-aware greedy, then a relabelling that makes every rank's nodes a contiguous id range
+# so the 1D machinery above (bounds, G2L, halo lists) applies unchanged.  Phase I (METIS) is
+# out of scope.  Reading R9: ties in every sort / argmin go to the smaller node id / lower rank.
+# ---------------------------------------------------------------------------
+def connected_components(g: Graph):
+    """Component id per node by BFS over A ("detects ... connected components via BFS"),
+    ids numbered in order of each component's smallest node."""
+    n = g.num_nodes
+    comp = np.full(n, -1, dtype=np.int64)
+    c = 0
+    for s in range(n):
+        if comp[s] >= 0:
+            continue
+        comp[s] = c
+        queue = [s]
+        while queue:
+            u = queue.pop()
+            for v in g.col_idx[g.row_ptr[u]:g.row_ptr[u + 1]]:
+                if comp[v] < 0:
+                    comp[v] = c
+                    queue.append(int(v))
+        c += 1
+    return comp, c
+
+
+def partition_components(g: Graph, world: int):
+    """Phase II (Alg. 4 lines "Sort Comps by size descending ... p = argmin(Weights) ...
+    Weights[p] += |C|").  Returns (part, n_components); part is None for a connected graph (the
+    algorithm falls through to Phase III)."""
+    comp, nc = connected_components(g)
+    if nc <= 1:
+        return None, nc
+    sizes = np.bincount(comp, minlength=nc)
+    order = sorted(range(nc), key=lambda c: (-int(sizes[c]), c))     # size desc, then first node
+    weights = [0] * world
+    part = np.empty(g.num_nodes, dtype=np.int32)
+    for c in order:
+        p = min(range(world), key=lambda q: (weights[q], q))
+        part[comp == c] = p
+        weights[p] += int(sizes[c])
+    return part, nc
+
+
+def partition_greedy(g: Graph, world: int) -> np.ndarray:
+    """Phase III (Alg. 4: "Sort V by Degree descending ... p = argmin(Weights); Weights[p] +=
+    deg(v) + 1"); deg(v) = |N(v)| in A, so deg(v) + 1 = d̃_v."""
+    d = g.deg.astype(np.int64) - 1
+    order = sorted(range(g.num_nodes), key=lambda v: (-int(d[v]), v))
+    weights = [0] * world
+    part = np.empty(g.num_nodes, dtype=np.int32)
+    for v in order:
+        p = min(range(world), key=lambda q: (weights[q], q))
+        part[v] = p
+        weights[p] += int(d[v]) + 1
+    return part
+
+
+def partition_hierarchical(g: Graph, world: int):
+    """Alg. 4 without Phase I: Phase II when the graph is disconnected, else Phase III.
+    Returns (part, phase)."""
+    part, nc = partition_components(g, world)
+    if part is not None:
+        return part, 2
+    return partition_greedy(g, world), 3
+
+
+def relabel(part, world: int):
+    """New ids: rank 0's nodes first, then rank 1's, ..., each rank's in ascending old id.
+    Returns (new_id[old], bounds[world+1]) so rank r owns new ids [bounds[r], bounds[r+1])."""
+    part = np.asarray(part, dtype=np.int64)
+    n = part.size
+    order = np.lexsort((np.arange(n), part))
+    new_id = np.empty(n, dtype=np.int64)
+    new_id[order] = np.arange(n)
+    bounds = np.zeros(world + 1, dtype=np.int64)
+    np.cumsum(np.bincount(part, minlength=world), out=bounds[1:])
+    return new_id, bounds
+
+
+def partition_stats(g: Graph, part, world: int) -> np.ndarray:
+    """Per rank [owned nodes, Σ d̃ (the SpMM work, T_comp ∝ Σ deg·F), distinct ghost
+    nodes (halo rows received per exchange), cut entries (nonzeros of A whose column
+    lives on another rank)]."""
+    part = np.asarray(part, dtype=np.int64)
+    rows = g.rows
+    cols = g.col_idx.astype(np.int64)
+    out = np.zeros((world, 4), dtype=np.int64)
+    for r in range(world):
+        mine = part == r
+        out[r, 0] = int(mine.sum())
+        out[r, 1] = int(g.deg[mine].astype(np.int64).sum())
+        sel = mine[rows] & (part[cols] != r)
+        out[r, 2] = int(np.unique(cols[sel]).size)
+        out[r, 3] = int(sel.sum())
+    return out
 
 
 @dataclasses.dataclass
