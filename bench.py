@@ -165,7 +165,31 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------------- our arm
-def _build_model(P, torch, w, world, rank, comm):
+def _relabel_workload(P, torch, w, world, how):
+    """Alg. 4 partition (NEXT-3) + relabelling: returns the workload in new ids and the contiguous
+    bounds that realise the partition.  Host work, outside the timed region."""
+    n = w["cfg"].num_nodes
+    g = P.Graph(w["src"], w["dst"], n)
+    rp, ci = (t.cpu().numpy() for t in g.csr()[:2])
+    del g
+    part = P.partition_greedy(rp, world)[0] if how == "greedy" else P.partition_hierarchical(rp, ci, world)[0]
+    new_id, bounds = P.relabel(part, world)
+    inv = np.empty(n, dtype=np.int64)
+    inv[new_id] = np.arange(n)
+    out = dict(w, src=new_id[w["src"]].astype(np.int32), dst=new_id[w["dst"]].astype(np.int32), y=w["y"][inv])
+    if w["X"] is not None:
+        out["X"] = np.ascontiguousarray(w["X"][inv])
+    else:
+        ptr, idx, val = w["X_csr"]
+        lens = np.diff(ptr)[inv]
+        nptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lens, out=nptr[1:])
+        take = np.concatenate([np.arange(ptr[v], ptr[v + 1]) for v in inv]) if n else np.zeros(0, np.int64)
+        out["X_csr"] = (nptr, idx[take], val[take])
+    return out, bounds
+
+
+def _build_model(P, torch, w, world, rank, comm, bounds=None):
     cfg = w["cfg"]
     n = cfg.num_nodes
     X = w["X"]
@@ -188,7 +212,8 @@ def _build_model(P, torch, w, world, rank, comm):
         gfull = P.Graph(w["src"], w["dst"], n)
         rp, ci = gfull.csr()[0].cpu().numpy(), gfull.csr()[1].cpu().numpy()
         del gfull
-        bounds = P.partition_1d(rp, world)
+        if bounds is None:
+            bounds = P.partition_1d(rp, world)
         plan = P.Plan(rp, ci, n, bounds, rank)
         del rp, ci
         g = P.Graph.from_plan(plan)
@@ -210,7 +235,10 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     w = make_workload(config)
     t_gen = time.perf_counter() - t_setup
     t0 = time.perf_counter()
-    g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm)
+    bounds = None
+    if world > 1 and args.partition != "1d":
+        w, bounds = _relabel_workload(P, torch, w, world, args.partition)
+    g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm, bounds)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     cfg = w["cfg"]
@@ -336,7 +364,9 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         "value": ms, "ms_per_step": ms,
         "config": {"workload": config, "nodes": cfg.num_nodes, "nnz_A": cfg.nnz_a, "dims": list(cfg.dims),
                    "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
-                   "parallelism": f"1d-row-partition x{world}" if world > 1 else "single-gpu",
+                   "parallelism": (f"1d-row-partition x{world}" + ("" if args.partition == "1d" else
+                                                                    f" ({args.partition} + relabel)"))
+                   if world > 1 else "single-gpu",
                    "layer_order": ["AF" if o else "TF" for o in m.order],
                    "cuda_graph": use_graph,
                    "l2": "inputs larger than L2 (X and col_idx > 126 MB); no flush" if cfg.num_nodes > 100000
@@ -437,6 +467,8 @@ def main():
     ap.add_argument("--config", default="reddit", choices=["cora", "pubmed", "arxiv", "reddit", "products", "nell"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partition", default="1d", choices=["1d", "greedy", "hierarchical"],
+                    help="N > 1: contiguous 1D (north star) or Alg. 4 Phase III / II-III + relabelling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the gather-bandwidth probe")
     ap.add_argument("--graph", action="store_true",

@@ -283,6 +283,32 @@ int mph_probe_gather(const float* table_d, int64_t n_rows, int32_t w, const int3
  * (Alg. 4 Phase III weight; reading Q20).  Host only. */
 int mph_partition_1d(const int64_t* row_ptr_h, int32_t N, int32_t world, int64_t* bounds_h);
 
+/* Alg. 4 partitioners.  Host only; row_ptr_h / col_idx_h are the
+ * GLOBAL Ã CSR (diagonal included, so a row's length is d̃_v = deg(v) + 1).  Reading R9: ties go
+ * to the smaller node id / lower rank (bit-exact with the oracle).  Phase I (METIS) is out of
+ * scope.
+ *   mph_partition_greedy      Phase III: nodes by deg descending, each to the rank of least
+ *                             weight, weight += deg(v) + 1.  load_h[world] nullable.
+ *   mph_partition_components  Phase II: connected components by BFS, sorted by size descending,
+ *                             each to the lightest rank, weight += |C|.  *n_comp_h =
+ *                             component count; part_h is written only when it is > 1.
+ *   mph_partition_hierarchical  Phase II when disconnected, else Phase III; *phase_h = 2 or 3.
+ *   mph_relabel               new_id_h[v]: rank 0's nodes first, then rank 1's, ..., ascending old
+ *                             id within a rank; bounds_h[world+1] so the relabelled graph's
+ *                             contiguous ranges are exactly the partition (feed bounds_h to
+ *                             mph_plan_create).  MPH_EINVAL if part_h[v] is outside [0, world).
+ *   mph_partition_stats       stats_h[4*world]: per rank {owned nodes, Σ d̃ (SpMM work,
+ *                             P:550-555), distinct ghost nodes (halo rows), cut
+ *                             entries of A}. */
+int mph_partition_greedy(const int64_t* row_ptr_h, int32_t N, int32_t world, int32_t* part_h, int64_t* load_h);
+int mph_partition_components(const int64_t* row_ptr_h, const int32_t* col_idx_h, int32_t N, int32_t world,
+                             int32_t* part_h, int32_t* n_comp_h);
+int mph_partition_hierarchical(const int64_t* row_ptr_h, const int32_t* col_idx_h, int32_t N, int32_t world,
+                               int32_t* part_h, int32_t* phase_h);
+int mph_relabel(const int32_t* part_h, int32_t N, int32_t world, int64_t* new_id_h, int64_t* bounds_h);
+int mph_partition_stats(const int64_t* row_ptr_h, const int32_t* col_idx_h, int32_t N, const int32_t* part_h,
+                        int32_t world, int64_t* stats_h);
+
 /* D2-D4: G2L local-then-ghost layout and halo lists.  Host only.
  * ghosts ascending by global id; local row = [owned cols | ghost cols], split[i] = #owned;
  * recv slice of peer q = ghost rows [recv_offset[q], recv_offset[q]+n_recv[q]);

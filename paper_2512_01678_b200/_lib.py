@@ -92,6 +92,11 @@ _SIGS = {
     "mph_optim_step": [P, P, P, P, i64, C.POINTER(OptimCfg), i32, P],
     "mph_xavier_fill": [P, i32, i32, i32, u64, i32, P],
     "mph_partition_1d": [P, i32, i32, P],
+    "mph_partition_greedy": [P, i32, i32, P, P],
+    "mph_partition_components": [P, P, i32, i32, P, C.POINTER(i32)],
+    "mph_partition_hierarchical": [P, P, i32, i32, P, C.POINTER(i32)],
+    "mph_relabel": [P, i32, i32, P, P],
+    "mph_partition_stats": [P, P, i32, P, i32, P],
     "mph_plan_create": [P, P, i32, P, i32, i32, PP],
     "mph_plan_info": [P, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)],
     "mph_plan_arrays": [P, PP, PP, PP, PP, PP, PP, PP, PP, PP],

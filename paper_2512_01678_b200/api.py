@@ -163,6 +163,57 @@ class Features:
             self.h = None
 
 
+def partition_greedy(row_ptr: np.ndarray, world: int):
+    """Alg. 4 Phase III (mph_partition_greedy): (part int32[N], load int64[world])."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    n = rp.size - 1
+    part = np.empty(n, dtype=np.int32)
+    load = np.empty(world, dtype=np.int64)
+    L.mph_partition_greedy(rp.ctypes.data, n, world, part.ctypes.data, load.ctypes.data)
+    return part, load
+
+
+def partition_components(row_ptr: np.ndarray, col_idx: np.ndarray, world: int):
+    """Alg. 4 Phase II (mph_partition_components): (part or None when connected, n_components)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    n = rp.size - 1
+    part = np.empty(n, dtype=np.int32)
+    nc = C.c_int32()
+    L.mph_partition_components(rp.ctypes.data, ci.ctypes.data, n, world, part.ctypes.data, C.byref(nc))
+    return (part if nc.value > 1 else None), nc.value
+
+
+def partition_hierarchical(row_ptr: np.ndarray, col_idx: np.ndarray, world: int):
+    """Alg. 4 Phases II-III (mph_partition_hierarchical): (part, phase)."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    n = rp.size - 1
+    part = np.empty(n, dtype=np.int32)
+    ph = C.c_int32()
+    L.mph_partition_hierarchical(rp.ctypes.data, ci.ctypes.data, n, world, part.ctypes.data, C.byref(ph))
+    return part, ph.value
+
+
+def relabel(part: np.ndarray, world: int):
+    """mph_relabel: (new_id int64[N], bounds int64[world+1])."""
+    pa = np.ascontiguousarray(part, dtype=np.int32)
+    new_id = np.empty(pa.size, dtype=np.int64)
+    bounds = np.empty(world + 1, dtype=np.int64)
+    L.mph_relabel(pa.ctypes.data, pa.size, world, new_id.ctypes.data, bounds.ctypes.data)
+    return new_id, bounds
+
+
+def partition_stats(row_ptr: np.ndarray, col_idx: np.ndarray, part: np.ndarray, world: int) -> np.ndarray:
+    """mph_partition_stats: int64[world, 4] = {owned, Σ d̃, distinct ghosts, cut entries}."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    pa = np.ascontiguousarray(part, dtype=np.int32)
+    out = np.empty((world, 4), dtype=np.int64)
+    L.mph_partition_stats(rp.ctypes.data, ci.ctypes.data, rp.size - 1, pa.ctypes.data, world, out.ctypes.data)
+    return out
+
+
 class Plan:
     """D1-D4 host plan of one rank (mph_plan_create)."""
 

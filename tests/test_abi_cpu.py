@@ -106,3 +106,33 @@ def test_plan_rejects_bad_arguments():
         Plan(g.row_ptr, g.col_idx, 3, np.array([0, 2, 3]), 5)
     with pytest.raises(MorphlingError):
         Plan(g.row_ptr, g.col_idx, 3, np.array([0, 3, 2]), 0)
+
+
+# ---------------------------------------------------------------- Alg. 4 partitioners (NEXT-3)
+@pytest.mark.parametrize("seed,n,m", [(0, 300, 2500), (1, 1200, 9000), (2, 500, 350)])
+def test_alg4_partitioners_match_oracle_bit_exact(seed, n, m):
+    import paper_2512_01678_b200 as P
+    w = make_small(n, m, 4, 3, seed=seed, alpha=2.1)
+    g = oracle.graph_build(w["src"], w["dst"], n)
+    for world in (1, 2, 3, 4, 8):
+        part, load = P.partition_greedy(g.row_ptr, world)
+        ref = oracle.partition_greedy(g, world)
+        assert np.array_equal(part, ref)
+        assert np.array_equal(load, np.bincount(ref, weights=g.deg, minlength=world).astype(np.int64))
+        pc, nc = P.partition_components(g.row_ptr, g.col_idx, world)
+        rc, rnc = oracle.partition_components(g, world)
+        assert nc == rnc and ((pc is None and rc is None) or np.array_equal(pc, rc))
+        ph, phase = P.partition_hierarchical(g.row_ptr, g.col_idx, world)
+        rh, rphase = oracle.partition_hierarchical(g, world)
+        assert phase == rphase and np.array_equal(ph, rh)
+        new_id, bounds = P.relabel(ph, world)
+        rn, rb = oracle.relabel(rh, world)
+        assert np.array_equal(new_id, rn) and np.array_equal(bounds, rb)
+        assert np.array_equal(P.partition_stats(g.row_ptr, g.col_idx, ph, world), oracle.partition_stats(g, rh, world))
+
+
+def test_relabel_rejects_bad_parts():
+    import paper_2512_01678_b200 as P
+    with pytest.raises(_lib().MorphlingError) as e:
+        P.relabel(np.array([0, 1, 2], np.int32), 2)
+    assert e.value.name == "MPH_EINVAL"

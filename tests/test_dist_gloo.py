@@ -57,15 +57,25 @@ def _local_agg(a, n_own, buf):
     return out
 
 
-def _worker(rank, world, port, n, m, result_q):
+def _worker(rank, world, port, n, m, result_q, partition="1d"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2512_01678_b200 import Plan, partition_1d
+        from paper_2512_01678_b200 import Plan, partition_1d, partition_greedy, relabel
         w = make_small(n, m, 5, 3, seed=17, alpha=2.1, mu=0.3)
-        g = oracle.graph_build(w["src"], w["dst"], n)
-        bounds = partition_1d(g.row_ptr, world)
+        g0 = oracle.graph_build(w["src"], w["dst"], n)
+        X0, y0 = w["X"], w["y"]
+        if partition == "greedy":
+            # Alg. 4 Phase III, then relabel so each rank's nodes are one contiguous range (NEXT-3)
+            new_id, bounds = relabel(partition_greedy(g0.row_ptr, world)[0], world)
+            inv = np.empty(n, dtype=np.int64)
+            inv[new_id] = np.arange(n)
+            g = oracle.graph_build(new_id[w["src"]].astype(np.int32), new_id[w["dst"]].astype(np.int32), n)
+            w = dict(w, X=X0[inv], y=y0[inv])
+        else:
+            g = g0
+            bounds = partition_1d(g.row_ptr, world)
         plan = Plan(g.row_ptr, g.col_idx, n, bounds, rank)
         a = plan.arrays()
         n_own, row0 = plan.n_own, plan.row0
@@ -109,22 +119,22 @@ def _worker(rank, world, port, n, m, result_q):
                 dZ = (G @ Ws[1].T) * (Zs[0] > 0)
         flat = torch.from_numpy(np.concatenate([x.ravel() for x in grads] + [np.array([loss])]))
         dist.all_reduce(flat)                           # a11
-        if rank == 0:
-            Z, cache = oracle.forward(g, X, Ws, bs)
-            lref, dZr = oracle.softmax_ce(Z, w["y"])
-            dWs, dbs = oracle.backward(g, cache, Ws, dZr)
+        if rank == 0:   # the single-graph oracle on the ORIGINAL ids (relabelling must not matter)
+            Z, cache = oracle.forward(g0, X0.astype(np.float64), Ws, bs)
+            lref, dZr = oracle.softmax_ce(Z, y0)
+            dWs, dbs = oracle.backward(g0, cache, Ws, dZr)
             ref = np.concatenate([dWs[0].ravel(), dbs[0], dWs[1].ravel(), dbs[1], [lref]])
             result_q.put(float(np.max(np.abs(flat.numpy() - ref) / (np.abs(ref) + 1e-12))))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_epoch_over_gloo(world):
+@pytest.mark.parametrize("world,partition", [(2, "1d"), (3, "1d"), (2, "greedy"), (3, "greedy")])
+def test_distributed_epoch_over_gloo(world, partition):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, 240, 1800, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, 240, 1800, q, partition)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
