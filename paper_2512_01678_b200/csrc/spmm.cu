@@ -343,11 +343,14 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.epi.row0 = epi ? epi->row0 : 0;
   if (a.epi.drop.threshold == 0) a.epi.flags &= ~MPH_EPI_DROPOUT;
   a.epi.c4_0 = 0;
-  // Column slabs: rows of w >= 128 are aggregated as two halves, one launch each, so the slab of
-  // the gathered operand that a community of rows touches is half as large and stays in L2
-  // (measured: products w = 256 -4 %, reddit w = 128 -2 %).  MPH_SPMM_SLAB overrides (-1: off).
+  // Column slabs: on graphs with a mean degree >= 16, rows of w = 128 / 256 are aggregated as two
+  // halves, one launch each, so the slab of the gathered operand that a community of rows
+  // touches is half as large and stays in L2 (measured: products -1..4 %, reddit -2 %); on
+  // sparse graphs the doubled per-row overhead costs more (arxiv, mean degree 7: +13 %).
+  // MPH_SPMM_SLAB overrides (-1: off).
   static const int slab_env = env_int("MPH_SPMM_SLAB");
-  const int slab = slab_env != 0 ? slab_env : ((w == 128 || w == 256) ? w / 2 : 0);
+  const bool deep = g->nnz >= 16 * (int64_t)g->n_rows;
+  const int slab = slab_env != 0 ? slab_env : ((deep && (w == 128 || w == 256)) ? w / 2 : 0);
   if (slab > 0 && part == -1 && w > slab && slab % 4 == 0) {
     for (int c0 = 0; c0 < w; c0 += slab) {
       SpmmArgs b = a;
