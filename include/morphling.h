@@ -374,6 +374,11 @@ int mph_gcn_params_updated(mph_gcn* m, void* stream);
  * copies): X_h [n_rows][ld_h], F columns.  Re-derives everything the model derives from X
  * (the dinv pre-scale of an aggregate-first layer 1 and its ghost rows).  Dense mode only. */
 int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_h, void* stream);
+/* Pipelined variant (a data loader's prefetch): the H2D copy runs on copy_stream once the
+ * previous upload has been consumed, and the derivation (TF32 copy / pre-scale / MAX of X) is
+ * enqueued on `stream` behind it.  The epoch reads only the derived buffers, so the copy of the
+ * next step's X overlaps the current epoch.  X_h must stay valid (pinned) until the copy is done. */
+int mph_gcn_upload_features_async(mph_gcn* m, const float* X_h, int32_t ld_h, void* copy_stream, void* stream);
 /* Labels (int32, owned rows), optional uint8 mask, and the GLOBAL labelled count. */
 int mph_gcn_set_labels(mph_gcn* m, const int32_t* labels_d, const uint8_t* mask_d, int64_t n_lab_global);
 int mph_gcn_forward(mph_gcn* m, int32_t epoch, void* stream);

@@ -114,6 +114,7 @@ _SIGS = {
     "mph_gcn_init_xavier": [P, u64, P],
     "mph_gcn_params_updated": [P, P],
     "mph_gcn_upload_features": [P, P, i32, P],
+    "mph_gcn_upload_features_async": [P, P, i32, P, P],
     "mph_gcn_set_labels": [P, P, P, i64],
     "mph_profile_enable": [i32],
     "mph_probe_gather": [P, i64, i32, P, i64, P, P],

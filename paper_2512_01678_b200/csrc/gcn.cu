@@ -67,6 +67,7 @@ struct mph_gcn {
   // P > 1: NCCL runs on its own stream, ordered against the compute stream by events
   cudaStream_t cs = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_grad = nullptr, ev_comm_done = nullptr, ev_loss = nullptr;
+  cudaEvent_t ev_copied = nullptr, ev_derived = nullptr;  // mph_gcn_upload_features_async pipeline
   // CUDA-graph replay of one epoch: step counter and loss live in device memory
   int32_t* t_dev = nullptr;
   double* loss_dev = nullptr;
@@ -102,7 +103,7 @@ static void gcn_free(mph_gcn* m) {
   dev_free(m->Xr);
   dev_free(m->Xs);
   dev_free(m->ws);
-  for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss})
+  for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss, m->ev_copied, m->ev_derived})
     if (e) cudaEventDestroy(e);
   if (m->cs) cudaStreamDestroy(m->cs);
   if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
@@ -527,16 +528,19 @@ extern "C" int mph_gcn_params_updated(mph_gcn* m, void* stream) {
   return refresh_wt(m, (cudaStream_t)stream);
 }
 
-extern "C" int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_h, void* stream) {
-  if (!m || !X_h || ld_h < m->f->F) return fail(MPH_EINVAL, "upload_features arguments");
-  if (m->f->mode != 0) return fail(MPH_ENOTSUP, "upload_features: sparse-mode features are fixed at creation");
-  cudaStream_t s = (cudaStream_t)stream;
-  const mph_features* f = m->f;
+static int copy_features(const mph_features* f, const float* X_h, int32_t ld_h, cudaStream_t s) {
   if (ld_h == f->P)  // host rows already padded: one contiguous copy (the padding must be zero)
     MPH_CUDA_TRY(cudaMemcpyAsync(f->X, X_h, (size_t)f->N * f->P * 4, cudaMemcpyHostToDevice, s));
   else
     MPH_CUDA_TRY(cudaMemcpy2DAsync(f->X, (size_t)f->P * 4, X_h, (size_t)ld_h * 4, (size_t)f->F * 4, (size_t)f->N,
                                    cudaMemcpyHostToDevice, s));
+  return MPH_OK;
+}
+
+// Everything the epoch reads is derived from X here (TF32 copy Xr, pre-scaled Xs, or MAX(X)); the
+// epoch itself never reads f->X, so the next step's X may land in f->X while an epoch runs.
+static int derive_from_features(mph_gcn* m, cudaStream_t s) {
+  const mph_features* f = m->f;
   if (m->agg == MPH_AGG_MAX) {
     const Layer& l = m->layers[0];
     mph_epilogue en = epi_none();
@@ -549,6 +553,33 @@ extern "C" int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_
   } else {
     MPH_TRY(rowscale_launch(f->X, f->P, nullptr, m->g->n_rows, f->P, m->Xr, f->P, 1, s));
   }
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_upload_features(mph_gcn* m, const float* X_h, int32_t ld_h, void* stream) {
+  if (!m || !X_h || ld_h < m->f->F) return fail(MPH_EINVAL, "upload_features arguments");
+  if (m->f->mode != 0) return fail(MPH_ENOTSUP, "upload_features: sparse-mode features are fixed at creation");
+  cudaStream_t s = (cudaStream_t)stream;
+  MPH_TRY(copy_features(m->f, X_h, ld_h, s));
+  return derive_from_features(m, s);
+}
+
+extern "C" int mph_gcn_upload_features_async(mph_gcn* m, const float* X_h, int32_t ld_h, void* copy_stream,
+                                             void* stream) {
+  if (!m || !X_h || ld_h < m->f->F) return fail(MPH_EINVAL, "upload_features arguments");
+  if (m->f->mode != 0) return fail(MPH_ENOTSUP, "upload_features: sparse-mode features are fixed at creation");
+  cudaStream_t cs = (cudaStream_t)copy_stream, s = (cudaStream_t)stream;
+  if (!m->ev_copied) {
+    MPH_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_copied, cudaEventDisableTiming));
+    MPH_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_derived, cudaEventDisableTiming));
+    MPH_CUDA_TRY(cudaEventRecord(m->ev_derived, s));
+  }
+  MPH_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev_derived, 0));  // the previous upload has been consumed
+  MPH_TRY(copy_features(m->f, X_h, ld_h, cs));
+  MPH_CUDA_TRY(cudaEventRecord(m->ev_copied, cs));
+  MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_copied, 0));
+  MPH_TRY(derive_from_features(m, s));
+  MPH_CUDA_TRY(cudaEventRecord(m->ev_derived, s));
   return MPH_OK;
 }
 

@@ -212,3 +212,42 @@ def test_cuda_graph_replay_bitwise_equals_eager(P, dropout_p):
     assert replayed == eager
     assert torch.equal(ma.params_flat, mb.params_flat)
     assert mb.graph_step.item() == 6
+
+
+@pytest.mark.parametrize("dims,agg", [((24, 32, 5), "gcn"), ((24, 16, 5), "gcn"), ((24, 16, 5), "max")])
+def test_async_feature_upload_matches_sync(P, dims, agg):
+    """mph_gcn_upload_features_async (copy stream, prefetch of the next step's X while an epoch
+    runs) gives bitwise the same training as the synchronous upload, for an aggregate-first layer 1
+    (pre-scaled copy), a transform-first one (TF32 copy) and max aggregation (MAX(X))."""
+    from paper_2512_01678_b200 import _lib as L
+    w = make_small(3000, 20000, 24, 5, seed=12)
+    Pw = P.pad_width(24)
+    hosts = []
+    for t in range(5):   # a different X every step (exact dyadic scaling), pinned, padded
+        h = torch.zeros((3000, Pw), dtype=torch.float32).pin_memory()
+        h[:, :24] = torch.from_numpy(w["X"] * np.float32(1 + t / 8))
+        hosts.append(h)
+    s = torch.cuda.current_stream()
+    runs = []
+    for mode in ("sync", "async"):
+        g = P.Graph(w["src"], w["dst"], 3000)
+        f = P.Features(cuda(w["X"]), force_mode=0)
+        m = P.GCN(g, f, dims, aggregator=agg)
+        m.init_xavier(42)
+        m.set_labels(cuda(w["y"].astype(np.int32)))
+        cs = torch.cuda.Stream()
+        losses = []
+        if mode == "async":
+            L.mph_gcn_upload_features_async(m.h, hosts[0].data_ptr(), Pw, cs.cuda_stream, s.cuda_stream)
+        for t in range(5):
+            if mode == "sync":
+                L.mph_gcn_upload_features(m.h, hosts[t].data_ptr(), Pw, s.cuda_stream)
+            out = torch.zeros(1, dtype=torch.float64, device="cuda")
+            m.train_epoch(t + 1, out=out)
+            if mode == "async" and t + 1 < 5:
+                L.mph_gcn_upload_features_async(m.h, hosts[t + 1].data_ptr(), Pw, cs.cuda_stream, s.cuda_stream)
+            losses.append(out)
+        torch.cuda.synchronize()
+        runs.append(([x.item() for x in losses], m.params_flat.clone()))
+    assert runs[0][0] == runs[1][0]
+    assert torch.equal(runs[0][1], runs[1][1])
