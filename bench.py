@@ -316,17 +316,25 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                 L.mph_gcn_upload_features_async(m.h, Xh.data_ptr(), Pw, copy_stream.cuda_stream, stream.cuda_stream)
             y.copy_(yh, non_blocking=True)
 
+        d2h_stream = torch.cuda.Stream()
         e0.record(stream)
         base = args.warmup + args.steps
         load_inputs()
         for i, t in enumerate(range(base + 1, base + steps_e2e + 1)):
             m.train_epoch(t)
-            lh.copy_(m.loss_buf, non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(stream)
+            epoch_done = torch.cuda.Event()
+            epoch_done.record(stream)
             if i + 1 < steps_e2e:
                 load_inputs()    # prefetch: the next step's copy overlaps this epoch
+            # the loss read-back is issued after the prefetch (the copy engines serve submissions in
+            # order, so a D2H queued behind a running epoch would hold the next H2D back)
+            d2h_stream.wait_event(epoch_done)
+            with torch.cuda.stream(d2h_stream):
+                lh.copy_(m.loss_buf, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(d2h_stream)
             done.synchronize()   # the step's result is on the host
+        stream.wait_stream(d2h_stream)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / steps_e2e
