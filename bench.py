@@ -310,22 +310,27 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         copy_stream = torch.cuda.Stream()
+        y_bufs = [y, torch.empty_like(y)]   # double-buffered labels: step i+1's land while step i reads
 
-        def load_inputs():   # this step's inputs from pinned host memory (H2D on the copy stream)
-            if upload:
+        def load_inputs(i):   # step i's inputs from pinned host memory, all H2D on the copy stream
+            with torch.cuda.stream(copy_stream):
+                y_bufs[i % 2].copy_(yh, non_blocking=True)   # epoch i-2, its last reader, has finished
+            if upload:   # waits for the previous X to be consumed, copies, then the compute stream waits
                 L.mph_gcn_upload_features_async(m.h, Xh.data_ptr(), Pw, copy_stream.cuda_stream, stream.cuda_stream)
-            y.copy_(yh, non_blocking=True)
+            else:
+                stream.wait_stream(copy_stream)
 
         d2h_stream = torch.cuda.Stream()
         e0.record(stream)
         base = args.warmup + args.steps
-        load_inputs()
+        load_inputs(0)
         for i, t in enumerate(range(base + 1, base + steps_e2e + 1)):
+            m.set_labels(y_bufs[i % 2], n_lab_global=cfg.num_nodes)
             m.train_epoch(t)
             epoch_done = torch.cuda.Event()
             epoch_done.record(stream)
             if i + 1 < steps_e2e:
-                load_inputs()    # prefetch: the next step's copy overlaps this epoch
+                load_inputs(i + 1)    # prefetch: the next step's copies overlap this epoch
             # the loss read-back is issued after the prefetch (the copy engines serve submissions in
             # order, so a D2H queued behind a running epoch would hold the next H2D back)
             d2h_stream.wait_event(epoch_done)
@@ -336,6 +341,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
             done.synchronize()   # the step's result is on the host
         stream.wait_stream(d2h_stream)
         e1.record(stream)
+        m.set_labels(y, n_lab_global=cfg.num_nodes)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / steps_e2e
         if world > 1:

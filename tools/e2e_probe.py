@@ -74,6 +74,44 @@ def main():
     for i in range(K):
         print(f"step {i}: copy {base.elapsed_time(cps[i][0]):8.2f} -> {base.elapsed_time(cps[i][1]):8.2f}   "
               f"epoch {base.elapsed_time(eps[i][0]):8.2f} -> {base.elapsed_time(eps[i][1]):8.2f}")
+    # variants of the bench loop
+    yh = torch.from_numpy(np.ascontiguousarray(w["y"])).pin_memory()
+    lh = torch.zeros(1, dtype=torch.float64).pin_memory()
+    d2h = torch.cuda.Stream()
+    for variant in ("labels", "loss_same_stream", "loss_d2h_stream", "both"):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+
+        def load():
+            L.mph_gcn_upload_features_async(m.h, Xh.data_ptr(), Pw, cs.cuda_stream, s.cuda_stream)
+            if variant in ("labels", "both"):
+                y.copy_(yh, non_blocking=True)
+
+        load()
+        for i in range(K):
+            m.train_epoch(20 + i)
+            ed = torch.cuda.Event()
+            ed.record(s)
+            if i + 1 < K:
+                load()
+            if variant == "loss_same_stream":
+                lh.copy_(m.loss_buf, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(s)
+            elif variant in ("loss_d2h_stream", "both"):
+                d2h.wait_event(ed)
+                with torch.cuda.stream(d2h):
+                    lh.copy_(m.loss_buf, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(d2h)
+            else:
+                done = ed
+            done.synchronize()
+        s.wait_stream(d2h)
+        e1.record(s)
+        torch.cuda.synchronize()
+        print(variant, "ms/step", e0.elapsed_time(e1) / K)
 
 
 if __name__ == "__main__":
