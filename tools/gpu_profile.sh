@@ -6,8 +6,14 @@ NCU=/usr/local/cuda/bin/ncu
 TAG=${1:-r01}
 timeout 1200 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_bench.csv \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --secondary none --no-probe > gpurun_out/${TAG}_launches_bench.out 2>&1; echo "launch list rc=$?"
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_spmm -s 4 -c 4 -o gpurun_out/${TAG}_spmm_reddit python tools/profile_step.py --config reddit --epochs 2 > /dev/null 2>&1; echo "spmm reddit rc=$?"
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_spmm -s 5 -c 5 -o gpurun_out/${TAG}_spmm_products python tools/profile_step.py --config products --epochs 2 > /dev/null 2>&1; echo "spmm products rc=$?"
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_gemm -s 8 -c 8 -o gpurun_out/${TAG}_gemm_products python tools/profile_step.py --config products --epochs 2 > /dev/null 2>&1; echo "gemm products rc=$?"
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_gemm -s 5 -c 5 -o gpurun_out/${TAG}_gemm_reddit python tools/profile_step.py --config reddit --epochs 2 > /dev/null 2>&1; echo "gemm reddit rc=$?"
+cap() {  # name regex skip count config [agg]
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$2 -s $3 -c $4 -o gpurun_out/${TAG}_$1 \
+    python tools/profile_step.py --config $5 --epochs 2 --agg ${6:-gcn} > /dev/null 2>&1; echo "$1 rc=$?"
+}
+cap spmm_reddit k_spmm 6 6 reddit
+cap spmm_products k_spmm 7 7 products
+cap gemm_products k_gemm 8 8 products
+cap gemm_reddit k_gemm 5 5 reddit
+cap sparse_nell "k_spmm|k_sparse" 12 12 nell
+cap aggmax_arxiv "k_aggmax|k_colsum" 4 8 arxiv max
 ls -la gpurun_out/${TAG}_*

@@ -13,12 +13,17 @@ from synth.generate import make_workload  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="reddit")
 ap.add_argument("--epochs", type=int, default=3)
+ap.add_argument("--agg", default="gcn", choices=["gcn", "sum", "mean", "max"])
 a = ap.parse_args()
 w = make_workload(a.config)
 cfg = w["cfg"]
 g = P.Graph(w["src"], w["dst"], cfg.num_nodes)
-f = P.Features(torch.from_numpy(w["X"]).cuda())
-m = P.GCN(g, f, cfg.dims)
+if w["X"] is not None:
+    f = P.Features(torch.from_numpy(w["X"]).cuda())
+else:
+    ptr, idx, val = w["X_csr"]
+    f = P.Features.from_csr(ptr, idx, val, (cfg.num_nodes, cfg.num_features))
+m = P.GCN(g, f, cfg.dims, aggregator=a.agg)
 m.init_xavier(42)
 m.set_labels(torch.from_numpy(w["y"]).cuda())
 torch.cuda.synchronize()
