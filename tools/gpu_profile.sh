@@ -14,6 +14,6 @@ cap spmm_reddit k_spmm 6 6 reddit
 cap spmm_products k_spmm 7 7 products
 cap gemm_products k_gemm 8 8 products
 cap gemm_reddit k_gemm 5 5 reddit
-cap sparse_nell "k_spmm|k_sparse" 12 12 nell
-cap aggmax_arxiv "k_aggmax|k_colsum" 4 8 arxiv max
+cap sparse_nell "k_spmm|k_sparse" 9 9 nell
+cap aggmax_arxiv "k_aggmax|k_colsum" 7 6 arxiv max
 ls -la gpurun_out/${TAG}_*
