@@ -16,4 +16,14 @@ cap gemm_products k_gemm 8 8 products
 cap gemm_reddit k_gemm 5 5 reddit
 cap sparse_nell "k_spmm|k_sparse" 9 9 nell
 cap aggmax_arxiv "k_aggmax|k_colsum" 7 6 arxiv max
+# summaries on the box (the reports are too large to bring back: gpurun_out <= 64 MiB)
+python tools/ncu_summary.py --launches gpurun_out/${TAG}_launches_bench.csv --out gpurun_out/${TAG}_launches_bench.md \
+  --title "Launch list of python bench.py --steps 3 --warmup 3 (ncu --metrics gpu__time_duration.sum, cold, serialised)" > /dev/null
+python tools/ncu_summary.py gpurun_out/${TAG}_*.ncu-rep --out gpurun_out/${TAG}_ncu_full.md --json gpurun_out/${TAG}_ncu_full.json \
+  --title "ncu --set full --clock-control none captures (${TAG})" > /dev/null
+for r in gpurun_out/${TAG}_*.ncu-rep; do
+  ncu -i $r --page details --csv > ${r%.ncu-rep}_details.csv 2>/dev/null
+  gzip -9 -f ${r%.ncu-rep}_details.csv
+done
+rm -f gpurun_out/${TAG}_*.ncu-rep
 ls -la gpurun_out/${TAG}_*
