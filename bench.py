@@ -254,7 +254,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     barrier()
 
     # ---------------- device-timed region: K epochs, inputs resident in HBM
-    use_graph = bool(args.graph) and world == 1
+    use_graph = bool(args.graph) and (world == 1 or args.comm == "p2p")
     if use_graph:  # one captured epoch, replayed K times (the per-kernel breakdown needs eager launches)
         m.graph_capture(args.warmup + 1)
     clocks = ClockSampler(local)
@@ -390,7 +390,8 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         "config": {"workload": config, "nodes": cfg.num_nodes, "nnz_A": cfg.nnz_a, "dims": list(cfg.dims),
                    "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
                    "parallelism": (f"1d-row-partition x{world}" + ("" if args.partition == "1d" else
-                                                                    f" ({args.partition} + relabel)"))
+                                                                    f" ({args.partition} + relabel)")
+                                   + f", comm {args.comm}")
                    if world > 1 else "single-gpu",
                    "layer_order": ["AF" if o else "TF" for o in m.order],
                    "cuda_graph": use_graph,
@@ -451,7 +452,8 @@ def run_ours(args):
     from paper_2512_01678_b200 import _lib as L
 
     L.mph_device_check(C.byref(C.c_int32()))
-    comm = P.Comm(world, rank) if world > 1 else None
+    # N > 1: NCCL halo/all-reduce, or NVLink peer memory (NEXT-1: the model maps its peers itself)
+    comm = (P.Comm(world, rank) if args.comm == "nccl" else "p2p") if world > 1 else None
     main = _measure(P, L, torch, dist, C, args, args.config, world, rank, local, comm, full=True)
     secondary = {}
     for cfgname in ([] if args.secondary == "none" else args.secondary.split(",")):
@@ -494,6 +496,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--partition", default="1d", choices=["1d", "greedy", "hierarchical"],
                     help="N > 1: contiguous 1D (north star) or Alg. 4 Phase III / II-III + relabelling")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: NCCL grouped send/recv + all-reduce, or NVLink peer-memory pulls with the "
+                         "gradient sum fused into the optimizer (SURVEY §8(f) NEXT-1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the gather-bandwidth probe")
     ap.add_argument("--graph", action="store_true",

@@ -55,6 +55,7 @@ extern "C" {
 #define MPH_ENCCL (-7)       /* NCCL error */
 #define MPH_EDIVERGED (-8)   /* replica parameter hashes differ across ranks */
 #define MPH_ENOTSUP (-9)     /* shape outside what the kernels implement (e.g. width > 512) */
+#define MPH_ETIMEOUT (-10)   /* a peer-memory wait saw no signal within 10 s (mph_gcn_p2p_status) */
 
 int mph_version(void);
 const char* mph_last_error(void);
@@ -356,10 +357,16 @@ typedef struct {
   int32_t aggregator;    /* MPH_AGG_GCN (default, the north star), _SUM, _MEAN (linear: the layer
                             order of Q7 applies) or _MAX (Z = MAX(H)·W + b on every layer, R7;
                             dense-mode features and a single GPU only, else MPH_ENOTSUP) */
+  int32_t comm_mode;     /* P > 1 only: MPH_COMM_NCCL (0, default: pack + grouped ncclSend/Recv,
+                            ncclAllReduce) or MPH_COMM_P2P (1: NVLink peer memory, see below) */
 } mph_gcn_desc;
 
-/* graph may be global (comm NULL) or localized (comm non-NULL, world > 1); features hold the
- * owned rows.  Allocates parameters, gradients, Adam state and activations. */
+#define MPH_COMM_NCCL 0
+#define MPH_COMM_P2P 1
+
+/* graph may be global (comm NULL) or localized (world > 1: comm non-NULL for MPH_COMM_NCCL,
+ * NULL for MPH_COMM_P2P); features hold the owned rows.  Allocates parameters, gradients, Adam
+ * state and activations. */
 int mph_gcn_create(const mph_graph* g, const mph_features* f, const mph_gcn_desc* desc, mph_comm* comm,
                    void* stream, mph_gcn** out);
 /* Flat parameter buffer: W_l at offsets[2(l-1)] as [F_{l-1}][ld_w[l-1]] row-major,
@@ -407,6 +414,36 @@ int mph_gcn_graph_state(const mph_gcn* m, int32_t** t_d, double** loss_d);
  * (n_cols rows incl. ghosts), 5 = dZ'_l (dinv-prescaled gradient, n_cols rows; AF layer 1: dZ_1). */
 int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, const float** ptr_d, int32_t* rows_h,
                    int32_t* width_h, int32_t* ld_h);
+/* ---- NEXT-1: NVLink peer-memory halo exchange and gradient sum (
+ * halo P:517-523, gradient sum P:525-532, overlap P:765).
+ * A model created with comm_mode = MPH_COMM_P2P on a localized graph keeps every buffer a peer
+ * reads — the dinv-prescaled T'_l and dZ'_l (owned + ghost rows), dinv ⊙ X of an
+ * aggregate-first layer 1, two parity-indexed gradient receive slabs [world][num_params], the
+ * loss slots and the step flags — in ONE cudaMalloc arena that the peers map (CUDA IPC over
+ * NVLink / NVSwitch).  Per SpMM, the owner signals "rows ready" with a system-scope release
+ * store into every peer's flag row and the consumer's pull kernel (acquire-spin, then 16-byte
+ * peer loads) copies each ghost row from its owner's buffer into the local ghost slice while
+ * the local-edge SpMM runs — no pack, no send buffer, no NCCL.  Each layer's [dW | db] is
+ * pushed into every peer's receive slab as soon as it is complete; the optimizer kernel waits
+ * for all ranks, sums the P slabs in rank order (deterministic, identical on every rank) and
+ * applies the update in the same pass (all-reduce fused into Adam/SGD/AdamW).  The loss is
+ * summed the same way.  CUDA-graph capture is allowed in this mode (no host-side collective).
+ *
+ *   mph_gcn_p2p_export(m, blob_h)  writes this rank's MPH_P2P_BLOB_BYTES descriptor (IPC handle,
+ *                                  buffer offsets, row0).  MPH_ESTATE unless comm_mode = P2P.
+ *   mph_gcn_p2p_open(m, blobs_h, world, stream)  blobs_h = all ranks' descriptors in rank order
+ *                                  (the caller all-gathers them, e.g. over torch.distributed).
+ *                                  Maps the peers' arenas, builds the ghost-source table and
+ *                                  exchanges the ghost rows of dinv ⊙ X.  Collective: every rank
+ *                                  calls it once, before its first epoch.  Synchronises.
+ *   mph_gcn_p2p_status(m, err_h)   *err_h = 0, or MPH_ETIMEOUT if a wait gave up (a peer stopped
+ *                                  signalling): that epoch's results are undefined.  Synchronises.
+ * Constraints: world <= 16; every rank runs the same sequence of epochs. */
+#define MPH_P2P_BLOB_BYTES 512
+int mph_gcn_p2p_export(const mph_gcn* m, uint8_t* blob_h);
+int mph_gcn_p2p_open(mph_gcn* m, const uint8_t* blobs_h, int32_t world, void* stream);
+int mph_gcn_p2p_status(const mph_gcn* m, int32_t* err_h);
+
 /* order_h[l-1] = 0 transform-first, 1 aggregate-first; mode_h = feature mode. */
 int mph_gcn_info(const mph_gcn* m, int32_t* order_h, int32_t* mode_h);
 int mph_gcn_destroy(mph_gcn* m);

@@ -15,7 +15,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libmorphling.so")
 
 STATUS = {0: "MPH_OK", -1: "MPH_EINVAL", -2: "MPH_ERANGE", -3: "MPH_EDEGENERATE", -4: "MPH_ESTATE",
-          -5: "MPH_ENOMEM", -6: "MPH_ECUDA", -7: "MPH_ENCCL", -8: "MPH_EDIVERGED", -9: "MPH_ENOTSUP"}
+          -5: "MPH_ENOMEM", -6: "MPH_ECUDA", -7: "MPH_ENCCL", -8: "MPH_EDIVERGED", -9: "MPH_ENOTSUP",
+          -10: "MPH_ETIMEOUT"}
 
 EPI_BIAS, EPI_RELU, EPI_ROWSCALE, EPI_MASK, EPI_DROPOUT, EPI_COLSUM, EPI_TF32 = 1, 2, 4, 8, 16, 32, 64
 AGG = {"gcn": 0, "sum": 1, "mean": 2, "max": 3}            # MPH_AGG_*
@@ -47,7 +48,8 @@ class OptimCfg(C.Structure):
 
 class GcnDesc(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("dims_h", C.POINTER(C.c_int32)), ("dropout_p", C.c_float),
-                ("dropout_seed", C.c_uint64), ("order_policy", C.c_int32), ("aggregator", C.c_int32)]
+                ("dropout_seed", C.c_uint64), ("order_policy", C.c_int32), ("aggregator", C.c_int32),
+                ("comm_mode", C.c_int32)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -132,8 +134,14 @@ _SIGS = {
     "mph_gcn_graph_state": [P, PP, PP],
     "mph_gcn_tensor": [P, i32, i32, PP, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
     "mph_gcn_info": [P, P, C.POINTER(i32)],
+    "mph_gcn_p2p_export": [P, P],
+    "mph_gcn_p2p_open": [P, P, i32, P],
+    "mph_gcn_p2p_status": [P, C.POINTER(i32)],
     "mph_gcn_destroy": [P],
 }
+
+COMM = {"nccl": 0, "p2p": 1}
+P2P_BLOB_BYTES = 512
 
 EXPORTED = ["mph_version", "mph_last_error"] + list(_SIGS)
 

@@ -301,17 +301,29 @@ class GCN:
     """The L-layer GCN training step (initializeLayers / forwardPass / backPropagation / optimizer)."""
 
     def __init__(self, graph: Graph, features: Features, dims, dropout_p: float = 0.0, dropout_seed: int = 0,
-                 order_policy: int = 0, comm: Comm | None = None, stream=None, aggregator: str = "gcn"):
-        self.graph, self.features, self.comm = graph, features, comm
+                 order_policy: int = 0, comm: "Comm | str | None" = None, stream=None, aggregator: str = "gcn",
+                 pg=None):
+        """comm: None (one GPU), a Comm (NCCL halo + all-reduce) or "p2p" (NVLink peer memory,
+        NEXT-1): the ranks' arena descriptors are all-gathered over the torch.distributed group
+        `pg` (plumbing only) and mapped by mph_gcn_p2p_open."""
+        self.graph, self.features = graph, features
+        p2p = isinstance(comm, str)
+        if p2p and comm != "p2p":
+            raise ValueError(f"comm must be a Comm, 'p2p' or None, not {comm!r}")
+        self.comm = None if p2p else comm
+        self.comm_mode = "p2p" if p2p else "nccl"
         self.dims = tuple(int(d) for d in dims)
         self.L = len(self.dims) - 1
         self.aggregator = aggregator
         arr = (C.c_int32 * len(self.dims))(*self.dims)
-        desc = GcnDesc(self.L, arr, float(dropout_p), int(dropout_seed), int(order_policy), L.AGG[aggregator])
+        desc = GcnDesc(self.L, arr, float(dropout_p), int(dropout_seed), int(order_policy), L.AGG[aggregator],
+                       L.COMM[self.comm_mode])
         h = _out_ptr()
-        L.mph_gcn_create(graph.h, features.h, C.byref(desc), comm.h if comm is not None else None,
+        L.mph_gcn_create(graph.h, features.h, C.byref(desc), self.comm.h if self.comm is not None else None,
                          stream_ptr(stream), C.byref(h))
         self.h = h
+        if p2p:
+            self._p2p_open(pg, stream)
         n = C.c_int64()
         offs = (C.c_int64 * (2 * self.L))()
         lds = (C.c_int32 * self.L)()
@@ -329,6 +341,25 @@ class GCN:
         self.order = list(order)
         self.loss_buf = torch.zeros(1, dtype=torch.float64, device="cuda")
         self._labels = None
+
+    def _p2p_open(self, pg, stream):
+        import torch.distributed as dist
+        blob = (C.c_uint8 * L.P2P_BLOB_BYTES)()
+        L.mph_gcn_p2p_export(self.h, C.cast(blob, C.c_void_p))
+        world = dist.get_world_size(pg)
+        mine = torch.tensor(list(bytes(blob)), dtype=torch.uint8)
+        if dist.get_backend(pg) == "nccl":
+            mine = mine.cuda()
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=pg)
+        allb = np.concatenate([p.cpu().numpy() for p in parts]).astype(np.uint8)
+        L.mph_gcn_p2p_open(self.h, allb.ctypes.data, world, stream_ptr(stream))
+
+    def p2p_status(self) -> int:
+        """0, or MPH_ETIMEOUT (-10) when a peer-memory wait gave up (NEXT-1)."""
+        e = C.c_int32()
+        L.mph_gcn_p2p_status(self.h, C.byref(e))
+        return e.value
 
     # -- parameter views ([F_in][F_out] weights, [F_out] biases; padding excluded)
     def _views(self, flat):

@@ -110,6 +110,38 @@ __device__ __forceinline__ float4 f4_tf32(float4 v) {
   return make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
 }
 
+// ---- peer-memory flags (NEXT-1, p2p.cu): system-scope release/acquire over NVLink
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t global_timer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// One thread waits until flags_row[q] >= seq for every q < world (each peer's monotone step
+// counter, written remotely by st_release_sys_u64).  Gives up after 10 s, recording the
+// timeout in *err (and every later wait returns at once), so a lost peer cannot hang the GPU.
+__device__ __forceinline__ bool p2p_wait_all(const uint64_t* flags_row, int world, uint64_t seq, int* err) {
+  if (*(volatile int*)err) return false;
+  const uint64_t t0 = global_timer_ns();
+  for (int q = 0; q < world; ++q) {
+    while (ld_acquire_sys_u64(flags_row + q) < seq) {
+      if (global_timer_ns() - t0 > 10000000000ull) {
+        atomicExch(err, 1);
+        return false;
+      }
+      __nanosleep(128);
+    }
+  }
+  return true;
+}
+
 // Philox4x32-10 (Salmon et al., SC'11) — the dropout mask of reading Q10.
 struct PhiloxOut {
   uint32_t v[4];

@@ -172,17 +172,32 @@ int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* label
 // ------------------------------------------------------------------ a9 Adam
 // Bias corrections are computed on the device from t (host value, or device counter during a
 // CUDA-graph replay), so eager and graph epochs are bitwise identical.
-__global__ void k_optim(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+__global__ void k_optim(float* __restrict__ p, float* __restrict__ g, float* __restrict__ m,
                         float* __restrict__ v, int64_t n, int kind, float lr, float b1, float b2, float eps, float wd,
-                        float mu, int t_host, const int32_t* t_dev) {
+                        float mu, int t_host, const int32_t* t_dev, const float* __restrict__ gsum, int world,
+                        const uint64_t* flags_grad, const int64_t* gen_dev, int* err) {
   const int t = t_dev ? *t_dev : t_host;
   float bc1 = 1.0f, bc2 = 1.0f;
   if (kind != MPH_OPT_SGD) {
     bc1 = (float)(1.0 - pow((double)b1, (double)t));
     bc2 = (float)(1.0 - pow((double)b2, (double)t));
   }
+  if (gsum) {  // NEXT-1: every rank's slab of this generation has landed (p2p.cu)
+    __shared__ int ok;
+    if (threadIdx.x == 0) ok = p2p_wait_all(flags_grad, world, (uint64_t)*gen_dev, err);
+    __syncthreads();
+    if (!ok) return;
+    gsum += (*gen_dev & 1) * world * n;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
+    float gi;
+    if (gsum) {  // the all-reduce: slabs summed in rank order, the same bits on every rank
+      gi = __ldcg(gsum + i);
+      for (int q = 1; q < world; ++q) gi += __ldcg(gsum + (int64_t)q * n + i);
+      g[i] = gi;
+    } else {
+      gi = g[i];
+    }
     if (kind == MPH_OPT_SGD) {  // d = g + wd·p; m = μ·m + d (μ > 0); p -= lr·d   (R8)
       float d = wd != 0.0f ? gi + wd * p[i] : gi;
       if (mu != 0.0f) {
@@ -202,19 +217,41 @@ __global__ void k_optim(float* __restrict__ p, const float* __restrict__ g, floa
   }
 }
 
-int optim_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_optim_cfg* cfg, int t,
-                 cudaStream_t s, const int32_t* t_dev) {
+static int optim_check(const float* p, const float* g, const float* m, const float* v, int64_t n,
+                       const mph_optim_cfg* cfg, int t, const int32_t* t_dev) {
   if (!p || !g || !cfg || n < 0 || (t < 1 && !t_dev) || cfg->kind < MPH_OPT_ADAM || cfg->kind > MPH_OPT_ADAMW)
     return fail(MPH_EINVAL, "optim: bad arguments");
   if (cfg->kind != MPH_OPT_SGD && (!m || !v)) return fail(MPH_EINVAL, "optim: Adam/AdamW need m and v");
   if (cfg->kind == MPH_OPT_SGD && cfg->momentum != 0.0f && !m) return fail(MPH_EINVAL, "optim: momentum needs m");
+  return MPH_OK;
+}
+
+int optim_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_optim_cfg* cfg, int t,
+                 cudaStream_t s, const int32_t* t_dev) {
+  MPH_TRY(optim_check(p, g, m, v, n, cfg, t, t_dev));
   if (n == 0) return MPH_OK;
   const float wd = cfg->kind == MPH_OPT_ADAM ? 0.0f : cfg->weight_decay;
   const float mu = cfg->kind == MPH_OPT_SGD ? cfg->momentum : 0.0f;
   k_optim<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 8), 256, 0, s>>>(
-      p, g, m, v, n, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, wd, mu, t, t_dev);
+      p, const_cast<float*>(g), m, v, n, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, wd, mu, t, t_dev,
+      nullptr, 1, nullptr, nullptr, nullptr);
   count_launch();
   return launch_check("optim");
+}
+
+int optim_sum_launch(float* p, float* grads, float* m, float* v, int64_t n, const mph_optim_cfg* cfg, int t,
+                     cudaStream_t s, const int32_t* t_dev, const float* gsum, int world, const uint64_t* flags_grad,
+                     const int64_t* gen_dev, int* err) {
+  MPH_TRY(optim_check(p, grads, m, v, n, cfg, t, t_dev));
+  if (!gsum || !flags_grad || !gen_dev || !err || world < 1) return fail(MPH_EINVAL, "optim_sum: bad arguments");
+  if (n == 0) return MPH_OK;
+  const float wd = cfg->kind == MPH_OPT_ADAM ? 0.0f : cfg->weight_decay;
+  const float mu = cfg->kind == MPH_OPT_SGD ? cfg->momentum : 0.0f;
+  k_optim<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 4), 256, 0, s>>>(
+      p, grads, m, v, n, cfg->kind, cfg->lr, cfg->beta1, cfg->beta2, cfg->eps, wd, mu, t, t_dev, gsum, world,
+      flags_grad, gen_dev, err);
+  count_launch();
+  return launch_check("optim (fused gradient sum)");
 }
 
 int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_adam_cfg* cfg, int t, cudaStream_t s,

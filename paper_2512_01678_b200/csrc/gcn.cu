@@ -43,6 +43,7 @@ struct mph_gcn {
   const mph_graph* g = nullptr;
   const mph_features* f = nullptr;
   mph_comm* comm = nullptr;
+  P2PState* p2p = nullptr;  // MPH_COMM_P2P: NVLink peer-memory exchange (p2p.cu, NEXT-1)
   int world = 1;
   int L = 0;
   int agg = MPH_AGG_GCN;  // aggregation scheme (NEXT-4)
@@ -82,12 +83,18 @@ namespace mph {
 
 static int64_t align16(int64_t x) { return (x + 15) / 16 * 16; }
 
+static bool in_arena(const mph_gcn* m, const void* ptr) {
+  if (!m->p2p || !m->p2p->arena || !ptr) return false;
+  const char* c = (const char*)ptr;
+  return c >= m->p2p->arena && c < m->p2p->arena + m->p2p->arena_bytes;
+}
+
 static void gcn_free(mph_gcn* m) {
   if (!m) return;
   for (auto& l : m->layers) {
-    dev_free(l.T);
+    if (!in_arena(m, l.T)) dev_free(l.T);
     dev_free(l.out);
-    dev_free(l.dZ);
+    if (!in_arena(m, l.dZ)) dev_free(l.dZ);
     dev_free(l.G);
     dev_free(l.Y);
     dev_free(l.colsum);
@@ -101,7 +108,7 @@ static void gcn_free(mph_gcn* m) {
   dev_free(m->wt);
   dev_free(m->wr);
   dev_free(m->Xr);
-  dev_free(m->Xs);
+  if (!in_arena(m, m->Xs)) dev_free(m->Xs);
   dev_free(m->ws);
   for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss, m->ev_copied, m->ev_derived})
     if (e) cudaEventDestroy(e);
@@ -110,6 +117,7 @@ static void gcn_free(mph_gcn* m) {
   if (m->graph) cudaGraphDestroy(m->graph);
   dev_free(m->t_dev);
   dev_free(m->loss_dev);
+  p2p_free(m->p2p);
   delete m;
 }
 
@@ -136,14 +144,27 @@ static int spmm_p(const mph_graph* g, const float* in, int w, int ld_in, float* 
 // pack runs on the compute stream, the grouped send/recv on the comm stream, and the
 // local-edge part of the SpMM overlaps the transfer; the ghost-edge part and the fused
 // epilogue run once the halo has landed (overlap P:765).
-static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogue* e, const float* post,
-                     cudaStream_t s) {
+// Shared-buffer indices of the P2P arena (P2PState::off_buf): T'_l, dZ'_l, dinv ⊙ X.
+static int buf_T(int li) { return 2 * li; }
+static int buf_dZ(int li) { return 2 * li + 1; }
+static int buf_Xs(const mph_gcn* m) { return 2 * m->L; }
+
+static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogue* e, const float* post, int xchg,
+                     int buf, cudaStream_t s) {
   const mph_graph* g = m->g;
   if (m->world == 1) return spmm_p(g, in, w, w, out, w, e, post, s);
-  MPH_TRY(halo_pack(g, in, w, w, s));
-  MPH_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
-  MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_pack, 0));
-  {
+  if (m->p2p) {
+    // NEXT-1: publish "my rows of this buffer are final" (exchange xchg of this generation),
+    // then the comm stream pulls the ghost rows from their owners over NVLink
+    MPH_TRY(p2p_signal(m->p2p, kSlotHalo, true, kP2PHaloPerGen, xchg, s));
+    MPH_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
+    MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_pack, 0));
+    prof::Scope sc(MPH_PROF_HALO, m->cs, 4.0 * (double)(g->n_cols - g->n_rows) * w, 0.0);
+    MPH_TRY(p2p_pull(m->p2p, buf, in, w, kSlotHalo, true, kP2PHaloPerGen, xchg, m->cs));
+  } else {
+    MPH_TRY(halo_pack(g, in, w, w, s));
+    MPH_CUDA_TRY(cudaEventRecord(m->ev_pack, s));
+    MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_pack, 0));
     prof::Scope sc(MPH_PROF_HALO, m->cs, 4.0 * (double)(g->n_cols - g->n_rows) * w, 0.0);
     MPH_TRY(halo_sendrecv(g, m->comm, in, w, w, m->cs));
   }
@@ -162,6 +183,7 @@ static int grad_allreduce_async(mph_gcn* m, int li, cudaStream_t s) {
   const int64_t b = li + 1 < m->L ? m->layers[li + 1].off_w : m->n_params;
   MPH_CUDA_TRY(cudaEventRecord(m->ev_grad, s));
   MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_grad, 0));
+  if (m->p2p) return p2p_grad_push(m->p2p, m->grads, a, b, m->cs);  // NEXT-1: into every rank's slab
   return mph_allreduce_sum(m->comm, m->grads + a, b - a, 0, m->cs);
 }
 static int gemm_nt_p(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
@@ -245,7 +267,7 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
       MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, A, lda, m->wt + l.off_wt, l.pin, l.T, l.pout, &et, s));
     }
     // a10 + a3: ghost rows of T' from their owners; Z = Â·T + b, ReLU (dropout) fused
-    MPH_TRY(spmm_halo(m, l.T, l.pout, l.out, &eo, m->fpost, s));
+    MPH_TRY(spmm_halo(m, l.T, l.pout, l.out, &eo, m->fpost, li, buf_T(li), s));
   } else {
     // aggregate-first layer 1: Y = Â·X (on dinv ⊙ X), Z = Y·W + b with the epilogue fused in the GEMM
     mph_epilogue en = epi_none();
@@ -258,6 +280,7 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
 
 static int do_forward(mph_gcn* m, int epoch, cudaStream_t s) {
   m->epoch = epoch;
+  if (m->p2p) MPH_TRY(p2p_gen_advance(m->p2p, s));  // one generation of flags per epoch
   for (int li = 0; li < m->L; ++li) MPH_TRY(layer_forward(m, li, s));
   m->fwd_done = true;
   m->loss_done = false;
@@ -303,7 +326,7 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       // a10 + a6: G = AGGᵀ·dZ = bpost ⊙ Ã·dZ' (Â symmetric: the forward kernel)
       mph_epilogue en = epi_none();
       en.flags = MPH_EPI_TF32;  // G only feeds the dW and dH GEMMs
-      MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, m->bpost, s));
+      MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, m->bpost, m->L + li, buf_dZ(li), s));
       Gsrc = l.G;
       // a7: dW = H^T·G  (sparse layer 1: X_csc^T·G)
       if (li == 0 && m->f->mode == 1) {
@@ -343,6 +366,7 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
     }
   }
   if (m->world > 1) {  // Adam needs every summed gradient segment
+    if (m->p2p) MPH_TRY(p2p_signal(m->p2p, kSlotGrad, true, 1, 0, m->cs));  // all my slabs are pushed
     MPH_CUDA_TRY(cudaEventRecord(m->ev_comm_done, m->cs));
     MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_comm_done, 0));
   }
@@ -364,9 +388,21 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   if (desc->dropout_p < 0.0f || desc->dropout_p >= 1.0f) return fail(MPH_EINVAL, "dropout_p must be in [0,1)");
   if (desc->aggregator < MPH_AGG_GCN || desc->aggregator > MPH_AGG_MAX)
     return fail(MPH_EINVAL, "unknown aggregator %d", desc->aggregator);
+  if (desc->comm_mode != MPH_COMM_NCCL && desc->comm_mode != MPH_COMM_P2P)
+    return fail(MPH_EINVAL, "unknown comm_mode %d", desc->comm_mode);
+  const bool p2p = desc->comm_mode == MPH_COMM_P2P && g->local && g->world > 1;
   int world = 1;
-  if (comm) MPH_TRY(mph_comm_info(comm, &world, nullptr));
+  if (p2p) {
+    if (comm) return fail(MPH_EINVAL, "MPH_COMM_P2P takes comm = NULL (the peers are mapped by mph_gcn_p2p_open)");
+    if (g->world > kP2PMaxWorld) return fail(MPH_ENOTSUP, "MPH_COMM_P2P: world %d > %d", g->world, kP2PMaxWorld);
+    if (2 * desc->num_layers > kP2PHaloPerGen) return fail(MPH_ENOTSUP, "MPH_COMM_P2P: more than 8 layers");
+    world = g->world;
+  } else if (comm) {
+    MPH_TRY(mph_comm_info(comm, &world, nullptr));
+  }
   if (world > 1 && !g->local) return fail(MPH_EINVAL, "distributed model needs a localized graph");
+  if (g->local && g->world > 1 && world != g->world)
+    return fail(MPH_EINVAL, "localized graph of world %d needs a comm (NCCL) or comm_mode = MPH_COMM_P2P", g->world);
   const bool max_agg = desc->aggregator == MPH_AGG_MAX;
   if (max_agg && (world > 1 || f->mode != 0))
     return fail(MPH_ENOTSUP, "max aggregation: single GPU, dense-mode features only");
@@ -417,17 +453,47 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     return bail(rc);
   size_t ws = softmax_ce_ws_bytes(g->n_rows, m->layers.back().fout);
   const int64_t nr = g->n_rows, nc = g->n_cols;
+  // NEXT-1: every buffer a peer reads (T'_l, dZ'_l of transform-first layers, dinv ⊙ X of an
+  // aggregate-first layer 1) is carved from the rank's peer-mapped arena
+  auto shared_bytes = [&](int64_t rows, int w) { return (rows * w * 4 + 255) / 256 * 256; };
+  int64_t arena_next = 0;
+  auto carve = [&](float** ptr, int64_t rows, int w, int buf) {
+    m->p2p->off_buf[buf] = arena_next;
+    *ptr = (float*)(m->p2p->arena + arena_next);
+    arena_next += shared_bytes(rows, w);
+  };
+  if (p2p) {
+    m->p2p = new P2PState();
+    m->p2p->world = world;
+    m->p2p->rank = g->rank;
+    m->p2p->n_params = off;
+    m->p2p->n_rows = nr;
+    m->p2p->row0 = g->row0;
+    m->p2p->off_buf.assign(2 * m->L + 1, -1);
+    int64_t bytes = 0;
+    for (const auto& l : m->layers)
+      if (l.order == 0) bytes += 2 * shared_bytes(nc, l.pout);
+    if (m->layers[0].order == 1) bytes += shared_bytes(nc, m->layers[0].pin);
+    if ((rc = p2p_alloc_arena(m->p2p, (size_t)bytes))) return bail(rc);
+    arena_next = (int64_t)m->p2p->arena_bytes - bytes;
+  }
   for (int li = 0; li < m->L; ++li) {
     Layer& l = m->layers[li];
     if ((rc = dev_alloc(&l.out, (size_t)nr * l.pout))) return bail(rc);
-    if ((rc = dev_alloc(&l.dZ, (size_t)(l.order == 0 ? nc : nr) * l.pout))) return bail(rc);
+    if (p2p && l.order == 0)
+      carve(&l.dZ, nc, l.pout, buf_dZ(li));
+    else if ((rc = dev_alloc(&l.dZ, (size_t)(l.order == 0 ? nc : nr) * l.pout)))
+      return bail(rc);
     if ((rc = dev_alloc(&l.colsum, (size_t)ceil_div(nr, 128) * l.pout))) return bail(rc);
     if (max_agg) {
       if ((rc = dev_alloc(&l.Y, (size_t)nr * l.pin))) return bail(rc);
       if (li > 0 && ((rc = dev_alloc(&l.arg, (size_t)nr * l.pin)) || (rc = dev_alloc(&l.dY, (size_t)nr * l.pin))))
         return bail(rc);
     } else if (l.order == 0) {
-      if ((rc = dev_alloc(&l.T, (size_t)nc * l.pout))) return bail(rc);
+      if (p2p)
+        carve(&l.T, nc, l.pout, buf_T(li));
+      else if ((rc = dev_alloc(&l.T, (size_t)nc * l.pout)))
+        return bail(rc);
       if ((rc = dev_alloc(&l.G, (size_t)nr * l.pout))) return bail(rc);
     } else {
       if ((rc = dev_alloc(&l.Y, (size_t)nr * l.pin))) return bail(rc);
@@ -462,11 +528,15 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   } else if (m->layers[0].order == 1) {
     // X is constant input data: its pre-scale (and, distributed, its ghost rows) are set up once.
     const Layer& l = m->layers[0];
-    if ((rc = dev_alloc(&m->Xs, (size_t)nc * l.pin))) return bail(rc);
+    if (p2p)
+      carve(&m->Xs, nc, l.pin, buf_Xs(m));
+    else if ((rc = dev_alloc(&m->Xs, (size_t)nc * l.pin)))
+      return bail(rc);
     e = cudaMemsetAsync(m->Xs, 0, (size_t)nc * l.pin * 4, s);
     if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "memset: %s", cudaGetErrorString(e)));
     if ((rc = rowscale_launch(f->X, f->P, m->fpre, (int)nr, l.pin, m->Xs, l.pin, 0, s))) return bail(rc);
-    if (world > 1 && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
+    // P2P: the ghost rows of dinv ⊙ X arrive in mph_gcn_p2p_open, once the peers are mapped
+    if (world > 1 && !p2p && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
   }
   if (world > 1) {
     e = cudaStreamCreateWithFlags(&m->cs, cudaStreamNonBlocking);
@@ -475,7 +545,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create streams: %s", cudaGetErrorString(e)));
     int wmax = m->layers[0].pin;
     for (const auto& l : m->layers) wmax = std::max(wmax, l.pout);
-    if ((rc = halo_reserve(g, wmax))) return bail(rc);  // no reallocation while sends are in flight
+    if (!p2p && (rc = halo_reserve(g, wmax))) return bail(rc);  // no reallocation while sends are in flight
   }
   if (m->layers[0].order == 0 && f->mode == 0 && !max_agg) {
     // TF32-rounded copy of X: the A operand of the layer-1 transform and of its dW GEMM
@@ -537,6 +607,14 @@ static int copy_features(const mph_features* f, const float* X_h, int32_t ld_h, 
   return MPH_OK;
 }
 
+// Ghost rows of the constant operand dinv ⊙ X (aggregate-first layer 1) over peer memory: a
+// setup-slot signal with a host counter (create/upload are not captured in graphs), then a pull.
+static int p2p_setup_exchange(mph_gcn* m, cudaStream_t s) {
+  const int64_t seq = ++m->p2p->xgen;
+  MPH_TRY(p2p_signal(m->p2p, kSlotSetup, false, 0, seq, s));
+  return p2p_pull(m->p2p, buf_Xs(m), m->Xs, m->layers[0].pin, kSlotSetup, false, 0, seq, s);
+}
+
 // Everything the epoch reads is derived from X here (TF32 copy Xr, pre-scaled Xs, or MAX(X)); the
 // epoch itself never reads f->X, so the next step's X may land in f->X while an epoch runs.
 static int derive_from_features(mph_gcn* m, cudaStream_t s) {
@@ -549,7 +627,11 @@ static int derive_from_features(mph_gcn* m, cudaStream_t s) {
   } else if (m->layers[0].order == 1) {
     const Layer& l = m->layers[0];
     MPH_TRY(rowscale_launch(f->X, f->P, m->fpre, m->g->n_rows, l.pin, m->Xs, l.pin, 0, s));
-    if (m->world > 1) MPH_TRY(mph_halo_exchange(m->g, m->comm, m->Xs, l.pin, l.pin, s));
+    if (m->p2p) {
+      MPH_TRY(p2p_setup_exchange(m, s));
+    } else if (m->world > 1) {
+      MPH_TRY(mph_halo_exchange(m->g, m->comm, m->Xs, l.pin, l.pin, s));
+    }
   } else {
     MPH_TRY(rowscale_launch(f->X, f->P, nullptr, m->g->n_rows, f->P, m->Xr, f->P, 1, s));
   }
@@ -603,7 +685,10 @@ extern "C" int mph_gcn_loss(mph_gcn* m, double* loss_d, void* stream) {
   if (m->world > 1) {  // global loss = sum of per-rank partial sums / global N_lab
     MPH_CUDA_TRY(cudaEventRecord(m->ev_loss, s));
     MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_loss, 0));
-    MPH_TRY(mph_allreduce_sum(m->comm, loss_d, 1, 1, m->cs));
+    if (m->p2p)
+      MPH_TRY(p2p_loss_sum(m->p2p, loss_d, m->cs));
+    else
+      MPH_TRY(mph_allreduce_sum(m->comm, loss_d, 1, 1, m->cs));
     MPH_CUDA_TRY(cudaEventRecord(m->ev_loss, m->cs));
     MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_loss, 0));
   }
@@ -624,7 +709,13 @@ extern "C" int mph_gcn_optim_step(mph_gcn* m, const mph_optim_cfg* cfg, int32_t 
   if (!m || !cfg) return fail(MPH_EINVAL, "gcn_optim_step arguments");
   cudaStream_t s = (cudaStream_t)stream;
   prof::Scope sc(MPH_PROF_ADAM, s, (cfg->kind == MPH_OPT_SGD ? 20.0 : 28.0) * m->n_params, 0.0);
-  MPH_TRY(optim_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s, m->graph_mode ? m->t_dev : nullptr));
+  if (m->p2p) {  // NEXT-1: gradient all-reduce fused into the update (rank-order slab sum)
+    MPH_TRY(optim_sum_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s,
+                             m->graph_mode ? m->t_dev : nullptr, p2p_gsum_local(m->p2p), m->world,
+                             p2p_flags_local(m->p2p, kSlotGrad), m->p2p->gen_dev, m->p2p->err_dev));
+  } else {
+    MPH_TRY(optim_launch(m->params, m->grads, m->m, m->v, m->n_params, cfg, t, s, m->graph_mode ? m->t_dev : nullptr));
+  }
   return refresh_wt(m, s);
 }
 
@@ -666,7 +757,8 @@ extern "C" int mph_gcn_graph_capture(mph_gcn* m, const mph_adam_cfg* cfg, int32_
 
 extern "C" int mph_gcn_graph_capture_opt(mph_gcn* m, const mph_optim_cfg* cfg, int32_t t_next, void* stream) {
   if (!m || !cfg || t_next < 1) return fail(MPH_EINVAL, "graph_capture arguments");
-  if (m->world > 1) return fail(MPH_ENOTSUP, "graph capture is single-GPU (NCCL p2p is issued eagerly)");
+  if (m->world > 1 && !m->p2p)
+    return fail(MPH_ENOTSUP, "graph capture with P > 1 needs comm_mode = MPH_COMM_P2P (NCCL calls are eager)");
   if (!m->warm) return fail(MPH_ESTATE, "run one eager mph_gcn_train_epoch before capturing (lazy setup)");
   cudaStream_t user = (cudaStream_t)stream;
   MPH_CUDA_TRY(cudaStreamSynchronize(user));
@@ -786,6 +878,36 @@ extern "C" int mph_gcn_info(const mph_gcn* m, int32_t* order_h, int32_t* mode_h)
   if (order_h)
     for (int li = 0; li < m->L; ++li) order_h[li] = m->layers[li].order;
   if (mode_h) *mode_h = m->f->mode;
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_p2p_export(const mph_gcn* m, uint8_t* blob_h) {
+  if (!m || !blob_h) return fail(MPH_EINVAL, "p2p_export arguments");
+  if (!m->p2p) return fail(MPH_ESTATE, "p2p_export: model was not created with comm_mode = MPH_COMM_P2P");
+  return p2p_export(m->p2p, blob_h);
+}
+
+extern "C" int mph_gcn_p2p_open(mph_gcn* m, const uint8_t* blobs_h, int32_t world, void* stream) {
+  if (!m || !blobs_h) return fail(MPH_EINVAL, "p2p_open arguments");
+  if (!m->p2p) return fail(MPH_ESTATE, "p2p_open: model was not created with comm_mode = MPH_COMM_P2P");
+  cudaStream_t s = (cudaStream_t)stream;
+  MPH_CUDA_TRY(cudaDeviceSynchronize());  // the arena (and dinv ⊙ X) are initialised before peers look
+  MPH_TRY(p2p_open(m->p2p, m->g, blobs_h, world));
+  if (m->Xs) MPH_TRY(p2p_setup_exchange(m, s));
+  MPH_CUDA_TRY(cudaStreamSynchronize(s));
+  int err = 0;
+  MPH_CUDA_TRY(cudaMemcpy(&err, m->p2p->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) return fail(MPH_ETIMEOUT, "p2p_open: a peer did not signal within 10 s");
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_p2p_status(const mph_gcn* m, int32_t* err_h) {
+  if (!m || !err_h) return fail(MPH_EINVAL, "p2p_status arguments");
+  *err_h = 0;
+  if (!m->p2p) return MPH_OK;
+  int err = 0;
+  MPH_CUDA_TRY(cudaMemcpy(&err, m->p2p->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  *err_h = err ? MPH_ETIMEOUT : 0;
   return MPH_OK;
 }
 

@@ -429,6 +429,7 @@ extern "C" int mph_graph_from_plan(const mph_plan* p, void* stream, mph_graph** 
   g->recv_offset = p->recv_offset;
   g->n_recv = p->n_recv;
   g->send_offset = p->send_offset;
+  g->ghosts = p->ghosts;
   g->n_send = (int64_t)p->send_ids.size();
   int64_t* split_count = nullptr;
   int rc = MPH_OK;

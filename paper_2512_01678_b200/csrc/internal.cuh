@@ -21,6 +21,7 @@ struct mph_graph {
   int64_t row0 = 0;
   int64_t* split = nullptr;  // [n_rows] absolute edge index where ghost columns start
   std::vector<int64_t> recv_offset, n_recv, send_offset;  // host, per peer
+  std::vector<int64_t> ghosts;                            // host, global ids of the ghost columns
   int32_t* send_ids = nullptr;                            // device, concatenated per peer
   int64_t n_send = 0;
   float* send_buf = nullptr;
@@ -59,6 +60,58 @@ struct mph_features {
 };
 
 constexpr int64_t kSegNnz = 128;
+
+// NEXT-1: peer-memory (NVLink) communication state of a MPH_COMM_P2P model (p2p.cu).
+// One cudaMalloc arena per rank, mapped by every peer through CUDA IPC:
+//   [flags: uint64 [kP2PSlots][kP2PMaxWorld]] [loss: double [2][kP2PMaxWorld]]
+//   [gsum: float [2][world][n_params]] [shared buffers: T'_l, dZ'_l, dinv ⊙ X ...]
+// flags[slot][q] is the latest step counter rank q has signalled for that slot; the loss and
+// gradient slabs are indexed by the parity of the generation (double buffered).
+constexpr int kP2PMaxWorld = 16;
+enum P2PSlot { kSlotHalo = 0, kSlotLoss = 1, kSlotGrad = 2, kSlotSetup = 3, kP2PSlots = 4 };
+constexpr int kP2PHaloPerGen = 16;  // halo exchanges per epoch (2L <= 16)
+
+struct P2PState {
+  int world = 1, rank = 0;
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  int64_t off_flags = 0, off_loss = 0, off_gsum = 0;  // bytes into the arena
+  int64_t n_params = 0;
+  int64_t n_rows = 0, row0 = 0;
+  std::vector<int64_t> off_buf;  // this rank's shared buffers (byte offsets, -1 = absent)
+  // after mph_gcn_p2p_open
+  bool opened = false;
+  std::vector<char*> peer_base;                 // mapped arenas (own arena at [rank])
+  std::vector<std::vector<int64_t>> peer_off;   // peers' off_buf
+  std::vector<int64_t> peer_flags_off, peer_loss_off, peer_gsum_off;
+  int32_t* ghost_ref = nullptr;  // device [n_ghost]: owner << 27 | owner-local row
+  int64_t n_ghost = 0;
+  int64_t* gen_dev = nullptr;    // device generation counter, advanced once per forward
+  int* err_dev = nullptr;        // device timeout flag
+  int64_t xgen = 0;              // host counter of setup exchanges (constant operands)
+};
+
+namespace mph {
+int p2p_alloc_arena(P2PState* p, size_t bytes);
+void p2p_free(P2PState* p);
+int p2p_export(const P2PState* p, uint8_t* blob);
+int p2p_open(P2PState* p, const mph_graph* g, const uint8_t* blobs, int world);
+// flags[slot][rank] := gen·mult + add in every peer's arena (gen from the device counter when
+// use_gen, else 0), after a system-scope fence: everything this stream wrote before is visible.
+int p2p_signal(const P2PState* p, int slot, bool use_gen, int64_t mult, int64_t add, cudaStream_t s);
+// Wait for every peer's flags[slot] >= gen·mult + add, then copy each ghost row of shared buffer
+// `buf` from its owner into the local ghost slice [n_rows, n_cols) of `local` (stride ld = w).
+int p2p_pull(const P2PState* p, int buf, float* local, int w, int slot, bool use_gen, int64_t mult, int64_t add,
+             cudaStream_t s);
+// grads[a, b) -> every rank's gradient slab [parity][rank] (a, b, multiples of 4).
+int p2p_grad_push(const P2PState* p, const float* grads, int64_t a, int64_t b, cudaStream_t s);
+// Global loss: push this rank's partial, signal, wait for all, sum in rank order into loss_d.
+int p2p_loss_sum(const P2PState* p, double* loss_d, cudaStream_t s);
+int p2p_gen_advance(const P2PState* p, cudaStream_t s);
+// The gradient slabs of the current parity and the grad flag row, for the fused optimizer.
+const float* p2p_gsum_local(const P2PState* p);
+const uint64_t* p2p_flags_local(const P2PState* p, int slot);
+}  // namespace mph
 
 namespace mph {
 
@@ -108,6 +161,12 @@ int adam_launch(float* p, const float* g, float* m, float* v, int64_t n, const m
                 const int32_t* t_dev = nullptr);
 int optim_launch(float* p, const float* g, float* m, float* v, int64_t n, const mph_optim_cfg* cfg, int t,
                  cudaStream_t s, const int32_t* t_dev = nullptr);
+// NEXT-1 fused gradient sum + optimizer: waits until every rank's flags_grad >= *gen, takes
+// g[i] = Σ_q gsum[(par·world + q)·n + i] in rank order (par = *gen & 1), writes it to grads[i]
+// and applies the update of optim_launch in the same pass.
+int optim_sum_launch(float* p, float* grads, float* m, float* v, int64_t n, const mph_optim_cfg* cfg, int t,
+                     cudaStream_t s, const int32_t* t_dev, const float* gsum, int world, const uint64_t* flags_grad,
+                     const int64_t* gen_dev, int* err);
 int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int layer, cudaStream_t s);
 // dst_t[j*ld_t + i] = tf32(src[i*ld_src + j]), dst_r[i*ld_r + j] = tf32(src[i*ld_src + j]) (dst_r nullable)
 int weight_copies_launch(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,
