@@ -8,7 +8,10 @@ forward, softmax-CE, backward, (halo + gradient all-reduce when N > 1) and Adam,
 synthetic graph shaped like the named config (synth/, seeded).  For N > 1 launch with
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N
-(one rank per GPU, NCCL; the graph is 1D row-partitioned, so total work is fixed: strong scaling).
+(one rank per GPU; the graph is 1D row-partitioned, so total work is fixed: strong scaling).  The
+halo rows and the gradient sum travel over NVLink peer memory by default (--comm p2p, SURVEY §8(f)
+NEXT-1: the ranks map each other's buffers via CUDA IPC; torch.distributed only all-gathers the
+descriptors, barriers and takes the max of the timings) or through NCCL (--comm nccl).
 """
 from __future__ import annotations
 
@@ -496,9 +499,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--partition", default="1d", choices=["1d", "greedy", "hierarchical"],
                     help="N > 1: contiguous 1D (north star) or Alg. 4 Phase III / II-III + relabelling")
-    ap.add_argument("--comm", default="nccl", choices=["nccl", "p2p"],
-                    help="N > 1: NCCL grouped send/recv + all-reduce, or NVLink peer-memory pulls with the "
-                         "gradient sum fused into the optimizer (SURVEY §8(f) NEXT-1)")
+    ap.add_argument("--comm", default="p2p", choices=["nccl", "p2p"],
+                    help="N > 1: NVLink peer-memory halo pulls with the gradient sum fused into the optimizer "
+                         "(default; SURVEY §8(f) NEXT-1), or NCCL grouped send/recv + all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the gather-bandwidth probe")
     ap.add_argument("--graph", action="store_true",

@@ -436,13 +436,16 @@ int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, const float** 
  *                                  Maps the peers' arenas, builds the ghost-source table and
  *                                  exchanges the ghost rows of dinv ⊙ X.  Collective: every rank
  *                                  calls it once, before its first epoch.  Synchronises.
- *   mph_gcn_p2p_status(m, err_h)   *err_h = 0, or MPH_ETIMEOUT if a wait gave up (a peer stopped
- *                                  signalling): that epoch's results are undefined.  Synchronises.
+ *   mph_gcn_p2p_status(m, err_h, gen_h, flags_h)  *err_h = 0, or MPH_ETIMEOUT if a wait gave up (a
+ *                                  peer stopped signalling): that epoch's results are undefined.
+ *                                  Diagnostics (nullable): *gen_h = epochs run, flags_h[slot·world + q]
+ *                                  = the last step counter rank q signalled here for slot 0 halo,
+ *                                  1 loss, 2 gradient, 3 setup (4·world values).  Synchronises.
  * Constraints: world <= 16; every rank runs the same sequence of epochs. */
 #define MPH_P2P_BLOB_BYTES 512
 int mph_gcn_p2p_export(const mph_gcn* m, uint8_t* blob_h);
 int mph_gcn_p2p_open(mph_gcn* m, const uint8_t* blobs_h, int32_t world, void* stream);
-int mph_gcn_p2p_status(const mph_gcn* m, int32_t* err_h);
+int mph_gcn_p2p_status(const mph_gcn* m, int32_t* err_h, int64_t* gen_h, uint64_t* flags_h);
 
 /* order_h[l-1] = 0 transform-first, 1 aggregate-first; mode_h = feature mode. */
 int mph_gcn_info(const mph_gcn* m, int32_t* order_h, int32_t* mode_h);

@@ -136,7 +136,7 @@ _SIGS = {
     "mph_gcn_info": [P, P, C.POINTER(i32)],
     "mph_gcn_p2p_export": [P, P],
     "mph_gcn_p2p_open": [P, P, i32, P],
-    "mph_gcn_p2p_status": [P, C.POINTER(i32)],
+    "mph_gcn_p2p_status": [P, C.POINTER(i32), C.POINTER(i64), P],
     "mph_gcn_destroy": [P],
 }
 

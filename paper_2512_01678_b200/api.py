@@ -77,7 +77,9 @@ class Graph:
     def from_plan(cls, plan: "Plan", stream=None) -> "Graph":
         h = _out_ptr()
         L.mph_graph_from_plan(plan.h, stream_ptr(stream), C.byref(h))
-        return cls(_handle=h)
+        g = cls(_handle=h)
+        g.world, g.rank = plan.world, plan.rank
+        return g
 
     def csr(self):
         rp, ci, dg, di = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
@@ -355,11 +357,19 @@ class GCN:
         allb = np.concatenate([p.cpu().numpy() for p in parts]).astype(np.uint8)
         L.mph_gcn_p2p_open(self.h, allb.ctypes.data, world, stream_ptr(stream))
 
-    def p2p_status(self) -> int:
-        """0, or MPH_ETIMEOUT (-10) when a peer-memory wait gave up (NEXT-1)."""
-        e = C.c_int32()
-        L.mph_gcn_p2p_status(self.h, C.byref(e))
+    def p2p_status(self, detail: bool = False):
+        """0, or MPH_ETIMEOUT (-10) when a peer-memory wait gave up (NEXT-1).  detail=True also
+        returns the generation and the flag rows [4 slots][world] (halo, loss, grad, setup)."""
+        e, gen = C.c_int32(), C.c_int64()
+        world = max(1, self.graph_world())
+        flags = np.zeros(4 * world, dtype=np.uint64)
+        L.mph_gcn_p2p_status(self.h, C.byref(e), C.byref(gen), flags.ctypes.data)
+        if detail:
+            return e.value, gen.value, flags.reshape(4, world)
         return e.value
+
+    def graph_world(self) -> int:
+        return getattr(self.graph, "world", 1)
 
     # -- parameter views ([F_in][F_out] weights, [F_out] biases; padding excluded)
     def _views(self, flat):

@@ -326,7 +326,9 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       // a10 + a6: G = AGGᵀ·dZ = bpost ⊙ Ã·dZ' (Â symmetric: the forward kernel)
       mph_epilogue en = epi_none();
       en.flags = MPH_EPI_TF32;  // G only feeds the dW and dH GEMMs
-      MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, m->bpost, m->L + li, buf_dZ(li), s));
+      // exchange indices must increase within a generation (the flags are monotone counters):
+      // forward layers 0..L-1, then backward layers L-1..0
+      MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, m->bpost, 2 * m->L - 1 - li, buf_dZ(li), s));
       Gsrc = l.G;
       // a7: dW = H^T·G  (sparse layer 1: X_csc^T·G)
       if (li == 0 && m->f->mode == 1) {
@@ -678,9 +680,8 @@ extern "C" int mph_gcn_forward(mph_gcn* m, int32_t epoch, void* stream) {
   return do_forward(m, epoch, (cudaStream_t)stream);
 }
 
-extern "C" int mph_gcn_loss(mph_gcn* m, double* loss_d, void* stream) {
-  if (!m || !loss_d) return fail(MPH_EINVAL, "gcn_loss arguments");
-  cudaStream_t s = (cudaStream_t)stream;
+// Loss of this rank's rows, then (P > 1) the global sum over ranks on the comm stream.
+static int loss_global(mph_gcn* m, double* loss_d, cudaStream_t s) {
   MPH_TRY(do_loss(m, loss_d, s));
   if (m->world > 1) {  // global loss = sum of per-rank partial sums / global N_lab
     MPH_CUDA_TRY(cudaEventRecord(m->ev_loss, s));
@@ -693,6 +694,11 @@ extern "C" int mph_gcn_loss(mph_gcn* m, double* loss_d, void* stream) {
     MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_loss, 0));
   }
   return MPH_OK;
+}
+
+extern "C" int mph_gcn_loss(mph_gcn* m, double* loss_d, void* stream) {
+  if (!m || !loss_d) return fail(MPH_EINVAL, "gcn_loss arguments");
+  return loss_global(m, loss_d, (cudaStream_t)stream);
 }
 
 extern "C" int mph_gcn_backward(mph_gcn* m, void* stream) {
@@ -784,7 +790,7 @@ extern "C" int mph_gcn_graph_capture_opt(mph_gcn* m, const mph_optim_cfg* cfg, i
     k_step_advance<<<1, 1, 0, cap>>>(m->t_dev);
     count_launch();
     rc = do_forward(m, t_next, cap);
-    if (rc == MPH_OK) rc = do_loss(m, m->loss_dev, cap);
+    if (rc == MPH_OK) rc = loss_global(m, m->loss_dev, cap);
     if (rc == MPH_OK) rc = do_backward(m, cap);
     if (rc == MPH_OK) rc = mph_gcn_optim_step(m, &m->graph_cfg, t_next, cap);
     cudaGraph_t gph = nullptr;
@@ -901,13 +907,19 @@ extern "C" int mph_gcn_p2p_open(mph_gcn* m, const uint8_t* blobs_h, int32_t worl
   return MPH_OK;
 }
 
-extern "C" int mph_gcn_p2p_status(const mph_gcn* m, int32_t* err_h) {
+extern "C" int mph_gcn_p2p_status(const mph_gcn* m, int32_t* err_h, int64_t* gen_h, uint64_t* flags_h) {
   if (!m || !err_h) return fail(MPH_EINVAL, "p2p_status arguments");
   *err_h = 0;
   if (!m->p2p) return MPH_OK;
+  MPH_CUDA_TRY(cudaDeviceSynchronize());
   int err = 0;
   MPH_CUDA_TRY(cudaMemcpy(&err, m->p2p->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
   *err_h = err ? MPH_ETIMEOUT : 0;
+  if (gen_h) MPH_CUDA_TRY(cudaMemcpy(gen_h, m->p2p->gen_dev, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (flags_h)
+    for (int slot = 0; slot < kP2PSlots; ++slot)
+      MPH_CUDA_TRY(cudaMemcpy(flags_h + (size_t)slot * m->world, p2p_flags_local(m->p2p, slot),
+                              sizeof(uint64_t) * m->world, cudaMemcpyDeviceToHost));
   return MPH_OK;
 }
 
