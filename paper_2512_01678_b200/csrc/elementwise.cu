@@ -110,6 +110,133 @@ __global__ void __launch_bounds__(kCeThreads) k_softmax_ce(const float* Z, int N
   }
 }
 
+// Vectorised variant (ld, ld_dz multiples of 4, 16-byte aligned rows): LPR lanes x VPL float4
+// cover a row, 32/LPR rows per warp at once, so a 47-class row is 4 lanes x 3 float4 and no lane
+// idles; exp is evaluated once per element (exp2 of the log2e-scaled shifted logit) and reused
+// for the sum and the gradient.  Same partial layout as k_softmax_ce (fixed-order reductions).
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(kCeThreads) k_softmax_ce4(const float* __restrict__ Z, int N, int C, int ld,
+                                                            const int32_t* __restrict__ labels,
+                                                            const uint8_t* __restrict__ mask, float inv_nlab,
+                                                            const float* __restrict__ row_scale, float* __restrict__ dZ,
+                                                            int ld_dz, double* part_loss, float* part_db,
+                                                            int round_tf32) {
+  constexpr int SPW = 32 / LPR;  // rows per warp step
+  constexpr float kLog2e = 1.4426950408889634f;
+  __shared__ double s_loss[kCeThreads / 32];
+  __shared__ float s_db[kCeThreads / 32][kCeMaxC];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = lane / LPR, sub = lane % LPR;
+  const int nv4 = (C + 3) >> 2;
+  float4 dbacc[VPL];
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) dbacc[j] = f4_zero();
+  double lacc = 0.0;
+  const int64_t gw = (int64_t)blockIdx.x * (kCeThreads / 32) + warp;
+  const int64_t nw = (int64_t)gridDim.x * (kCeThreads / 32);
+  for (int64_t i = gw * SPW + slot; i - slot < N; i += nw * SPW) {
+    const bool ok = i < N;
+    const int64_t r = ok ? i : 0;
+    float4 z[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c4 = sub + j * LPR;
+      z[j] = (ok && c4 < nv4) ? __ldg(reinterpret_cast<const float4*>(Z + r * ld) + c4)
+                              : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (4 * c4 + 3 >= C) {  // columns >= C of the last float4 are padding
+        if (4 * c4 + 1 >= C) z[j].y = -INFINITY;
+        if (4 * c4 + 2 >= C) z[j].z = -INFINITY;
+        if (4 * c4 + 3 >= C) z[j].w = -INFINITY;
+        if (4 * c4 >= C) z[j].x = -INFINITY;
+      }
+    }
+    const int y = ok ? __ldg(labels + r) : -1;
+    const float rsv = (ok && row_scale) ? __ldg(row_scale + r) : 1.0f;
+    const bool lab = ok && (mask ? (__ldg(mask + r) != 0) : true);
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) m = fmaxf(m, fmaxf(fmaxf(z[j].x, z[j].y), fmaxf(z[j].z, z[j].w)));
+#pragma unroll
+    for (int o = 1; o < LPR; o <<= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float ms = ok ? m * kLog2e : 0.0f;
+    float4 ex[VPL];
+    float se = 0.0f, zy = 0.0f;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      ex[j].x = exp2f(fmaf(z[j].x, kLog2e, -ms));
+      ex[j].y = exp2f(fmaf(z[j].y, kLog2e, -ms));
+      ex[j].z = exp2f(fmaf(z[j].z, kLog2e, -ms));
+      ex[j].w = exp2f(fmaf(z[j].w, kLog2e, -ms));
+      se += (ex[j].x + ex[j].y) + (ex[j].z + ex[j].w);
+      const int c0 = 4 * (sub + j * LPR);
+      if (y >= c0 && y < c0 + 4) zy = y == c0 ? z[j].x : (y == c0 + 1 ? z[j].y : (y == c0 + 2 ? z[j].z : z[j].w));
+    }
+#pragma unroll
+    for (int o = 1; o < LPR; o <<= 1) {
+      se += __shfl_xor_sync(0xffffffffu, se, o);
+      zy += __shfl_xor_sync(0xffffffffu, zy, o);
+    }
+    if (!ok) continue;
+    float4* dz = reinterpret_cast<float4*>(dZ + r * ld_dz);
+    if (!lab) {
+#pragma unroll
+      for (int j = 0; j < VPL; ++j)
+        if (sub + j * LPR < nv4) dz[sub + j * LPR] = f4_zero();
+      continue;
+    }
+    const float inv_se = 1.0f / se;
+    if (sub == 0) lacc += (double)(m + logf(se)) - (double)zy;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c4 = sub + j * LPR;
+      if (c4 >= nv4) continue;
+      const int c0 = 4 * c4;
+      float4 g;
+      g.x = (ex[j].x * inv_se - (y == c0 ? 1.0f : 0.0f)) * inv_nlab;
+      g.y = (ex[j].y * inv_se - (y == c0 + 1 ? 1.0f : 0.0f)) * inv_nlab;
+      g.z = (ex[j].z * inv_se - (y == c0 + 2 ? 1.0f : 0.0f)) * inv_nlab;
+      g.w = (ex[j].w * inv_se - (y == c0 + 3 ? 1.0f : 0.0f)) * inv_nlab;
+      dbacc[j] = f4_add(dbacc[j], g);
+      g = make_float4(g.x * rsv, g.y * rsv, g.z * rsv, g.w * rsv);
+      dz[c4] = round_tf32 ? f4_tf32(g) : g;
+    }
+  }
+  // fixed-order reductions: slots of the warp by an xor tree, then warps in order
+#pragma unroll
+  for (int o = LPR; o < 32; o <<= 1) {
+    lacc += __shfl_xor_sync(0xffffffffu, lacc, o);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      dbacc[j].x += __shfl_xor_sync(0xffffffffu, dbacc[j].x, o);
+      dbacc[j].y += __shfl_xor_sync(0xffffffffu, dbacc[j].y, o);
+      dbacc[j].z += __shfl_xor_sync(0xffffffffu, dbacc[j].z, o);
+      dbacc[j].w += __shfl_xor_sync(0xffffffffu, dbacc[j].w, o);
+    }
+  }
+  if (lane == 0) s_loss[warp] = lacc;
+  if (slot == 0) {
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int c0 = 4 * (sub + j * LPR);
+      if (c0 + 0 < C) s_db[warp][c0 + 0] = dbacc[j].x;
+      if (c0 + 1 < C) s_db[warp][c0 + 1] = dbacc[j].y;
+      if (c0 + 2 < C) s_db[warp][c0 + 2] = dbacc[j].z;
+      if (c0 + 3 < C) s_db[warp][c0 + 3] = dbacc[j].w;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kCeThreads / 32; ++w) t += s_loss[w];
+    part_loss[blockIdx.x] = t;
+  }
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float t = 0.0f;
+    for (int w = 0; w < kCeThreads / 32; ++w) t += s_db[w][c];
+    part_db[(int64_t)blockIdx.x * C + c] = t;
+  }
+}
+
 // Block c < C reduces column c of the block partials, block C the loss; strided per-thread sums
 // then a fixed smem tree (deterministic).
 __global__ void __launch_bounds__(256) k_ce_finish(const double* part_loss, const float* part_db, int parts, int C,
@@ -155,7 +282,22 @@ int softmax_ce_launch(const float* Z, int N, int C, int ld, const int32_t* label
   double* part_loss = reinterpret_cast<double*>(ws);
   float* part_db = reinterpret_cast<float*>(part_loss + g);
   const float inv = (float)(1.0 / (double)n_lab);
-  switch ((C + 31) / 32) {
+  const bool vec = ld % 4 == 0 && ld_dz % 4 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(Z) | reinterpret_cast<uintptr_t>(dZ)) & 15) == 0;
+  const int nv4 = (C + 3) / 4;
+#define CE4(LPR, VPL) \
+  k_softmax_ce4<LPR, VPL><<<g, kCeThreads, 0, s>>>(Z, N, C, ld, labels, mask, inv, row_scale, dZ, ld_dz, part_loss, \
+                                                    part_db, round_tf32)
+  if (vec && nv4 <= 1) CE4(1, 1);
+  else if (vec && nv4 <= 2) CE4(2, 1);
+  else if (vec && nv4 <= 4) CE4(4, 1);
+  else if (vec && nv4 <= 8) CE4(8, 1);
+  else if (vec && nv4 <= 12) CE4(4, 3);
+  else if (vec && nv4 <= 16) CE4(16, 1);
+  else if (vec && nv4 <= 32) CE4(32, 1);
+  else if (vec && nv4 <= 64) CE4(32, 2);
+#undef CE4
+  else switch ((C + 31) / 32) {
 #define CE_CASE(NJ)                                                                                              \
   case NJ:                                                                                                       \
     k_softmax_ce<NJ><<<g, kCeThreads, 0, s>>>(Z, N, C, ld, labels, mask, inv, row_scale, dZ, ld_dz, part_loss, \

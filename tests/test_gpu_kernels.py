@@ -246,11 +246,15 @@ def test_gemm_tn(P, M, N, K):
 
 
 # ------------------------------------------------------------------ a5 loss, a9 Adam, Xavier
-@pytest.mark.parametrize("N,C_,masked", [(1, 3, False), (5000, 41, False), (3001, 47, True), (777, 7, True)])
-def test_softmax_ce(P, N, C_, masked):
+@pytest.mark.parametrize("N,C_,masked,ld_odd", [(1, 3, False, False), (5000, 41, False, False), (3001, 47, True, False),
+                                               (777, 7, True, False), (2000, 100, False, False),
+                                               (1500, 256, True, False), (999, 13, False, False),
+                                               (1234, 47, False, True), (321, 5, True, True)])
+def test_softmax_ce(P, N, C_, masked, ld_odd):
+    """Vectorised kernel (ld % 4 == 0: every LPR x VPL shape) and the scalar one (odd ld)."""
     from paper_2512_01678_b200._lib import mph_softmax_ce, mph_softmax_ce_workspace
     rng = np.random.default_rng(N)
-    ld = pad_width(C_)
+    ld = C_ if ld_odd else pad_width(C_)
     Z = (rng.standard_normal((N, C_)) * 5).astype(np.float32)
     y = rng.integers(0, C_, N).astype(np.int32)
     mask = (rng.random(N) < 0.6).astype(np.uint8) if masked else None
