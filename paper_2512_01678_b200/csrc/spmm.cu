@@ -61,35 +61,22 @@ __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int6
   return v;
 }
 
-struct RowSpan {
-  int64_t s, e;
-};
-// Edge range of `row` for this launch's part (-1 whole row, 0 owned columns, 1 ghost columns).
-__device__ __forceinline__ RowSpan row_span(const SpmmArgs& a, int row) {
-  int64_t s = __ldg(a.row_ptr + row), e = __ldg(a.row_ptr + row + 1);
-  if (a.part == 0) e = __ldg(a.split + row);
-  if (a.part == 1) s = __ldg(a.split + row);
-  return {s, e};
-}
-
-// One output row.  [s, e) is its edge range and `first_ids` the neighbour ids of its first 32
-// edges (lane k holds edge s + k), both loaded one row ahead by the item loop of k_spmm.
 template <int LPR, int VPL, bool HAS_VAL, int UOV>
-__device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane, int64_t s, int64_t e, int first_ids) {
+__device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   constexpr int ES = 32 / LPR;
   // U gathers per slot in flight; U*VPL float4 loads per lane before the first use
   constexpr int U0 = (32 / ES) < 8 ? (32 / ES) : 8;
   constexpr int U = UOV > 0 ? UOV : ((U0 * VPL > 8) ? ((8 / VPL) < 2 ? 2 : (8 / VPL)) : U0);
   const int slot = lane / LPR, sub = lane % LPR;
-  // epilogue scalars issued now, consumed after the gathers
-  const float du = (a.part != 0 && a.dinv) ? __ldg(a.dinv + row) : 1.0f;
-  const float rs = (a.part != 0 && (a.epi.flags & MPH_EPI_ROWSCALE)) ? __ldg(a.epi.row_scale + row) : 1.0f;
+  int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
+  if (a.part == 0) e = a.split[row];
+  if (a.part == 1) s = a.split[row];
   float4 acc[VPL];
 #pragma unroll
   for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
   const uint64_t pol = l2_policy_evict_first();
   const int* vbits = reinterpret_cast<const int*>(a.val);
-  int nxt = first_ids;
+  int nxt = (s + lane < e) ? ldg_stream_i32_hint(a.col + s + lane, pol) : 0;
   int nxv = (HAS_VAL && s + lane < e) ? ldg_stream_i32_hint(vbits + s + lane, pol) : 0;
   for (int64_t base = s; base < e; base += 32) {
     const int nb = (int)min((int64_t)32, e - base);
@@ -146,6 +133,8 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane, i
     return;
   }
   const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
+  const float du = a.dinv ? a.dinv[row] : 1.0f;
+  const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[row] : 1.0f;
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
     const int c4 = sub + j * LPR;
@@ -186,21 +175,7 @@ __global__ void __launch_bounds__(256, 3) k_spmm(SpmmArgs a) {
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
-    // two-stage row pipeline: while row r is gathered, the ids of row r+1 and the bounds of
-    // row r+2 are already in flight (the rows of an item are consecutive), so the row_ptr and
-    // neighbour-id latencies are paid once per item instead of once per row
-    const uint64_t pol = l2_policy_evict_first();
-    RowSpan b0 = row_span(a, rr.x);
-    RowSpan b1 = rr.x + 1 < rr.y ? row_span(a, rr.x + 1) : RowSpan{0, 0};
-    int id0 = (b0.s + lane < b0.e) ? ldg_stream_i32_hint(a.col + b0.s + lane, pol) : 0;
-    for (int row = rr.x; row < rr.y; ++row) {
-      const RowSpan b2 = row + 2 < rr.y ? row_span(a, row + 2) : RowSpan{0, 0};
-      const int id1 = (b1.s + lane < b1.e) ? ldg_stream_i32_hint(a.col + b1.s + lane, pol) : 0;
-      spmm_row<LPR, VPL, HAS_VAL, UOV>(a, row, lane, b0.s, b0.e, id0);
-      b0 = b1;
-      b1 = b2;
-      id0 = id1;
-    }
+    for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL, HAS_VAL, UOV>(a, row, lane);
   }
 }
 
