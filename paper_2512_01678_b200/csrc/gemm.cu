@@ -268,9 +268,14 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
   p.n_tiles = (int)ceil_div(M, kBM);
   p.colsum_rows = p.n_tiles;
   const size_t stage_bytes = kATileBytes + (size_t)BN * kBK * 4;
-  const size_t epi_bytes = 16 * (size_t)kEpiChunkBytes;
-  const size_t fixed = 1024 + epi_bytes + 64 * 8 + 16 + 4 * (size_t)BN * sizeof(float);
-  p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, (224 * 1024 - fixed) / stage_bytes));
+  // small K: the mainloop is short and the epilogue (C tile out, mask tile in) is the long pole,
+  // so it gets 8 warps; otherwise 4 warps leave room for a deeper operand ring
+  p.n_epi = (p.num_kb <= 4 && BN >= 64) ? 8 : 4;
+  const size_t epi_bytes = (size_t)p.n_epi * kEpiBufs * kEpiChunkBytes;
+  const size_t fixed = 1024 + epi_bytes + (size_t)BN * sizeof(float) +
+                       (size_t)(2 * 8 + 4 + p.n_epi * kEpiBufs) * 8 + 16 + 4 * (size_t)BN * sizeof(float);
+  constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
+  p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, (kMaxSmem - fixed) / stage_bytes));
   p.idesc = tc::idesc_tf32(kBM, BN, 0, 0);
   p.tmem_cols = tmem_cols_for(2 * BN);
   p.epi.flags = flags;
@@ -298,7 +303,7 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
     configured = smem;
   }
   const int grid = std::min(p.n_tiles, sms);
-  k_gemm_nt<<<grid, kThreads, smem, s>>>(ta, tb, tcm, tm, p);
+  k_gemm_nt<<<grid, 64 + 32 * p.n_epi, smem, s>>>(ta, tb, tcm, tm, p);
   count_launch();
   return launch_check("gemm_nt");
 }
