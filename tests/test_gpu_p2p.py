@@ -165,3 +165,104 @@ def test_p2p_epochs_match_oracle(case):
         for got_g, ref_g in ((gW[l], dWs[l]), (gb[l], dbs[l])):
             rel = np.linalg.norm(got_g - ref_g) / max(np.linalg.norm(ref_g), 1e-30)
             assert rel <= 2e-3, (case, l, rel)
+
+
+def _worker_reddit(rank, world, port, rows_per_rank, result_q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2512_01678_b200 as P
+        from synth.generate import make_workload
+        w = make_workload("reddit")
+        cfg = w["cfg"]
+        n = cfg.num_nodes
+        gfull = P.Graph(w["src"], w["dst"], n)
+        rp, ci = (t.cpu().numpy() for t in gfull.csr()[:2])
+        del gfull
+        bounds = P.partition_1d(rp, world)
+        plan = P.Plan(rp, ci, n, bounds, rank)
+        g = P.Graph.from_plan(plan)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        f = P.Features(torch.from_numpy(np.ascontiguousarray(w["X"][r0:r1])).cuda())
+        m = P.GCN(g, f, cfg.dims, comm="p2p")
+        m.init_xavier(42)
+        m.set_labels(torch.from_numpy(np.ascontiguousarray(w["y"][r0:r1])).cuda(), n_lab_global=n)
+        m.forward(1)
+        loss1 = m.loss().item()
+        rng = np.random.default_rng(rank)
+        rows = np.sort(rng.choice(np.arange(r0, r1), rows_per_rank, replace=False))
+        H1 = m.tensor(1, 1)[torch.as_tensor(rows - r0, device="cuda")].cpu().numpy()
+        m.backward()
+        m.adam(1)
+        loss2 = m.train_epoch(2).item()
+        torch.cuda.synchronize()
+        res = dict(rank=rank, loss1=loss1, loss2=loss2, rows=rows, H1=H1, params=m.params_flat.cpu().numpy().copy(),
+                   status=m.p2p_status(), n_ghost=plan.n_ghost, bounds=bounds)
+        dist.barrier()
+        del m
+        dist.barrier()
+        result_q.put(res)
+    except Exception as e:  # pragma: no cover
+        import traceback
+        result_q.put(dict(rank=rank, error=f"{e!r}\n{traceback.format_exc()}"))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+@pytest.mark.slow
+def test_p2p_reddit_fullsize_world2():
+    """The Reddit-shaped workload at full size as a 2-rank P2P job (each rank half the rows, ~120k
+    ghost rows pulled per exchange): epoch-1 loss against the FP64 oracle forward, sampled H_1
+    rows (aggregating ghost neighbours) against the oracle within the TF32 bound composed through
+    the aggregation, replicas bitwise identical after an Adam step."""
+    import torch.multiprocessing as mp
+    from synth.generate import make_workload
+    world, per = 2, 24
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_reddit, args=(r, world, port, per, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    try:
+        for _ in range(world):
+            r = q.get(timeout=900)
+            out[r["rank"]] = r
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.kill()
+    errs = [r["error"] for r in out.values() if "error" in r]
+    assert not errs, errs[0]
+    res = [out[r] for r in range(world)]
+    for r in res:
+        assert r["status"] == 0 and r["n_ghost"] > 100000
+    assert res[0]["loss1"] == res[1]["loss1"] and res[0]["loss2"] == res[1]["loss2"]
+    assert np.array_equal(res[0]["params"], res[1]["params"])
+    w = make_workload("reddit")
+    cfg = w["cfg"]
+    g = oracle.graph_build(w["src"], w["dst"], cfg.num_nodes)
+    Ws, bs = oracle.xavier_init(cfg.dims, 42)
+    W1 = Ws[0].astype(np.float64)
+    d = g.deg.astype(np.float64)
+    for r in res:
+        lo, hi = int(r["bounds"][r["rank"]]), int(r["bounds"][r["rank"] + 1])
+        crossing = 0
+        for u, h in zip(r["rows"], r["H1"]):
+            nb = g.col_idx[g.row_ptr[u]:g.row_ptr[u + 1]].astype(np.int64)
+            crossing += int(np.any((nb < lo) | (nb >= hi)))
+            a = 1.0 / np.sqrt(d[u] * d[nb])
+            Xn = w["X"][nb].astype(np.float64)
+            z = a @ (Xn @ W1)
+            lim = 2e-3 * (a @ (np.abs(Xn) @ np.abs(W1))) + 2.0 ** -11 * np.abs(z) + 1e-30
+            assert np.all(np.abs(h[:cfg.dims[1]] - np.maximum(z, 0)) <= lim), f"rank {r['rank']} row {u}"
+        assert crossing >= len(r["rows"]) // 2   # the sample exercises the pulled ghost rows
+    Z, _ = oracle.forward(g, w["X"], Ws, bs)
+    ref_loss, _ = oracle.softmax_ce(Z, w["y"])
+    assert abs(res[0]["loss1"] - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss)), (res[0]["loss1"], ref_loss)
