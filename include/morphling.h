@@ -59,6 +59,14 @@ extern "C" {
 
 int mph_version(void);
 const char* mph_last_error(void);
+/* library-internal device memory (CSR, plans, activations, workspaces) from a
+ * caller allocator, e.g. torch's caching allocator; alloc(bytes, stream, ctx) returns a device
+ * pointer or NULL, release(ptr, bytes, stream, ctx) takes it back (stream = the default stream).
+ * NULL callbacks restore cudaMalloc / cudaFree.  Memory is released through whichever allocator
+ * provided it.  The peer-mapped arena of a MPH_COMM_P2P model always comes from cudaMalloc
+ * (CUDA IPC needs it).  Not thread-safe against concurrent mph_* calls. */
+int mph_set_allocator(void* (*alloc)(size_t bytes, void* stream, void* ctx),
+                      void (*release)(void* ptr, size_t bytes, void* stream, void* ctx), void* ctx);
 /* Number of CUDA kernels this library has launched since it was loaded (bench accounting). */
 int mph_launch_count(int64_t* count_h);
 /* Resets the calling thread's error message; returns MPH_ECUDA unless an sm_100 device is present. */
@@ -200,6 +208,14 @@ int mph_gemm_nt(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, 
  *   C[M, N] = A[K, M]^T · B[K, N]    (A, B row-major; K = nodes)
  * Deterministic split-K: per-CTA FP32 partials in `ws_d`, reduced in a fixed order. */
 int mph_gemm_tn_workspace(int32_t M, int32_t N, int32_t K, size_t* bytes_h);
+/* SURVEY §8(b) generic form: C = op(A)·op(B) for the two shapes of the GCN path —
+ * (transA, transB) = (0, 1): mph_gemm_nt with the epilogue flags RELU / TF32 (those needing no
+ * operand pointer); (1, 0): mph_gemm_tn (workspace allocated and freed stream-ordered, flags
+ * must be 0).  precision: 0 = TF32 (the only one implemented; 1 = BF16 -> MPH_ENOTSUP).
+ * Other transpose combinations: MPH_ENOTSUP. */
+int mph_gemm(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, int32_t transA, const float* B_d,
+             int32_t ldb, int32_t transB, float* C_d, int32_t ldc, int32_t precision, uint32_t epilogue_flags,
+             void* stream);
 int mph_gemm_tn(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, const float* B_d, int32_t ldb,
                 float* C_d, int32_t ldc, void* ws_d, size_t ws_bytes, void* stream);
 
@@ -324,6 +340,16 @@ int mph_plan_arrays(const mph_plan* p, const int64_t** ghosts_h, const int64_t**
                     const int64_t** split_h, const int32_t** deg_local_h, const int64_t** recv_offset_h,
                     const int64_t** n_recv_h, const int64_t** send_offset_h, const int32_t** send_ids_h);
 int mph_plan_destroy(mph_plan* p);
+/* SURVEY §8(b) mph_graph_localize: G2L + halo plan of `rank` straight from a global graph
+ * (copies its CSR to the host, mph_plan_create, mph_graph_from_plan).  bounds_h: world+1 row
+ * bounds (mph_partition_1d / mph_relabel).  Synchronises. */
+int mph_graph_localize(const mph_graph* global, const int64_t* bounds_h, int32_t world, int32_t rank, void* stream,
+                       mph_graph** local_out);
+/* SURVEY §8(b) mph_halo_plan, for tests / inspection of a localized graph: the owned local row
+ * ids this rank sends to `peer` (device, borrowed), their count, and where `peer`'s rows land
+ * in the ghost slice (recv offset from n_rows, count). */
+int mph_halo_plan(const mph_graph* local, int32_t peer, const int32_t** send_local_ids_d, int64_t* n_send_h,
+                  int64_t* recv_offset_h, int64_t* n_recv_h);
 /* Upload a plan as a localized graph (dinv by the G6 recipe from deg_local).  Synchronises. */
 int mph_graph_from_plan(const mph_plan* p, void* stream, mph_graph** out);
 
@@ -373,6 +399,15 @@ int mph_gcn_create(const mph_graph* g, const mph_features* f, const mph_gcn_desc
  * b_l at offsets[2(l-1)+1] (ld_w[l-1] entries).  Padding entries are zero. */
 int mph_gcn_param_layout(const mph_gcn* m, int64_t* num_params_h, int64_t* offsets_h, int32_t* ld_w_h);
 int mph_gcn_buffers(const mph_gcn* m, float** params_d, float** grads_d, float** adam_m_d, float** adam_v_d);
+/* SURVEY §8(b) caller-owned state: mph_gcn_bind replaces the model's parameter / gradient /
+ * Adam-moment buffers (num_params floats each, layout of mph_gcn_param_layout) and its
+ * workspace (>= mph_gcn_workspace_size bytes) by caller-owned device memory; a NULL argument keeps
+ * the model's own buffer.  The caller's params_d becomes the model's parameters: call
+ * mph_gcn_params_updated (or mph_gcn_init_xavier) before the next epoch.  Caller buffers must
+ * outlive the model; they are never freed by it. */
+int mph_gcn_workspace_size(const mph_gcn* m, size_t* bytes_h);
+int mph_gcn_bind(mph_gcn* m, float* params_d, float* grads_d, float* adam_m_d, float* adam_v_d, void* workspace_d,
+                 size_t ws_bytes);
 /* initializeLayers("xaviers"): W by mph_xavier_fill(seed, layer = l), b = 0, m = v = 0. */
 int mph_gcn_init_xavier(mph_gcn* m, uint64_t seed, void* stream);
 /* Call after editing params_d directly (refreshes the transposed weight copies). */
@@ -392,6 +427,8 @@ int mph_gcn_forward(mph_gcn* m, int32_t epoch, void* stream);
 int mph_gcn_loss(mph_gcn* m, double* loss_d, void* stream);
 int mph_gcn_backward(mph_gcn* m, void* stream);
 int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream);
+/* SURVEY §8(b) name of the same step (optimizer("adam", ...)). */
+int mph_adam_step(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream);
 /* One epoch a2..a11: forward, loss (written to loss_d, global sum over ranks), backward,
  * gradient all-reduce (P > 1), Adam step t.  Capturable in a CUDA graph when comm == NULL. */
 int mph_gcn_train_epoch(mph_gcn* m, int32_t t, const mph_adam_cfg* cfg, double* loss_d, void* stream);

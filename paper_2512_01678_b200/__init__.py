@@ -8,8 +8,8 @@ no CPU fallback.
 from . import _lib  # noqa: F401  (raises ImportError when the library is missing)
 from .api import (Comm, Features, GCN, Graph, Plan, device_view, optimizer, pad_width,  # noqa: F401
                   partition_1d, partition_components, partition_greedy, partition_hierarchical, partition_stats,
-                  relabel, stream_ptr)
+                  relabel, stream_ptr, use_torch_allocator)
 
 __all__ = ["Comm", "Features", "GCN", "Graph", "Plan", "device_view", "optimizer", "pad_width", "partition_1d",
            "partition_components", "partition_greedy", "partition_hierarchical", "partition_stats", "relabel",
-           "stream_ptr"]
+           "stream_ptr", "use_torch_allocator"]

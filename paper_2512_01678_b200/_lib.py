@@ -134,6 +134,13 @@ _SIGS = {
     "mph_gcn_graph_state": [P, PP, PP],
     "mph_gcn_tensor": [P, i32, i32, PP, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
     "mph_gcn_info": [P, P, C.POINTER(i32)],
+    "mph_set_allocator": [P, P, P],
+    "mph_graph_localize": [P, P, i32, i32, P, PP],
+    "mph_halo_plan": [P, i32, PP, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)],
+    "mph_gemm": [i32, i32, i32, P, i32, i32, P, i32, i32, P, i32, i32, C.c_uint32, P],
+    "mph_gcn_workspace_size": [P, C.POINTER(sz)],
+    "mph_gcn_bind": [P, P, P, P, P, P, sz],
+    "mph_adam_step": [P, C.POINTER(AdamCfg), i32, P],
     "mph_gcn_p2p_export": [P, P],
     "mph_gcn_p2p_open": [P, P, i32, P],
     "mph_gcn_p2p_status": [P, C.POINTER(i32), C.POINTER(i64), P],

@@ -81,6 +81,22 @@ class Graph:
         g.world, g.rank = plan.world, plan.rank
         return g
 
+    def localize(self, bounds: np.ndarray, rank: int, stream=None) -> "Graph":
+        """mph_graph_localize: rank's owned+ghost view of this global graph (D1-D4)."""
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        h = _out_ptr()
+        L.mph_graph_localize(self.h, b.ctypes.data, int(b.size - 1), int(rank), stream_ptr(stream), C.byref(h))
+        g = Graph(_handle=h)
+        g.world, g.rank = int(b.size - 1), int(rank)
+        return g
+
+    def halo_plan(self, peer: int) -> dict:
+        """mph_halo_plan of a localized graph: send ids (device view), recv offset and count."""
+        ids, ns, ro, nr = C.c_void_p(), C.c_int64(), C.c_int64(), C.c_int64()
+        L.mph_halo_plan(self.h, int(peer), C.byref(ids), C.byref(ns), C.byref(ro), C.byref(nr))
+        return {"send_ids": device_view(ids.value, (ns.value,), torch.int32), "recv_offset": ro.value,
+                "n_recv": nr.value}
+
     def csr(self):
         rp, ci, dg, di = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
         L.mph_graph_csr(self.h, C.byref(rp), C.byref(ci), C.byref(dg), C.byref(di))
@@ -262,6 +278,33 @@ class Plan:
             self.h = None
 
 
+_ALLOC_T = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_RELEASE_T = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_torch_alloc_state = {}
+
+
+def use_torch_allocator(on: bool = True) -> dict:
+    """Route the library's internal device allocations through torch's caching allocator
+    (mph_set_allocator); returns the live-allocation table {ptr: tensor} for inspection."""
+    if not on:
+        L.mph_set_allocator(None, None, None)
+        return _torch_alloc_state.setdefault("live", {})
+    live = _torch_alloc_state.setdefault("live", {})
+
+    def alloc(nbytes, stream, ctx):
+        t = torch.empty(int(nbytes), dtype=torch.uint8, device="cuda")
+        live[t.data_ptr()] = t
+        return t.data_ptr()
+
+    def release(ptr, nbytes, stream, ctx):
+        live.pop(int(ptr), None)
+
+    cbs = (_ALLOC_T(alloc), _RELEASE_T(release))
+    _torch_alloc_state["cbs"] = cbs   # the callbacks must outlive their registration
+    L.mph_set_allocator(C.cast(cbs[0], C.c_void_p), C.cast(cbs[1], C.c_void_p), None)
+    return live
+
+
 def partition_1d(row_ptr: np.ndarray, world: int) -> np.ndarray:
     rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
     out = np.zeros(world + 1, dtype=np.int64)
@@ -387,6 +430,30 @@ class GCN:
 
     def grads(self):
         return self._views(self.grads_flat)
+
+    def workspace_size(self) -> int:
+        b = C.c_size_t()
+        L.mph_gcn_workspace_size(self.h, C.byref(b))
+        return b.value
+
+    def bind(self, params=None, grads=None, adam_m=None, adam_v=None, workspace=None):
+        """mph_gcn_bind: caller-owned (torch) buffers for the parameters, gradients, Adam moments
+        and workspace; None keeps the model's own.  Refresh with params_updated()/init_xavier()."""
+        def ptr(t, n_floats=None):
+            if t is None:
+                return None
+            assert t.is_cuda and t.is_contiguous()
+            if n_floats is not None:
+                assert t.dtype == torch.float32 and t.numel() >= n_floats
+            return t.data_ptr()
+        ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        L.mph_gcn_bind(self.h, ptr(params, self.num_params), ptr(grads, self.num_params), ptr(adam_m, self.num_params),
+                       ptr(adam_v, self.num_params), ptr(workspace), ws_bytes)
+        self._bound = (params, grads, adam_m, adam_v, workspace)   # keep alive
+        ptrs = [C.c_void_p() for _ in range(4)]
+        L.mph_gcn_buffers(self.h, *[C.byref(p) for p in ptrs])
+        self.params_flat, self.grads_flat, self.adam_m, self.adam_v = (
+            device_view(p.value, (self.num_params,), torch.float32) for p in ptrs)
 
     def init_xavier(self, seed: int = 42, stream=None):
         L.mph_gcn_init_xavier(self.h, int(seed), stream_ptr(stream))

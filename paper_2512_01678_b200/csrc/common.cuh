@@ -46,19 +46,18 @@ inline int round_up(int a, int b) { return (a + b - 1) / b * b; }
 // (SURVEY §8 "Per-config shapes"; padded columns are exactly zero, Q26).
 inline int pad_width(int w) { return w <= 4 ? 4 : round_up(w, 8); }
 
-// Device memory: plain cudaMalloc; the library owns what it allocates (include/morphling.h).
+// Device memory: cudaMalloc, or the caller's allocator when one is registered
+// (mph_set_allocator); the library owns what it allocates (include/morphling.h).
+int dev_alloc_bytes(void** p, size_t bytes);
+void dev_free(void* p);
 template <class T>
 int dev_alloc(T** p, size_t count) {
   *p = nullptr;
   if (count == 0) return MPH_OK;
-  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
-  if (e != cudaSuccess)
-    return fail(e == cudaErrorMemoryAllocation ? MPH_ENOMEM : MPH_ECUDA, "cudaMalloc(%zu B): %s", count * sizeof(T),
-                cudaGetErrorString(e));
+  void* q = nullptr;
+  MPH_TRY(dev_alloc_bytes(&q, count * sizeof(T)));
+  *p = static_cast<T*>(q);
   return MPH_OK;
-}
-inline void dev_free(void* p) {
-  if (p) cudaFree(p);
 }
 
 // Kernel launch counter (bench.py reports gpu_launches from it).

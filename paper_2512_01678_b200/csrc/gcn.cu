@@ -52,6 +52,7 @@ struct mph_gcn {
   const float *fpre = nullptr, *fpost = nullptr, *bpre = nullptr, *bpost = nullptr;
   std::vector<Layer> layers;
   float *params = nullptr, *grads = nullptr, *m = nullptr, *v = nullptr, *wt = nullptr;
+  bool own_params = true, own_grads = true, own_m = true, own_v = true, own_ws = true;  // mph_gcn_bind
   float* wr = nullptr;  // TF32-rounded copy of the W segments (B operand of the dH GEMM)
   float* Xr = nullptr;  // TF32-rounded copy of X (A operand of a dense transform-first layer 1)
   int64_t n_params = 0, n_wt = 0;
@@ -101,15 +102,15 @@ static void gcn_free(mph_gcn* m) {
     dev_free(l.arg);
     dev_free(l.dY);
   }
-  dev_free(m->params);
-  dev_free(m->grads);
-  dev_free(m->m);
-  dev_free(m->v);
+  if (m->own_params) dev_free(m->params);
+  if (m->own_grads) dev_free(m->grads);
+  if (m->own_m) dev_free(m->m);
+  if (m->own_v) dev_free(m->v);
   dev_free(m->wt);
   dev_free(m->wr);
   dev_free(m->Xr);
   if (!in_arena(m, m->Xs)) dev_free(m->Xs);
-  dev_free(m->ws);
+  if (m->own_ws) dev_free(m->ws);
   for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss, m->ev_copied, m->ev_derived})
     if (e) cudaEventDestroy(e);
   if (m->cs) cudaStreamDestroy(m->cs);
@@ -582,6 +583,39 @@ extern "C" int mph_gcn_buffers(const mph_gcn* m, float** params_d, float** grads
   return MPH_OK;
 }
 
+extern "C" int mph_gcn_workspace_size(const mph_gcn* m, size_t* bytes_h) {
+  if (!m || !bytes_h) return fail(MPH_EINVAL, "gcn_workspace_size arguments");
+  *bytes_h = m->ws_bytes;
+  return MPH_OK;
+}
+
+extern "C" int mph_gcn_bind(mph_gcn* m, float* params_d, float* grads_d, float* adam_m_d, float* adam_v_d,
+                            void* workspace_d, size_t ws_bytes) {
+  if (!m) return fail(MPH_EINVAL, "null model");
+  if (workspace_d && ws_bytes < m->ws_bytes)
+    return fail(MPH_EINVAL, "gcn_bind: workspace %zu B < mph_gcn_workspace_size %zu B", ws_bytes, m->ws_bytes);
+  for (const void* p : {(const void*)params_d, (const void*)grads_d, (const void*)adam_m_d, (const void*)adam_v_d})
+    if (p && (reinterpret_cast<uintptr_t>(p) & 15)) return fail(MPH_EINVAL, "gcn_bind: buffers must be 16-byte aligned");
+  if (m->graph_exec) return fail(MPH_ESTATE, "gcn_bind: a captured CUDA graph holds the old buffers");
+  MPH_CUDA_TRY(cudaDeviceSynchronize());  // nothing in flight still uses the buffers being replaced
+  auto swap = [](float*& cur, bool& own, float* nw) {
+    if (!nw) return;
+    if (own) dev_free(cur);
+    cur = nw;
+    own = false;
+  };
+  swap(m->params, m->own_params, params_d);
+  swap(m->grads, m->own_grads, grads_d);
+  swap(m->m, m->own_m, adam_m_d);
+  swap(m->v, m->own_v, adam_v_d);
+  if (workspace_d) {
+    if (m->own_ws) dev_free(m->ws);
+    m->ws = workspace_d;
+    m->own_ws = false;
+  }
+  return MPH_OK;
+}
+
 extern "C" int mph_gcn_init_xavier(mph_gcn* m, uint64_t seed, void* stream) {
   if (!m) return fail(MPH_EINVAL, "null model");
   cudaStream_t s = (cudaStream_t)stream;
@@ -729,6 +763,10 @@ extern "C" int mph_gcn_adam(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void
   if (!m || !cfg) return fail(MPH_EINVAL, "gcn_adam arguments");
   const mph_optim_cfg o = as_optim(cfg);
   return mph_gcn_optim_step(m, &o, t, stream);
+}
+
+extern "C" int mph_adam_step(mph_gcn* m, const mph_adam_cfg* cfg, int32_t t, void* stream) {
+  return mph_gcn_adam(m, cfg, t, stream);
 }
 
 extern "C" int mph_gcn_train_epoch_opt(mph_gcn* m, int32_t t, const mph_optim_cfg* cfg, double* loss_d, void* stream) {

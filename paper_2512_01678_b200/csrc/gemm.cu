@@ -387,3 +387,30 @@ extern "C" int mph_reduce_rows(const float* in_d, int32_t rows, int32_t cols, in
                                int32_t accumulate, void* stream) {
   return mph::reduce_rows_launch(in_d, rows, cols, ld, out_d, accumulate, (cudaStream_t)stream);
 }
+
+extern "C" int mph_gemm(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, int32_t transA,
+                        const float* B_d, int32_t ldb, int32_t transB, float* C_d, int32_t ldc, int32_t precision,
+                        uint32_t epilogue_flags, void* stream) {
+  using namespace mph;
+  if (precision != 0) return fail(MPH_ENOTSUP, "mph_gemm: precision %d (only 0 = TF32 is implemented)", precision);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (transA == 0 && transB == 1) {
+    if (epilogue_flags & ~(uint32_t)(MPH_EPI_RELU | MPH_EPI_TF32))
+      return fail(MPH_EINVAL, "mph_gemm: flags 0x%x need operands (use mph_gemm_nt)", epilogue_flags);
+    mph_epilogue e{};
+    e.flags = epilogue_flags;
+    e.mask_scale = 1.0f;
+    return gemm_nt_launch(M, N, K, A_d, lda, B_d, ldb, C_d, ldc, &e, s);
+  }
+  if (transA == 1 && transB == 0) {
+    if (epilogue_flags) return fail(MPH_EINVAL, "mph_gemm: no epilogue on the transposed-A shape");
+    const size_t ws_bytes = gemm_tn_ws_bytes(M, N, K);
+    void* ws = nullptr;
+    if (ws_bytes) MPH_CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
+    const int rc = gemm_tn_launch(M, N, K, A_d, lda, B_d, ldb, C_d, ldc, ws, ws_bytes, s);
+    if (ws) cudaFreeAsync(ws, s);
+    return rc;
+  }
+  return fail(MPH_ENOTSUP, "mph_gemm: (transA, transB) = (%d, %d); the GCN path uses (0, 1) and (1, 0)", transA,
+              transB);
+}

@@ -467,3 +467,35 @@ extern "C" int mph_graph_from_plan(const mph_plan* p, void* stream, mph_graph** 
   *out = g;
   return MPH_OK;
 }
+
+extern "C" int mph_graph_localize(const mph_graph* global, const int64_t* bounds_h, int32_t world, int32_t rank,
+                                  void* stream, mph_graph** local_out) {
+  if (!global || !bounds_h || !local_out || world < 1 || rank < 0 || rank >= world)
+    return fail(MPH_EINVAL, "graph_localize arguments");
+  if (global->local) return fail(MPH_EINVAL, "graph_localize: the input is already a localized graph");
+  *local_out = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int64_t> rp((size_t)global->n_rows + 1);
+  std::vector<int32_t> ci((size_t)global->nnz);
+  MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), global->row_ptr, rp.size() * 8, cudaMemcpyDeviceToHost, s));
+  if (global->nnz)
+    MPH_CUDA_TRY(cudaMemcpyAsync(ci.data(), global->col_idx, ci.size() * 4, cudaMemcpyDeviceToHost, s));
+  MPH_CUDA_TRY(cudaStreamSynchronize(s));
+  mph_plan* p = nullptr;
+  MPH_TRY(mph_plan_create(rp.data(), ci.data(), global->n_rows, bounds_h, world, rank, &p));
+  const int rc = mph_graph_from_plan(p, stream, local_out);
+  mph_plan_destroy(p);
+  return rc;
+}
+
+extern "C" int mph_halo_plan(const mph_graph* g, int32_t peer, const int32_t** send_local_ids_d, int64_t* n_send_h,
+                             int64_t* recv_offset_h, int64_t* n_recv_h) {
+  if (!g || !g->local) return fail(MPH_EINVAL, "halo_plan: needs a localized graph");
+  if (peer < 0 || peer >= g->world) return fail(MPH_EINVAL, "halo_plan: peer %d outside [0, %d)", peer, g->world);
+  const int64_t s0 = g->send_offset[peer], s1 = g->send_offset[peer + 1];
+  if (send_local_ids_d) *send_local_ids_d = g->send_ids ? g->send_ids + s0 : nullptr;
+  if (n_send_h) *n_send_h = s1 - s0;
+  if (recv_offset_h) *recv_offset_h = g->recv_offset[peer];
+  if (n_recv_h) *n_recv_h = g->n_recv[peer];
+  return MPH_OK;
+}
