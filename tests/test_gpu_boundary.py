@@ -54,7 +54,8 @@ def test_mph_gemm_generic(P, M, N, K):
     Bt = rng.standard_normal((N, K)).astype(np.float32)
     s = torch.cuda.current_stream().cuda_stream
     c = torch.zeros((M, N), device="cuda")
-    mph_gemm(M, N, K, cuda(A).data_ptr(), K, 0, cuda(Bt).data_ptr(), K, 1, c.data_ptr(), N, 0, 0, s)
+    a_d, bt_d = cuda(A), cuda(Bt)   # keep the device inputs alive across the asynchronous call
+    mph_gemm(M, N, K, a_d.data_ptr(), K, 0, bt_d.data_ptr(), K, 1, c.data_ptr(), N, 0, 0, s)
     torch.cuda.synchronize()
     assert_gemm_close(c.cpu().numpy(), A, Bt.T, what="mph_gemm NT")
     # transposed-A shape: C[M2, N2] = A2[K2, M2]^T B2[K2, N2] (contraction over K2 = "nodes")
@@ -62,13 +63,13 @@ def test_mph_gemm_generic(P, M, N, K):
     A2 = rng.standard_normal((K2, M2)).astype(np.float32)
     B2 = rng.standard_normal((K2, N2)).astype(np.float32)
     c2 = torch.zeros((M2, N2), device="cuda")
-    mph_gemm(M2, N2, K2, cuda(A2).data_ptr(), M2, 1, cuda(B2).data_ptr(), N2, 0, c2.data_ptr(), N2, 0, 0, s)
+    a2_d, b2_d = cuda(A2), cuda(B2)
+    mph_gemm(M2, N2, K2, a2_d.data_ptr(), M2, 1, b2_d.data_ptr(), N2, 0, c2.data_ptr(), N2, 0, 0, s)
     torch.cuda.synchronize()
     assert_gemm_close(c2.cpu().numpy(), A2.T, B2, what="mph_gemm TN")
     for bad in ((0, 0, 0), (1, 1, 0), (0, 1, 1)):   # (transA, transB, precision)
         with pytest.raises(MorphlingError) as e:
-            mph_gemm(M, N, K, cuda(A).data_ptr(), K, bad[0], cuda(Bt).data_ptr(), K, bad[1], c.data_ptr(), N,
-                     bad[2], 0, s)
+            mph_gemm(M, N, K, a_d.data_ptr(), K, bad[0], bt_d.data_ptr(), K, bad[1], c.data_ptr(), N, bad[2], 0, s)
         assert e.value.code == -9   # MPH_ENOTSUP
 
 
