@@ -231,6 +231,13 @@ def _build_model(P, torch, w, world, rank, comm, bounds=None):
     return g, f, m, y, own, extra
 
 
+def _max_over_ranks(torch, dist, v: float) -> float:
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    tt = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return tt.item()
+
+
 def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full: bool):
     """Build one workload and time it.  full=False skips e2e and the CPU baseline (secondary)."""
     t_setup = time.perf_counter()
@@ -291,9 +298,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     L.mph_profile_enable(0)
     loss_last = m.loss_buf.item()
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = tt.item()
+        ms = _max_over_ranks(torch, dist, ms)
 
     # ---------------- end-to-end through the public API with host buffers
     e2e = None
@@ -348,9 +353,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / steps_e2e
         if world > 1:
-            tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_ms = tt.item()
+            e2e_ms = _max_over_ranks(torch, dist, e2e_ms)
         e2e = {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 4 * upload + yh.numel() * 4),
                "d2h_bytes_per_step": 8, "steps": steps_e2e,
                "inputs": "features (padded, pinned) + labels H2D and loss D2H every step; the next step's "
@@ -447,9 +450,19 @@ def run_ours(args):
     local = _env_int("LOCAL_RANK", 0)
     if world != args.gpus:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
+    if args.share_device:
+        # functional check of the N > 1 code path on a one-GPU box: every rank on cuda:0, gloo
+        # plumbing, P2P transport (ranks time-slice the GPU, so the timings mean nothing)
+        if args.comm != "p2p":
+            print("--share-device needs --comm p2p (NCCL refuses two ranks on one device)", file=sys.stderr)
+            return 2
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.share_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2512_01678_b200 as P
     from paper_2512_01678_b200 import _lib as L
@@ -502,6 +515,9 @@ def main():
     ap.add_argument("--comm", default="p2p", choices=["nccl", "p2p"],
                     help="N > 1: NVLink peer-memory halo pulls with the gradient sum fused into the optimizer "
                          "(default; SURVEY §8(f) NEXT-1), or NCCL grouped send/recv + all-reduce")
+    ap.add_argument("--share-device", action="store_true",
+                    help="testing only: run every rank on cuda:0 (gloo plumbing, --comm p2p) to exercise the "
+                         "N > 1 path on a one-GPU box; the timings are not meaningful")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the gather-bandwidth probe")
     ap.add_argument("--graph", action="store_true",
