@@ -52,6 +52,13 @@ def device_view(ptr: int, shape, dtype) -> torch.Tensor:
     return torch.as_tensor(_CAI(ptr, shape, _TYPESTR[dtype]), device="cuda")
 
 
+def _destroy(fn_name: str, h):
+    """Release a handle; a no-op during interpreter teardown (module globals already cleared)."""
+    fn = getattr(L, fn_name, None)
+    if callable(fn):
+        fn(h)
+
+
 def _out_ptr():
     return C.c_void_p()
 
@@ -120,7 +127,7 @@ class Graph:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            L.mph_graph_destroy(h)
+            _destroy("mph_graph_destroy", h)
             self.h = None
 
 
@@ -177,7 +184,7 @@ class Features:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            L.mph_features_destroy(h)
+            _destroy("mph_features_destroy", h)
             self.h = None
 
 
@@ -274,7 +281,7 @@ class Plan:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            L.mph_plan_destroy(h)
+            _destroy("mph_plan_destroy", h)
             self.h = None
 
 
@@ -338,7 +345,7 @@ class Comm:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            L.mph_comm_destroy(h)
+            _destroy("mph_comm_destroy", h)
             self.h = None
 
 
@@ -522,5 +529,5 @@ class GCN:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            L.mph_gcn_destroy(h)
+            _destroy("mph_gcn_destroy", h)
             self.h = None

@@ -21,6 +21,7 @@
 //    and a fixed xor-shuffle tree across slots.
 //  * epilogue fused: dinv, bias, ReLU, inverted dropout (Philox, Q10), row scale, TF32 store.
 #include <algorithm>
+#include <cstdio>
 #include <vector>
 
 #include "internal.cuh"
@@ -284,9 +285,34 @@ static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
   return launch_check("spmm");
 }
 
+
 static int env_int(const char* name) {
   const char* v = getenv(name);
   return v ? atoi(v) : 0;
+}
+
+// Experiment hook: MPH_SPMM_U_<LPR>_<VPL>=<n> overrides the per-round unroll U of a main shape.
+template <int LPR, int VPL, bool HAS_VAL>
+static int launch_spmm_u(const SpmmArgs& a, cudaStream_t s) {
+  char name[32];
+  snprintf(name, sizeof(name), "MPH_SPMM_U_%d_%d", LPR, VPL);
+  const int u = env_int(name);
+  if (!HAS_VAL) {
+    switch (u) {
+      case 2: return launch_spmm<LPR, VPL, HAS_VAL, 2>(a, s);
+      case 3: return launch_spmm<LPR, VPL, HAS_VAL, 3>(a, s);
+      case 4: return launch_spmm<LPR, VPL, HAS_VAL, 4>(a, s);
+      case 6: return launch_spmm<LPR, VPL, HAS_VAL, 6>(a, s);
+      case 8: return launch_spmm<LPR, VPL, HAS_VAL, 8>(a, s);
+      case 12: return launch_spmm<LPR, VPL, HAS_VAL, 12>(a, s);
+      case 16: return launch_spmm<LPR, VPL, HAS_VAL, 16>(a, s);
+      default: break;
+    }
+  }
+  // measured (tools/spmm_u_sweep.py): 256-wide rows (32 lanes x 2 float4) gain from 8 gathers
+  // in flight per slot (arxiv SpMM -8 %); every other shape is best at the default U
+  if (LPR == 32 && VPL == 2) return launch_spmm<LPR, VPL, HAS_VAL, 8>(a, s);
+  return launch_spmm<LPR, VPL, HAS_VAL>(a, s);
 }
 
 template <bool HAS_VAL>
@@ -296,10 +322,10 @@ static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
   if (nv4 <= 2) return launch_spmm<2, 1, HAS_VAL>(a, s);
   if (nv4 <= 4) return launch_spmm<4, 1, HAS_VAL>(a, s);
   if (nv4 <= 8) return launch_spmm<8, 1, HAS_VAL>(a, s);
-  if (nv4 <= 12) return launch_spmm<4, 3, HAS_VAL>(a, s);
-  if (nv4 <= 16) return launch_spmm<16, 1, HAS_VAL>(a, s);
-  if (nv4 <= 32) return launch_spmm<32, 1, HAS_VAL>(a, s);
-  if (nv4 <= 64) return launch_spmm<32, 2, HAS_VAL>(a, s);
+  if (nv4 <= 12) return launch_spmm_u<4, 3, HAS_VAL>(a, s);
+  if (nv4 <= 16) return launch_spmm_u<16, 1, HAS_VAL>(a, s);
+  if (nv4 <= 32) return launch_spmm_u<32, 1, HAS_VAL>(a, s);
+  if (nv4 <= 64) return launch_spmm_u<32, 2, HAS_VAL>(a, s);
   if (nv4 <= 96) return launch_spmm<32, 3, HAS_VAL>(a, s);
   return launch_spmm<32, 4, HAS_VAL>(a, s);
 }
