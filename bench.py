@@ -231,6 +231,47 @@ def _build_model(P, torch, w, world, rank, comm, bounds=None):
     return g, f, m, y, own, extra
 
 
+def _spmm_widths(P, m):
+    """Padded widths of one epoch's aggregation calls (forward, then backward), from the layer
+    orders of reading Q7: a transform-first layer aggregates its output width forward and
+    backward; an aggregate-first layer 1 aggregates its input width forward only."""
+    dims = m.dims
+    fwd, bwd = [], []
+    for l, o in enumerate(m.order):
+        if o == 1:
+            fwd.append(P.pad_width(dims[l]))
+        else:
+            fwd.append(P.pad_width(dims[l + 1]))
+            bwd.append(P.pad_width(dims[l + 1]))
+    return fwd + bwd[::-1]
+
+
+def _spmm_fractions(r, peak_hbm, l2_gather_gbps, l2_bytes=126 * 2 ** 20):
+    """SURVEY §8(d) d.4's three SpMM roofline fractions for one measured workload: (1) ncu DRAM
+    bytes / time / HBM peak, (2) time efficiency E = T_floor / T_measured with T_floor =
+    Σ_calls max(floor bytes / HBM, [operand <= L2] · nnz·4·w / L2-gather), (3) algorithmic
+    (no-reuse) bytes / time / HBM peak (== roofline.frac)."""
+    k = r["kernels"].get("spmm")
+    geo = r.get("_spmm_geometry")
+    if not k or not geo:
+        return None
+    n, nc, nnz = geo["n_rows"], geo["n_cols"], geo["nnz"]
+    t_floor_ms = 0.0
+    for wpad in geo["widths"]:
+        floor_bytes = 4.0 * wpad * (nc + n) + 4.0 * nnz + 8.0 * (n + 1) + 4.0 * n
+        t = floor_bytes / (peak_hbm * 1e6)
+        if l2_gather_gbps and nc * 4.0 * wpad <= l2_bytes:
+            t = max(t, nnz * 4.0 * wpad / (l2_gather_gbps * 1e6))
+        t_floor_ms += t
+    out = {"time_efficiency_E": t_floor_ms / k["ms_per_epoch"], "floor_ms_per_epoch": t_floor_ms,
+           "widths": geo["widths"], "effective_frac_of_hbm": k["algorithmic_GBps"] / peak_hbm,
+           "l2_gather_GBps_used": l2_gather_gbps}
+    traffic = (r.get("roofline") or {}).get("traffic")
+    if traffic:
+        out["dram_frac_of_hbm"] = traffic / (k["avg_launch_ms"] * 1e6) / peak_hbm
+    return out
+
+
 def _max_over_ranks(torch, dist, v: float) -> float:
     dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
     tt = torch.tensor([v], dtype=torch.float64, device=dev)
@@ -274,19 +315,23 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     time.sleep(0.15)
     barrier()
     torch.cuda.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for t in range(args.warmup + 1, args.warmup + args.steps + 1):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]   # one per epoch boundary
+    evs[0].record(stream)
+    for i, t in enumerate(range(args.warmup + 1, args.warmup + args.steps + 1)):
         if use_graph:
             m.replay()
         else:
             m.train_epoch(t)
-    ev1.record(stream)
+        evs[i + 1].record(stream)
+    ev0, ev1 = evs[0], evs[-1]
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     launches = L.launch_count() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
+    per_epoch = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+    q = lambda f: per_epoch[min(len(per_epoch) - 1, int(round(f * (len(per_epoch) - 1))))]  # noqa: E731
+    epoch_stats = {"median": q(0.5), "p10": q(0.1), "p90": q(0.9), "unit": "ms", "this_rank": True}
     kernels = {}
     for kind, name in PROF_KINDS.items():
         cnt, tms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
@@ -405,7 +450,9 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                    else "small workload: operands L2-resident across epochs (no flush)",
                    **extra},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
-        "kernels": kernels, "final_loss": loss_last,
+        "kernels": kernels, "final_loss": loss_last, "epoch_ms": epoch_stats,
+        "_spmm_geometry": {"widths": _spmm_widths(P, m), "n_rows": g.n_rows,
+                           "n_cols": g.n_cols, "nnz": g.nnz},
         "setup_s": {"generate": round(t_gen, 2), "graph_build_and_init": round(t_build, 2)},
     }
     del m, f, g
@@ -476,8 +523,16 @@ def run_ours(args):
         if cfgname and cfgname != args.config:
             r = _measure(P, L, torch, dist, C, args, cfgname, world, rank, local, comm, full=False)
             secondary[cfgname] = {k: r[k] for k in ("value", "config", "roofline", "kernels", "gpu_launches",
-                                                    "final_loss", "clocks")}
+                                                    "final_loss", "clocks", "epoch_ms", "_spmm_geometry")}
     peaks = _gather_peaks(L, torch) if (world == 1 and not args.no_probe) else None
+    peak_hbm = _peaks()[0]
+    l2g = peaks["l2_resident_64MB"] if peaks else None
+    for r in [main] + list(secondary.values()):
+        if r.get("roofline") is not None:
+            fr = _spmm_fractions(r, peak_hbm, l2g)
+            if fr:
+                r["roofline"]["spmm_fractions"] = fr
+        r.pop("_spmm_geometry", None)
     if peaks and main["roofline"] and main["roofline"]["kernel"] == "spmm":
         main["roofline"]["measured_gather_peaks_GBps"] = peaks
         main["roofline"]["frac_of_l2_gather_peak"] = main["roofline"]["achieved"] / peaks["l2_resident_64MB"]
@@ -493,6 +548,7 @@ def run_ours(args):
             "data": "synthetic", "config": main["config"], "roofline": main["roofline"],
             "cpu_baseline": main["cpu_baseline"], "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
             "clocks": main["clocks"], "kernels": main["kernels"], "final_loss": main["final_loss"],
+            "epoch_ms": main["epoch_ms"],
             "setup_s": main["setup_s"], "secondary": secondary or None,
         }
         print(json.dumps(line), flush=True)
