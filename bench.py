@@ -145,6 +145,17 @@ def _sample_desc(sample):
             f"(N={sample['n']}, nnz(A)={sample['nnz_a']}, dims={list(c.dims)}), time x{sample['k']}")
 
 
+def _config_common(args, world):
+    """The config keys both arms report (the reference arm adds how the oracle sampled it)."""
+    from synth.generate import CONFIGS
+    cfg = CONFIGS[args.config]
+    return {"workload": args.config, "nodes": cfg.num_nodes, "nnz_A": cfg.nnz_a, "dims": list(cfg.dims),
+            "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
+            "parallelism": (f"1d-row-partition x{world}" + ("" if args.partition == "1d" else
+                                                             f" ({args.partition} + relabel)") + f", comm {args.comm}")
+            if world > 1 else "single-gpu"}
+
+
 def run_reference(args):
     rank = _env_int("RANK", 0)
     if rank != 0:
@@ -159,7 +170,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "oracle_scale": f"1/{sample['k']}"},
+        "config": {**_config_common(args, args.gpus), "oracle_scale": f"1/{sample['k']}"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": _sample_desc(sample)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -438,12 +449,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
 
     out = {
         "value": ms, "ms_per_step": ms,
-        "config": {"workload": config, "nodes": cfg.num_nodes, "nnz_A": cfg.nnz_a, "dims": list(cfg.dims),
-                   "layers": cfg.num_layers, "global_batch": cfg.num_nodes, "seq_len": None,
-                   "parallelism": (f"1d-row-partition x{world}" + ("" if args.partition == "1d" else
-                                                                    f" ({args.partition} + relabel)")
-                                   + f", comm {args.comm}")
-                   if world > 1 else "single-gpu",
+        "config": {**_config_common(argparse.Namespace(**{**vars(args), "config": config}), world),
                    "layer_order": ["AF" if o else "TF" for o in m.order],
                    "cuda_graph": use_graph,
                    "l2": "inputs larger than L2 (X and col_idx > 126 MB); no flush" if cfg.num_nodes > 100000
