@@ -206,7 +206,7 @@ int mph_gemm_nt(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, 
                 float* C_d, int32_t ldc, const mph_epilogue* epi, void* stream);
 /* a7 — weight gradient (contraction over the node dimension, P:525-532 step (a)):
  *   C[M, N] = A[K, M]^T · B[K, N]    (A, B row-major; K = nodes)
- * Deterministic split-K: per-CTA FP32 partials in `ws_d`, reduced in a fixed order. */
+ * Deterministic split-K: per-CTA FP32 partials in `ws_d` (16-byte aligned), reduced in a fixed order. */
 int mph_gemm_tn_workspace(int32_t M, int32_t N, int32_t K, size_t* bytes_h);
 /* SURVEY §8(b) generic form: C = op(A)·op(B) for the two shapes of the GCN path —
  * (transA, transB) = (0, 1): mph_gemm_nt with the epilogue flags RELU / TF32 (those needing no
@@ -403,8 +403,9 @@ int mph_gcn_buffers(const mph_gcn* m, float** params_d, float** grads_d, float**
  * Adam-moment buffers (num_params floats each, layout of mph_gcn_param_layout) and its
  * workspace (>= mph_gcn_workspace_size bytes) by caller-owned device memory; a NULL argument keeps
  * the model's own buffer.  The caller's params_d becomes the model's parameters: call
- * mph_gcn_params_updated (or mph_gcn_init_xavier) before the next epoch.  Caller buffers must
- * outlive the model; they are never freed by it. */
+ * mph_gcn_params_updated (or mph_gcn_init_xavier) before the next epoch; its padding entries (and
+ * those of adam_m_d / adam_v_d) must be zero.  grads_d is zeroed here.  Synchronises.  Caller
+ * buffers must outlive the model; they are never freed by it. */
 int mph_gcn_workspace_size(const mph_gcn* m, size_t* bytes_h);
 int mph_gcn_bind(mph_gcn* m, float* params_d, float* grads_d, float* adam_m_d, float* adam_v_d, void* workspace_d,
                  size_t ws_bytes);

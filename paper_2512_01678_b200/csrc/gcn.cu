@@ -606,6 +606,8 @@ extern "C" int mph_gcn_bind(mph_gcn* m, float* params_d, float* grads_d, float* 
   };
   swap(m->params, m->own_params, params_d);
   swap(m->grads, m->own_grads, grads_d);
+  // gradient entries the kernels never write (padding) must read zero, as in the model's own buffer
+  if (grads_d) MPH_CUDA_TRY(cudaMemset(grads_d, 0, (size_t)m->n_params * sizeof(float)));
   swap(m->m, m->own_m, adam_m_d);
   swap(m->v, m->own_v, adam_v_d);
   if (workspace_d) {

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::fence_after_sync();
     }
     float* out = p.ws + ((int64_t)split * p.M + row) * p.N;
+    const bool vec = (p.N & 3) == 0;  // partial rows 16-byte aligned: float4 stores
     for (int c0 = 0; c0 < p.BN; c0 += 16) {
       float v[16];
       if (nkb > 0)
@@ -142,9 +143,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0.0f;
       if (row < p.M) {
+        if (vec) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (c0 + i < p.N) out[c0 + i] = v[i];
+          for (int j = 0; j < 4; ++j)
+            if (c0 + 4 * j < p.N)
+              reinterpret_cast<float4*>(out + c0)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < p.N) out[c0 + i] = v[i];
+        }
       }
     }
   }
@@ -176,7 +184,47 @@ __global__ void __launch_bounds__(256) k_reduce_rows(const float* in, int rows, 
   }
 }
 
-// out[r*ldc + c] = sum_s ws[(s*M + r)*N + c]   (fixed order over splits)
+// out[r*ldc + c] = sum_s ws[(s*M + r)*N + c] in a fixed order: a block owns 128 consecutive
+// outputs (32 lanes x float4), warp w sums the splits s = w, w+8, w+16, ... (two accumulators,
+// even and odd steps), then lane sums of the 8 warps are added in warp order.  Deterministic for
+// a given (splits, M, N).  Needs M*N % 4 == 0 and 16-byte aligned ws.
+__global__ void __launch_bounds__(256) k_reduce_splits4(const float* __restrict__ ws, int splits, int M, int N,
+                                                        float* __restrict__ C, int ldc) {
+  __shared__ float4 part[8][32];
+  const int64_t total4 = (int64_t)M * N / 4;
+  const int64_t t4 = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+  const int w = threadIdx.x >> 5;
+  float4 a0 = f4_zero(), a1 = f4_zero();
+  if (t4 < total4) {
+    const float4* src = reinterpret_cast<const float4*>(ws) + t4;
+    int k = w;
+    for (; k + 8 < splits; k += 16) {
+      a0 = f4_add(a0, __ldcs(src + (int64_t)k * total4));
+      a1 = f4_add(a1, __ldcs(src + (int64_t)(k + 8) * total4));
+    }
+    if (k < splits) a0 = f4_add(a0, __ldcs(src + (int64_t)k * total4));
+  }
+  part[w][threadIdx.x & 31] = f4_add(a0, a1);
+  __syncthreads();
+  if (w == 0 && t4 < total4) {
+    float4 s4 = part[0][threadIdx.x];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) s4 = f4_add(s4, part[g][threadIdx.x]);
+    const int64_t e = t4 * 4;
+    const int64_t r = e / N;
+    const int c = (int)(e - r * N);  // N % 4 == 0: the 4 outputs share a row
+    if ((ldc & 3) == 0 && ((reinterpret_cast<uintptr_t>(C) & 15) == 0)) {
+      *reinterpret_cast<float4*>(C + r * ldc + c) = s4;
+    } else {
+      C[r * ldc + c] = s4.x;
+      C[r * ldc + c + 1] = s4.y;
+      C[r * ldc + c + 2] = s4.z;
+      C[r * ldc + c + 3] = s4.w;
+    }
+  }
+}
+
+// out[r*ldc + c] = sum_s ws[(s*M + r)*N + c]   (fixed order over splits; any N)
 __global__ void k_reduce_splits(const float* ws, int splits, int M, int N, float* C, int ldc) {
   const int64_t total = (int64_t)M * N;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -323,6 +371,7 @@ int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B,
     return fail(MPH_EINVAL, "gemm_tn: A and B must be 16-byte aligned");
   const size_t need = gemm_tn_ws_bytes(M, N, K);
   if (!ws || ws_bytes < need) return fail(MPH_EINVAL, "gemm_tn: workspace %zu < %zu bytes", ws_bytes, need);
+  if (reinterpret_cast<uintptr_t>(ws) & 15) return fail(MPH_EINVAL, "gemm_tn: workspace must be 16-byte aligned");
   const int BN = round_up(N, 32);
   TnParams p{};
   p.M = M;
@@ -353,7 +402,11 @@ int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B,
   count_launch();
   MPH_TRY(launch_check("gemm_tn"));
   const int64_t total = (int64_t)M * N;
-  k_reduce_splits<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, s>>>(p.ws, splits, M, N, C, ldc);
+  if (N % 4 == 0)
+    k_reduce_splits4<<<(unsigned)ceil_div(total / 4, 32), 256, 0, s>>>(p.ws, splits, M, N, C, ldc);
+  else
+    k_reduce_splits<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, s>>>(p.ws, splits, M, N, C,
+                                                                                              ldc);
   count_launch();
   return launch_check("reduce_splits");
 }
