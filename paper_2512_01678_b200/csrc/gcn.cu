@@ -188,11 +188,11 @@ static int grad_allreduce_async(mph_gcn* m, int li, cudaStream_t s) {
   return mph_allreduce_sum(m->comm, m->grads + a, b - a, 0, m->cs);
 }
 static int gemm_nt_p(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
-                     const mph_epilogue* e, cudaStream_t s) {
+                     const mph_epilogue* e, cudaStream_t s, int colsum_fill = 1) {
   double extra = (e && (e->flags & MPH_EPI_MASK)) ? 4.0 * M * N : 0.0;
   prof::Scope sc(MPH_PROF_GEMM_NT, s, 4.0 * ((double)M * K + (double)N * K + (double)M * N) + extra,
                  2.0 * M * N * K);
-  return gemm_nt_launch(M, N, K, A, lda, Bt, ldb, C, ldc, e, s);
+  return gemm_nt_launch(M, N, K, A, lda, Bt, ldb, C, ldc, e, s, colsum_fill);
 }
 static int gemm_tn_p(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
                      void* ws, size_t wsb, cudaStream_t s) {
@@ -364,8 +364,10 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       ed.colsum_out = pl.colsum;
       ed.row_scale = m->bpre;
       MPH_TRY(gemm_nt_p(g->n_rows, pl.pout, l.pout, Gsrc, l.pout, m->wr + l.off_w, l.pout, pl.dZ, pl.pout, &ed,
-                        s));
-      MPH_TRY(reduce_rows_launch(pl.colsum, (int)ceil_div(g->n_rows, 128), pl.pout, pl.pout, m->grads + pl.off_b, 0, s));
+                        s, /*colsum_fill=*/0));
+      // db_{l-1}: the GEMM wrote one column-sum row per persistent CTA
+      MPH_TRY(reduce_rows_launch(pl.colsum, gemm_nt_colsum_rows(g->n_rows), pl.pout, pl.pout, m->grads + pl.off_b, 0,
+                                 s));
     }
   }
   if (m->world > 1) {  // Adam needs every summed gradient segment

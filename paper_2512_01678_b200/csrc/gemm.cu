@@ -283,8 +283,22 @@ int gemm_tn_splits(int M, int N, int K) {
 
 }  // namespace
 
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+// Rows of colsum partials a launch writes when not zero-filling: one per persistent CTA.
+int gemm_nt_colsum_rows(int M) { return (int)std::min<int64_t>(ceil_div(M, kBM), sm_count()); }
+
 int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
-                   const mph_epilogue* epi, cudaStream_t s) {
+                   const mph_epilogue* epi, cudaStream_t s, int colsum_fill) {
   if (M < 0 || N <= 0 || K < 0 || !A || !Bt || !C) return fail(MPH_EINVAL, "gemm_nt: bad arguments");
   if (N > 256) return fail(MPH_ENOTSUP, "gemm_nt: N=%d > 256", N);
   if (lda % 4 || ldb % 4 || ldc % 4 || lda < K || ldb < K || ldc < N)
@@ -299,13 +313,7 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
     return fail(MPH_EINVAL, "gemm_nt: mask_src must be 16-byte aligned with ld_mask %% 4 == 0, >= N");
   if ((flags & MPH_EPI_COLSUM) && !epi->colsum_out) return fail(MPH_EINVAL, "gemm_nt: null colsum_out");
   if (M == 0) return MPH_OK;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = sm_count();
   const int BN = round_up(N, 32);
   NtParams p{};
   p.M = M;
@@ -314,7 +322,7 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
   p.BN = BN;
   p.num_kb = (int)ceil_div(K, kBK);
   p.n_tiles = (int)ceil_div(M, kBM);
-  p.colsum_rows = p.n_tiles;
+  p.colsum_rows = colsum_fill ? p.n_tiles : 0;  // rows beyond the grid are zero-filled only for the ABI
   const size_t stage_bytes = kATileBytes + (size_t)BN * kBK * 4;
   // small K: the mainloop is short and the epilogue (C tile out, mask tile in) is the long pole,
   // so it gets 8 warps; otherwise 4 warps leave room for a deeper operand ring

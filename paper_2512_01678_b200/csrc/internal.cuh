@@ -146,8 +146,11 @@ int halo_sendrecv(const mph_graph* g, mph_comm* c, float* buf, int w, int ld, cu
 // Halo pack (spmm.cu): send_buf[j] = buf[send_ids[j]] for the whole send list.
 int pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int w, float* out, cudaStream_t s);
 
+// colsum_fill: 1 = the ABI contract (colsum_out has ceil(M/128) rows, the ones no CTA owns are
+// zero-filled); 0 = only the first gemm_nt_colsum_rows(M) rows are written (internal callers).
 int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
-                   const mph_epilogue* epi, cudaStream_t s);
+                   const mph_epilogue* epi, cudaStream_t s, int colsum_fill = 1);
+int gemm_nt_colsum_rows(int M);
 size_t gemm_tn_ws_bytes(int M, int N, int K);
 int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
                    void* ws, size_t ws_bytes, cudaStream_t s);
