@@ -49,6 +49,7 @@ struct SpmmArgs {
   int* counter;
   int n_items;
   int ld_in, ld_out, n_rows, nv4, part;
+  int row_slots;  // 1: narrow rows of a low-degree graph -> k_spmm_rows
   EpiDev epi;
 };
 
@@ -60,6 +61,53 @@ __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int6
   v.z = r.v[2] >= d.threshold ? v.z * d.scale : 0.0f;
   v.w = r.v[3] >= d.threshold ? v.w * d.scale : 0.0f;
   return v;
+}
+
+// Fused epilogue of one aggregated row: the LPR lanes of a slot hold acc[j] = columns
+// 4·(sub + j·LPR) .. +3.  part 0 stores raw sums; part 1 adds them to part 0's; then dinv, bias,
+// ReLU, dropout, row scale, TF32 (Q1, Q6, Q8, Q10).
+constexpr int64_t kRowSlotMaxDegree = 32;  // mean degree (incl. self loop) below which k_spmm_rows serves w <= 64
+
+template <int LPR, int VPL>
+__device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, const float4 (&acc)[VPL], float du,
+                                          float rs, uint64_t pol) {
+  float4* orow = reinterpret_cast<float4*>(a.out + (int64_t)row * a.ld_out);
+  if (a.part == 0) {
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+      if (sub + j * LPR < a.nv4) orow[sub + j * LPR] = acc[j];
+    return;
+  }
+  const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int c4 = sub + j * LPR;
+    if (c4 >= a.nv4) continue;
+    float4 v = acc[j];
+    if (a.part == 1) v = f4_add(v, orow[c4]);
+    v.x *= du;
+    v.y *= du;
+    v.z *= du;
+    v.w *= du;
+    if (a.epi.flags & MPH_EPI_BIAS) {
+      float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
+      v = f4_add(v, b);
+    }
+    if (a.epi.flags & MPH_EPI_RELU) {
+      v.x = fmaxf(v.x, 0.0f);
+      v.y = fmaxf(v.y, 0.0f);
+      v.z = fmaxf(v.z, 0.0f);
+      v.w = fmaxf(v.w, 0.0f);
+    }
+    if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, a.epi.c4_0 + c4);
+    if (a.epi.flags & MPH_EPI_ROWSCALE) {
+      v.x *= rs;
+      v.y *= rs;
+      v.z *= rs;
+      v.w *= rs;
+    }
+    st_f4_hint(orow + c4, to_tf32 ? f4_tf32(v) : v, pol);
+  }
 }
 
 template <int LPR, int VPL, bool HAS_VAL, int UOV>
@@ -126,45 +174,9 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
       acc[j].w += __shfl_xor_sync(0xffffffffu, acc[j].w, off);
     }
   if (slot != 0) return;
-  float4* orow = reinterpret_cast<float4*>(a.out + (int64_t)row * a.ld_out);
-  if (a.part == 0) {
-#pragma unroll
-    for (int j = 0; j < VPL; ++j)
-      if (sub + j * LPR < a.nv4) orow[sub + j * LPR] = acc[j];
-    return;
-  }
-  const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
-  const float du = a.dinv ? a.dinv[row] : 1.0f;
-  const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[row] : 1.0f;
-#pragma unroll
-  for (int j = 0; j < VPL; ++j) {
-    const int c4 = sub + j * LPR;
-    if (c4 >= a.nv4) continue;
-    float4 v = acc[j];
-    if (a.part == 1) v = f4_add(v, orow[c4]);
-    v.x *= du;
-    v.y *= du;
-    v.z *= du;
-    v.w *= du;
-    if (a.epi.flags & MPH_EPI_BIAS) {
-      float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
-      v = f4_add(v, b);
-    }
-    if (a.epi.flags & MPH_EPI_RELU) {
-      v.x = fmaxf(v.x, 0.0f);
-      v.y = fmaxf(v.y, 0.0f);
-      v.z = fmaxf(v.z, 0.0f);
-      v.w = fmaxf(v.w, 0.0f);
-    }
-    if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, a.epi.c4_0 + c4);
-    if (a.epi.flags & MPH_EPI_ROWSCALE) {
-      v.x *= rs;
-      v.y *= rs;
-      v.z *= rs;
-      v.w *= rs;
-    }
-    st_f4_hint(orow + c4, to_tf32 ? f4_tf32(v) : v, pol);
-  }
+  const float du = (a.part != 0 && a.dinv) ? a.dinv[row] : 1.0f;
+  const float rs = (a.part != 0 && (a.epi.flags & MPH_EPI_ROWSCALE)) ? a.epi.row_scale[row] : 1.0f;
+  store_row<LPR, VPL>(a, row, sub, acc, du, rs, pol);
 }
 
 template <int LPR, int VPL, bool HAS_VAL, int UOV>
@@ -177,6 +189,129 @@ __global__ void __launch_bounds__(256, 3) k_spmm(SpmmArgs a) {
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
     for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL, HAS_VAL, UOV>(a, row, lane);
+  }
+}
+
+// Row-slot variant for narrow rows on low-degree graphs (arxiv; products at w <= 64): the
+// warp-per-row kernel spends its 32/LPR edge slots on ONE row, so a row of ~8-26 edges costs a
+// row_ptr, an id and one or two gather latencies with most slots idle.  Here each slot of LPR
+// lanes owns whole rows and the ES = 32/LPR slots of a warp work on ES different rows of the item
+// at once.  A slot about to finish its row (last step) claims the item's next unclaimed row in the
+// same step (claims in slot order through a ballot; the item's row bounds come from one coalesced
+// load per 32 rows held across the warp's lanes), and loads that row's first neighbour ids, so
+// its next step gathers immediately.  Per step a slot gathers U neighbours (U·VPL independent
+// 16-byte loads per lane) whose ids were loaded one step earlier.  Every row is summed by one
+// slot in edge order (pairwise tree per group of U): deterministic whatever the claim order.
+template <int LPR, int VPL, int U>
+__global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
+  constexpr int ES = 32 / LPR;
+  constexpr int NID = (U + LPR - 1) / LPR;  // id registers per lane
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, slot = lane / LPR, sub = lane % LPR;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const uint64_t pol = l2_policy_evict_first();
+  const bool scaled = a.part != 0;
+  while (true) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(a.counter, 1);
+    it = __shfl_sync(FULL, it, 0);
+    if (it >= a.n_items) break;
+    const int2 rr = a.items[it];
+    int w0 = rr.x;  // row bounds window: lane i holds [ws, we) of row w0 + i
+    int64_t ws = 0, we = 0;
+    {
+      const int r = w0 + lane;
+      if (r < rr.y) {
+        ws = __ldg(a.row_ptr + r);
+        we = __ldg(a.row_ptr + r + 1);
+        if (a.part == 0) we = __ldg(a.split + r);
+        if (a.part == 1) ws = __ldg(a.split + r);
+      }
+    }
+    int next = rr.x;
+    int row = -1;  // this slot's current row (identical across the slot's lanes)
+    int64_t s = 0, e = 0;
+    float du = 1.0f, rs = 1.0f;
+    int ids[NID];
+#pragma unroll
+    for (int k = 0; k < NID; ++k) ids[k] = 0;
+    float4 acc[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
+    while (true) {
+      // ---- claims: slots that are idle or on their last step take the next rows
+      const bool want = row < 0 || s + U >= e;
+      const unsigned need = __ballot_sync(FULL, want && sub == 0);
+      const int n_need = __popc(need);
+      if (next < rr.y && next + n_need > w0 + 32) {  // refill the bounds window (warp-uniform)
+        w0 = next;
+        const int r = w0 + lane;
+        ws = we = 0;
+        if (r < rr.y) {
+          ws = __ldg(a.row_ptr + r);
+          we = __ldg(a.row_ptr + r + 1);
+          if (a.part == 0) we = __ldg(a.split + r);
+          if (a.part == 1) ws = __ldg(a.split + r);
+        }
+      }
+      const int avail = min(n_need, rr.y - next);
+      int claim = (want && sub == 0 && __popc(need & lt_mask) < avail) ? next + __popc(need & lt_mask) : -1;
+      claim = __shfl_sync(FULL, claim, slot * LPR);
+      next += avail;
+      const int src = claim >= 0 ? claim - w0 : 0;
+      const int64_t ns = __shfl_sync(FULL, ws, src), ne = __shfl_sync(FULL, we, src);
+      if (!__any_sync(FULL, row >= 0 || claim >= 0)) break;  // item done
+      // ---- ids for the next step: the rest of this row, or the claimed row's first edges
+      const bool cont = row >= 0 && !want;
+      const int64_t nb = cont ? s + U : ns;
+      const int64_t nend = cont ? e : ne;
+      const bool nvalid = cont || claim >= 0;
+      int nids[NID];
+#pragma unroll
+      for (int k = 0; k < NID; ++k) {
+        const int64_t ei = nb + sub + (int64_t)k * LPR;
+        nids[k] = (nvalid && ei < nend && sub + k * LPR < U) ? ldg_stream_i32_hint(a.col + ei, pol) : 0;
+      }
+      const float ndu = (claim >= 0 && scaled && a.dinv) ? __ldg(a.dinv + claim) : 1.0f;
+      const float nrs = (claim >= 0 && scaled && (a.epi.flags & MPH_EPI_ROWSCALE)) ? __ldg(a.epi.row_scale + claim)
+                                                                                   : 1.0f;
+      // ---- this step's gathers: U neighbours of the current row
+      float4 x[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = __shfl_sync(FULL, ids[u / LPR], slot * LPR + (u % LPR));
+        const bool valid = row >= 0 && s + u < e;
+        const float4* p = reinterpret_cast<const float4*>(a.in + (int64_t)c * a.ld_in) + sub;
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) x[u][j] = (valid && sub + j * LPR < a.nv4) ? ldg_f4(p + j * LPR) : f4_zero();
+      }
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+#pragma unroll
+        for (int w = 1; w < U; w <<= 1)
+#pragma unroll
+          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add(x[uu][j], x[uu + w][j]);
+        acc[j] = f4_add(acc[j], x[0][j]);
+      }
+      // ---- a finished row is stored by its slot
+      if (row >= 0 && want) {
+        store_row<LPR, VPL>(a, row, sub, acc, du, rs, pol);
+#pragma unroll
+        for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
+      }
+      // ---- advance
+      if (want) {
+        row = claim;
+        s = ns;
+        e = ne;
+        du = ndu;
+        rs = nrs;
+      } else {
+        s += U;
+      }
+#pragma unroll
+      for (int k = 0; k < NID; ++k) ids[k] = nids[k];
+    }
   }
 }
 
@@ -286,6 +421,24 @@ static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
 }
 
 
+template <int LPR, int VPL, int U>
+static int launch_spmm_rows(const SpmmArgs& a, cudaStream_t s) {
+  static int blocks_per_sm = 0;
+  static int sms = 0;
+  if (!blocks_per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm_rows<LPR, VPL, U>, 256, 0);
+    blocks_per_sm = std::max(1, blocks_per_sm);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t grid = std::min<int64_t>((int64_t)sms * blocks_per_sm, ceil_div(a.n_items, 8));
+  MPH_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
+  k_spmm_rows<LPR, VPL, U><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
+  count_launch();
+  return launch_check("spmm (row slots)");
+}
+
 static int env_int(const char* name) {
   const char* v = getenv(name);
   return v ? atoi(v) : 0;
@@ -318,6 +471,14 @@ static int launch_spmm_u(const SpmmArgs& a, cudaStream_t s) {
 template <bool HAS_VAL>
 static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
   const int nv4 = a.nv4;
+  if (!HAS_VAL && a.row_slots && nv4 <= 16) {  // narrow rows, low degree: several rows per warp
+    if (nv4 <= 1) return launch_spmm_rows<1, 1, 4>(a, s);
+    if (nv4 <= 2) return launch_spmm_rows<2, 1, 4>(a, s);
+    if (nv4 <= 4) return launch_spmm_rows<4, 1, 4>(a, s);
+    if (nv4 <= 8) return launch_spmm_rows<8, 1, 8>(a, s);
+    if (nv4 <= 12) return launch_spmm_rows<4, 3, 4>(a, s);
+    return launch_spmm_rows<16, 1, 8>(a, s);
+  }
   if (nv4 <= 1) return launch_spmm<1, 1, HAS_VAL>(a, s);
   if (nv4 <= 2) return launch_spmm<2, 1, HAS_VAL>(a, s);
   if (nv4 <= 4) return launch_spmm<4, 1, HAS_VAL>(a, s);
@@ -369,6 +530,12 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.epi.row0 = epi ? epi->row0 : 0;
   if (a.epi.drop.threshold == 0) a.epi.flags &= ~MPH_EPI_DROPOUT;
   a.epi.c4_0 = 0;
+  // Row slots (k_spmm_rows) for narrow rows when the mean degree is low; MPH_SPMM_ROWS=0/1 overrides.
+  {
+    const char* rs_env = getenv("MPH_SPMM_ROWS");
+    const bool low_degree = g->nnz < kRowSlotMaxDegree * (int64_t)g->n_rows;
+    a.row_slots = rs_env ? (atoi(rs_env) != 0) : low_degree;
+  }
   // Column slabs: on graphs with a mean degree >= 16, rows of w = 128 / 256 are aggregated as two
   // halves, one launch each, so the slab of the gathered operand that a community of rows
   // touches is half as large and stays in L2 (measured: products -1..4 %, reddit -2 %); on

@@ -125,6 +125,50 @@ def test_spmm_widths(P, spmm_graph, w):
     assert_agg_close(Z, oracle.aggregate(ref, T), agg_bound(ref, T), what=f"spmm w={w}")
 
 
+@pytest.fixture(scope="module")
+def sparse_graph(P):
+    w = make_small(5003, 20000, 4, 5, seed=33, alpha=2.3)       # mean degree ~9 with hubs: row-slot regime
+    g = P.Graph(w["src"], w["dst"], 5003)
+    return g, oracle.graph_build(w["src"], w["dst"], 5003)
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("w", [4, 8, 16, 24, 40, 48, 64, 128])
+def test_spmm_row_slots_vs_warp_rows(P, sparse_graph, w, mode, monkeypatch):
+    """k_spmm_rows (several rows per warp, MPH_SPMM_ROWS=1) and the warp-per-row kernel (0) on a
+    low-degree graph: both within the FP32 aggregation bound, fused bias/ReLU/dropout epilogue
+    exact in its mask, and bitwise deterministic run to run."""
+    from paper_2512_01678_b200._lib import EPI_BIAS, EPI_DROPOUT, EPI_RELU, Epilogue
+    monkeypatch.setenv("MPH_SPMM_ROWS", mode)
+    g, ref = sparse_graph
+    rng = np.random.default_rng(w + 100)
+    T = rng.standard_normal((ref.num_nodes, w)).astype(np.float32)
+    Tp = (ref.dinv[:, None] * T).astype(np.float32)
+    tin = cuda(Tp)
+    out = torch.zeros((ref.num_nodes, w), device="cuda")
+    g.spmm(tin, out, w=w)
+    assert_agg_close(out.cpu().numpy(), oracle.aggregate(ref, T), agg_bound(ref, T), what=f"w={w} rows={mode}")
+    b = rng.standard_normal(w).astype(np.float32)
+    bias = cuda(b)
+    e = Epilogue()
+    e.flags = EPI_BIAS | EPI_RELU | EPI_DROPOUT
+    e.bias = bias.data_ptr()
+    e.mask_scale = 1.0
+    e.dropout_p, e.dropout_seed, e.dropout_layer, e.dropout_epoch = 0.25, 77, 2, 3
+    o1, o2 = torch.zeros_like(out), torch.zeros_like(out)
+    g.spmm(tin, o1, w=w, epi=e)
+    g.spmm(tin, o2, w=w, epi=e)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    keep = oracle.dropout_keep(ref.num_nodes, w, 0.25, 77, 2, 3)
+    zpre = oracle.aggregate(ref, T) + b
+    got = o1.cpu().numpy()
+    assert np.all(got[~keep] == 0)
+    sc = 1.0 / (1.0 - float(np.float32(0.25)))
+    assert_agg_close(got, np.maximum(zpre, 0) * keep * sc, (agg_bound(ref, T) + np.abs(b)) * sc + 1e-30,
+                     what=f"epilogue w={w} rows={mode}")
+
+
 def test_spmm_bias_relu_and_determinism(P, spmm_graph):
     from paper_2512_01678_b200._lib import EPI_BIAS, EPI_RELU, Epilogue
     g, ref = spmm_graph
