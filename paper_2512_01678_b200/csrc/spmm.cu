@@ -66,7 +66,7 @@ __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int6
 // Fused epilogue of one aggregated row: the LPR lanes of a slot hold acc[j] = columns
 // 4·(sub + j·LPR) .. +3.  part 0 stores raw sums; part 1 adds them to part 0's; then dinv, bias,
 // ReLU, dropout, row scale, TF32 (Q1, Q6, Q8, Q10).
-constexpr int64_t kRowSlotMaxDegree = 32;  // mean degree (incl. self loop) below which k_spmm_rows serves w <= 64
+constexpr int64_t kRowSlotMaxDegree = 16;  // mean degree (incl. self loop) below which k_spmm_rows serves w <= 64 (arxiv -7 %; products at 26 is 5 % slower with it)
 
 template <int LPR, int VPL>
 __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, const float4 (&acc)[VPL], float du,
@@ -217,6 +217,10 @@ __global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
     it = __shfl_sync(FULL, it, 0);
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
+    if (rr.y - rr.x == 1) {  // a long row (> E edges) is an item of its own: all slots on it
+      spmm_row<LPR, VPL, false, 0>(a, rr.x, lane);
+      continue;
+    }
     int w0 = rr.x;  // row bounds window: lane i holds [ws, we) of row w0 + i
     int64_t ws = 0, we = 0;
     {
