@@ -171,9 +171,12 @@ def test_errors_state_machine(P):
     assert e.value.name == "MPH_ESTATE"
 
 
-def test_localized_spmm_equals_global(P):
+@pytest.mark.parametrize("rows_mode", ["0", "1"])
+def test_localized_spmm_equals_global(P, rows_mode, monkeypatch):
     """D1-D4 on one GPU: each rank's owned+ghost view, ghost rows filled from their owners,
-    aggregates exactly the rows of the global SpMM (parts 0 then 1 == whole row)."""
+    aggregates exactly the rows of the global SpMM (parts 0 then 1 == whole row), with the
+    warp-per-row kernel and with the row-slot kernel (MPH_SPMM_ROWS)."""
+    monkeypatch.setenv("MPH_SPMM_ROWS", rows_mode)
     w = make_small(4000, 40000, 4, 6, seed=12, alpha=2.1, mu=0.5)
     g = P.Graph(w["src"], w["dst"], 4000)
     rp, ci, dg, di = (t.cpu().numpy() for t in g.csr())
