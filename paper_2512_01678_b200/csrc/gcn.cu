@@ -178,9 +178,19 @@ static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogu
 
 // a11: all-reduce one layer's [dW_l | b_l] gradient segment on the comm stream as soon as it is
 // complete, overlapping the rest of the backward pass (P:525-532 pipelined backward).
-static int grad_allreduce_async(mph_gcn* m, int li, cudaStream_t s) {
+// P2P: the dW GEMM's final reduction stores dW_l into every rank's slab itself (GradMirror), so
+// only the rest of the segment (b_l and padding) is pushed; `dw_mirrored` says which case.
+static int grad_mirror(mph_gcn* m, int li, GradMirror* mir, const GradMirror** out) {
+  *out = nullptr;
+  if (!m->p2p) return MPH_OK;
+  MPH_TRY(p2p_grad_mirror(m->p2p, m->layers[li].off_w, mir));
+  *out = mir;
+  return MPH_OK;
+}
+
+static int grad_allreduce_async(mph_gcn* m, int li, cudaStream_t s, bool dw_mirrored = false) {
   if (m->world == 1) return MPH_OK;
-  const int64_t a = m->layers[li].off_w;
+  const int64_t a = dw_mirrored ? m->layers[li].off_b : m->layers[li].off_w;
   const int64_t b = li + 1 < m->L ? m->layers[li + 1].off_w : m->n_params;
   MPH_CUDA_TRY(cudaEventRecord(m->ev_grad, s));
   MPH_CUDA_TRY(cudaStreamWaitEvent(m->cs, m->ev_grad, 0));
@@ -195,9 +205,9 @@ static int gemm_nt_p(int M, int N, int K, const float* A, int lda, const float* 
   return gemm_nt_launch(M, N, K, A, lda, Bt, ldb, C, ldc, e, s, colsum_fill);
 }
 static int gemm_tn_p(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
-                     void* ws, size_t wsb, cudaStream_t s) {
+                     void* ws, size_t wsb, cudaStream_t s, const GradMirror* mirror = nullptr) {
   prof::Scope sc(MPH_PROF_GEMM_TN, s, 4.0 * ((double)K * M + (double)K * N + (double)M * N), 2.0 * M * N * K);
-  return gemm_tn_launch(M, N, K, A, lda, B, ldb, C, ldc, ws, wsb, s);
+  return gemm_tn_launch(M, N, K, A, lda, B, ldb, C, ldc, ws, wsb, s, mirror);
 }
 
 static mph_epilogue epi_none() {
@@ -320,6 +330,8 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
   }
   for (int li = m->L - 1; li >= 0 && m->agg != MPH_AGG_MAX; --li) {
     Layer& l = m->layers[li];
+    GradMirror mir{};
+    const GradMirror* mirp = nullptr;  // set when this layer's dW GEMM writes every rank's slab itself
     const float* Hin = li == 0 ? m->Xr : m->layers[li - 1].out;
     const int ld_in = li == 0 ? m->f->P : m->layers[li - 1].pout;
     const float* Gsrc;  // gradient w.r.t. the transform output (TF) or Z (AF)
@@ -338,18 +350,20 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
                        2.0 * m->f->nnz * l.pout);
         MPH_TRY(sparse_xtg_launch(m->f, l.G, l.pout, l.pout, m->grads + l.off_w, l.pout, s));
       } else {
+        MPH_TRY(grad_mirror(m, li, &mir, &mirp));
         MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, Hin, ld_in, l.G, l.pout, m->grads + l.off_w, l.pout, m->ws,
-                          m->ws_bytes, s));
+                          m->ws_bytes, s, mirp));
       }
     } else {
       // AF layer 1: dZ_1 (unscaled) is the gradient of Z = Y·W + b
       Gsrc = l.dZ;
+      MPH_TRY(grad_mirror(m, li, &mir, &mirp));
       MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, l.Y, l.pin, l.dZ, l.pout, m->grads + l.off_w, l.pout, m->ws,
-                        m->ws_bytes, s));
+                        m->ws_bytes, s, mirp));
     }
     // [dW_l | db_l] complete (db_l came from the loss or the layer above): reduce it across ranks
     // while this layer's dH and the layers below proceed (a11)
-    MPH_TRY(grad_allreduce_async(m, li, s));
+    MPH_TRY(grad_allreduce_async(m, li, s, mirp != nullptr));
     if (li > 0) {
       // a8: dZ_{l-1} = (G·W^T) ⊙ 1[H_{l-1} > 0] (/(1-p)), db_{l-1} as column sums, then the dinv
       // pre-scale for the next backward SpMM (TF) — all in one GEMM epilogue.

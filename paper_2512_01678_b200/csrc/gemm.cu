@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) k_reduce_rows(const float* in, int rows, 
 // even and odd steps), then lane sums of the 8 warps are added in warp order.  Deterministic for
 // a given (splits, M, N).  Needs M*N % 4 == 0 and 16-byte aligned ws.
 __global__ void __launch_bounds__(256) k_reduce_splits4(const float* __restrict__ ws, int splits, int M, int N,
-                                                        float* __restrict__ C, int ldc) {
+                                                        float* __restrict__ C, int ldc, const GradMirror mir) {
   __shared__ float4 part[8][32];
   const int64_t total4 = (int64_t)M * N / 4;
   const int64_t t4 = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
@@ -221,11 +221,21 @@ __global__ void __launch_bounds__(256) k_reduce_splits4(const float* __restrict_
       C[r * ldc + c + 2] = s4.z;
       C[r * ldc + c + 3] = s4.w;
     }
+    if (mir.n) {  // NEXT-1: the finished dW also lands in every rank's gradient slab (P2P stores)
+      const int64_t o = r * ldc + c + (*mir.gen_dev & 1) * mir.par_stride;
+      for (int q = 0; q < mir.n; ++q) {
+        mir.base[q][o] = s4.x;
+        mir.base[q][o + 1] = s4.y;
+        mir.base[q][o + 2] = s4.z;
+        mir.base[q][o + 3] = s4.w;
+      }
+    }
   }
+  if (mir.n) __threadfence_system();
 }
 
 // out[r*ldc + c] = sum_s ws[(s*M + r)*N + c]   (fixed order over splits; any N)
-__global__ void k_reduce_splits(const float* ws, int splits, int M, int N, float* C, int ldc) {
+__global__ void k_reduce_splits(const float* ws, int splits, int M, int N, float* C, int ldc, const GradMirror mir) {
   const int64_t total = (int64_t)M * N;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = t / N;
@@ -233,7 +243,12 @@ __global__ void k_reduce_splits(const float* ws, int splits, int M, int N, float
     float s = 0.0f;
     for (int k = 0; k < splits; ++k) s += ws[(int64_t)k * total + t];
     C[r * ldc + c] = s;
+    if (mir.n) {
+      const int64_t o = r * ldc + c + (*mir.gen_dev & 1) * mir.par_stride;
+      for (int q = 0; q < mir.n; ++q) mir.base[q][o] = s;
+    }
   }
+  if (mir.n) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ host side
@@ -370,7 +385,7 @@ size_t gemm_tn_ws_bytes(int M, int N, int K) {
 }
 
 int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc, void* ws,
-                   size_t ws_bytes, cudaStream_t s) {
+                   size_t ws_bytes, cudaStream_t s, const GradMirror* mirror) {
   if (M <= 0 || N <= 0 || K < 0 || !A || !B || !C) return fail(MPH_EINVAL, "gemm_tn: bad arguments");
   if (N > 256) return fail(MPH_ENOTSUP, "gemm_tn: N=%d > 256", N);
   if (lda % 4 || ldb % 4 || lda < M || ldb < N || ldc < N)
@@ -410,11 +425,12 @@ int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B,
   count_launch();
   MPH_TRY(launch_check("gemm_tn"));
   const int64_t total = (int64_t)M * N;
-  if (N % 4 == 0)
-    k_reduce_splits4<<<(unsigned)ceil_div(total / 4, 32), 256, 0, s>>>(p.ws, splits, M, N, C, ldc);
+  const GradMirror mir = mirror ? *mirror : GradMirror{};
+  if (N % 4 == 0 && (ldc & 3) == 0)
+    k_reduce_splits4<<<(unsigned)ceil_div(total / 4, 32), 256, 0, s>>>(p.ws, splits, M, N, C, ldc, mir);
   else
     k_reduce_splits<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 148 * 8), 256, 0, s>>>(p.ws, splits, M, N, C,
-                                                                                              ldc);
+                                                                                              ldc, mir);
   count_launch();
   return launch_check("reduce_splits");
 }

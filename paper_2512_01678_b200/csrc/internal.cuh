@@ -91,8 +91,20 @@ struct P2PState {
   int64_t xgen = 0;              // host counter of setup exchanges (constant operands)
 };
 
+// A kernel that finalises gradient entries can also store them straight into every rank's
+// receive slab (the all-reduce's "send" fused into the producer): element i of the producer's
+// output also goes to base[q][i + (*gen_dev & 1) * par_stride] for q < n, then a system fence.
+struct GradMirror {
+  float* base[kP2PMaxWorld];
+  int n;
+  const int64_t* gen_dev;
+  int64_t par_stride;
+};
+
 namespace mph {
 int p2p_alloc_arena(P2PState* p, size_t bytes);
+// Mirror of this rank's slab slot, starting at flat parameter offset `off`, in every rank.
+int p2p_grad_mirror(const P2PState* p, int64_t off, GradMirror* out);
 void p2p_free(P2PState* p);
 int p2p_export(const P2PState* p, uint8_t* blob);
 int p2p_open(P2PState* p, const mph_graph* g, const uint8_t* blobs, int world);
@@ -153,7 +165,7 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
 int gemm_nt_colsum_rows(int M);
 size_t gemm_tn_ws_bytes(int M, int N, int K);
 int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
-                   void* ws, size_t ws_bytes, cudaStream_t s);
+                   void* ws, size_t ws_bytes, cudaStream_t s, const GradMirror* mirror = nullptr);
 int reduce_rows_launch(const float* in, int rows, int cols, int ld, float* out, int accumulate, cudaStream_t s);
 
 size_t softmax_ce_ws_bytes(int N, int C);

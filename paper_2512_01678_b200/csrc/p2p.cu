@@ -241,6 +241,17 @@ const uint64_t* p2p_flags_local(const P2PState* p, int slot) {
 }
 const float* p2p_gsum_local(const P2PState* p) { return (const float*)(p->arena + p->off_gsum); }
 
+int p2p_grad_mirror(const P2PState* p, int64_t off, GradMirror* out) {
+  if (!p->opened) return fail(MPH_ESTATE, "p2p: mph_gcn_p2p_open has not been called");
+  *out = GradMirror{};
+  for (int q = 0; q < p->world; ++q)
+    out->base[q] = (float*)(p->peer_base[q] + p->peer_gsum_off[q]) + (int64_t)p->rank * p->n_params + off;
+  out->n = p->world;
+  out->gen_dev = p->gen_dev;
+  out->par_stride = (int64_t)p->world * p->n_params;
+  return MPH_OK;
+}
+
 int p2p_gen_advance(const P2PState* p, cudaStream_t s) {
   k_gen_advance<<<1, 1, 0, s>>>(p->gen_dev);
   count_launch();
