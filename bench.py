@@ -353,6 +353,8 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                              "bytes_per_launch": by.value / cnt.value, "TFLOPs": fl.value / tms.value / 1e9}
     L.mph_profile_enable(0)
     loss_last = m.loss_buf.item()
+    if world > 1 and args.comm == "p2p" and m.p2p_status() != 0:
+        raise RuntimeError(f"rank {rank}: a peer-memory wait timed out (MPH_ETIMEOUT); the timings are invalid")
     if world > 1:
         ms = _max_over_ranks(torch, dist, ms)
 
