@@ -25,6 +25,7 @@ Parity status of each function (pins live in tests/test_oracle_*.py):
   train .............. pinned (monotone loss on the separable SBM toy)
   partition_1d / localize ... pinned (brute-force recount, union = global set)
   tf32_rna ........... pinned (known values incl. ties away from zero, bounds, idempotence)
+  bf16_rne ........... pinned (known values incl. ties to even, bounds, idempotence, torch bf16)
   aggregate_scheme (sum/mean) ... pinned (brute force over neighbour sets from the raw edge list,
                                   dense adjoints, Ã·1 = d̃, mean of a constant, torch autograd)
   aggregate_max / _backward ..... pinned (brute force with ties -> smallest id, hand star case,

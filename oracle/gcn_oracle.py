@@ -19,7 +19,7 @@ __all__ = [
     "OracleError", "Graph", "graph_build", "a_hat_values", "a_hat_dense_from_csr",
     "aggregate", "aggregate_rows", "analyze_features", "FeatureAnalysis",
     "splitmix64_stream", "xavier_init", "philox4x32_10", "dropout_keep",
-    "dropout_threshold", "tf32_rna", "forward", "softmax_ce", "backward", "adam_step", "train",
+    "dropout_threshold", "tf32_rna", "bf16_rne", "forward", "softmax_ce", "backward", "adam_step", "train",
     "AGGREGATORS", "aggregate_scheme", "aggregate_max", "aggregate_max_backward",
     "connected_components", "partition_components", "partition_greedy", "partition_hierarchical", "relabel",
     "partition_stats",
@@ -346,13 +346,28 @@ def tf32_rna(x) -> np.ndarray:
     return a.astype(np.float64)
 
 
+def bf16_rne(x) -> np.ndarray:
+    """BF16 operand rounding (north_star "TF32 or BF16 inputs, FP32 accumulate"): the value as an
+    fp32 number with its mantissa rounded to BF16's 7 bits, to nearest, ties to even (the
+    cvt.rn.bf16.f32 rule): add 0x7FFF plus the lowest kept bit, clear the low 16 bits.  Finite
+    inputs only."""
+    a = np.array(x, dtype=np.float32, copy=True)
+    u = a.view(np.uint32)
+    u += np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))
+    u &= np.uint32(0xFFFF0000)
+    return a.astype(np.float64)
+
+
 def _operand(M, rounding):
-    """A dense GEMM operand as the tensor core sees it (identity unless rounding == "tf32")."""
+    """A dense GEMM operand as the tensor core sees it (identity unless rounding is "tf32" or
+    "bf16")."""
     if rounding is None or sp.issparse(M):
         return M
-    if rounding != "tf32":
-        raise ValueError(rounding)
-    return tf32_rna(M)
+    if rounding == "tf32":
+        return tf32_rna(M)
+    if rounding == "bf16":
+        return bf16_rne(M)
+    raise ValueError(rounding)
 
 
 def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1, operand_rounding=None,

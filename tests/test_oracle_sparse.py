@@ -91,3 +91,42 @@ def test_tf32_forward_within_operand_bound():
     # sparse X: the layer-1 product stays exact
     _, cs = oracle.forward(g, sp.csr_matrix(w["X"]), Ws, bs, operand_rounding="tf32")
     assert np.allclose(cs["Z"][0], z1_exact, rtol=1e-13, atol=1e-15)
+
+
+# ---------------------------------------------------------------- BF16 operand rounding (north star option)
+def test_bf16_rne_known_values():
+    """cvt.rn.bf16.f32: 7 explicit mantissa bits, nearest, ties to even."""
+    u = 2.0 ** -7                                         # BF16 ulp at 1.0
+    cases = {1.0: 1.0, 1.0 + u / 2: 1.0, 1.0 + u + u / 2: 1.0 + 2 * u, -(1.0 + u + u / 2): -(1.0 + 2 * u),
+             1.0 + u / 4: 1.0, 1.0 + 3 * u / 4: 1.0 + u, 2.0 - u / 4: 2.0, 0.0: 0.0,
+             3.0 * 2.0 ** 100: 3.0 * 2.0 ** 100, 1.0 + 2.0 ** -23: 1.0}
+    for x, want in cases.items():
+        assert oracle.bf16_rne(np.float32(x)) == want, x
+
+
+def test_bf16_rne_properties_and_torch():
+    import torch
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal(100000) * np.exp(rng.uniform(-20, 20, 100000))).astype(np.float32)
+    r = oracle.bf16_rne(x)
+    assert np.all(np.abs(r - x) <= 2.0 ** -8 * np.abs(x.astype(np.float64)))
+    assert np.all(r.astype(np.float32).view(np.uint32) & 0xFFFF == 0)
+    assert np.array_equal(oracle.bf16_rne(r), r)                   # idempotent
+    assert np.array_equal(oracle.bf16_rne(-x), -r)                 # symmetric
+    # an independent implementation of the same rounding: torch's float32 -> bfloat16 cast
+    t = torch.from_numpy(x).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(r, t)
+
+
+def test_bf16_trajectory_within_north_star():
+    """BF16 GEMM operands (each dense product's operands rounded by bf16_rne, FP32-exact
+    accumulation in the oracle) keep loss_1..loss_10 within the north star's 1e-3 of the exact
+    trajectory on a Pubmed-shaped graph forced dense — the accuracy case for a BF16 path."""
+    w = make_small(2000, 16000, 60, 3, kind="dense", seed=11, alpha=2.4, mu=0.2)
+    g = oracle.graph_build(w["src"], w["dst"], 2000)
+    dims = (60, 32, 3)
+    ex, _ = oracle.train(g, w["X"], w["y"], dims, epochs=10, seed=42)
+    bf, _ = oracle.train(g, w["X"], w["y"], dims, epochs=10, seed=42, operand_rounding="bf16")
+    ex, bf = np.array(ex), np.array(bf)
+    assert np.all(np.abs(bf - ex) <= 1e-3 * np.maximum(1.0, np.abs(ex))), np.abs(bf - ex).max()
+    assert not np.array_equal(bf, ex)
