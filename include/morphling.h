@@ -211,8 +211,9 @@ int mph_gemm_tn_workspace(int32_t M, int32_t N, int32_t K, size_t* bytes_h);
 /* SURVEY §8(b) generic form: C = op(A)·op(B) for the two shapes of the GCN path —
  * (transA, transB) = (0, 1): mph_gemm_nt with the epilogue flags RELU / TF32 (those needing no
  * operand pointer); (1, 0): mph_gemm_tn (workspace allocated and freed stream-ordered, flags
- * must be 0).  precision: 0 = TF32 (the only one implemented; 1 = BF16 -> MPH_ENOTSUP).
- * Other transpose combinations: MPH_ENOTSUP. */
+ * must be 0).  precision: 0 = TF32 (A_d, B_d float32), 1 = BF16 (A_d, B_d point to bfloat16
+ * values; lda, ldb in elements, multiples of 8; tcgen05 kind::f16, FP32 accumulate).
+ * Other transpose combinations or precisions: MPH_ENOTSUP. */
 int mph_gemm(int32_t M, int32_t N, int32_t K, const float* A_d, int32_t lda, int32_t transA, const float* B_d,
              int32_t ldb, int32_t transB, float* C_d, int32_t ldc, int32_t precision, uint32_t epilogue_flags,
              void* stream);

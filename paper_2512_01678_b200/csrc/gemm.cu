@@ -54,13 +54,19 @@ __device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;"
 
 #include "gemm_nt.inc"
 
+// BF: BF16 operands.  MN-major tiles: a chunk is 32 (tf32) or 64 (bf16) MN elements = one 128-byte
+// row per node, kBK node rows per stage.  tf32 uses the SWIZZLE_128B_BASE32B layout (4-row atoms,
+// UMMA_K = 8 nodes = 1 KB); bf16 the plain SWIZZLE_128B layout (8-row atoms, UMMA_K = 16 nodes =
+// 2 KB).  In both, LBO = the stride between MN chunks, SBO = the stride between K atoms.
+template <bool BF>
 __global__ void __launch_bounds__(kThreads, 1)
     k_gemm_tn(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t kChunk = kBK * 128;  // one 32-wide MN chunk of BK rows: 4 KB
-  const uint32_t a_bytes = 4 * kChunk;    // 128 = 4 chunks of 32 along M
-  const uint32_t nchunk_b = (uint32_t)p.BN / 32;
+  constexpr int kMN = BF ? 64 : 32;            // MN elements per 128-byte row
+  constexpr uint32_t kChunk = kBK * 128;       // one MN chunk of BK node rows: 4 KB
+  const uint32_t a_bytes = (kBM / kMN) * kChunk;
+  const uint32_t nchunk_b = (uint32_t)p.BN / kMN;
   const uint32_t b_bytes = nchunk_b * kChunk;
   uint8_t* sA = smem;
   uint8_t* sB = smem + (size_t)p.stages * a_bytes;
@@ -103,8 +109,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* a_dst = sA + (size_t)s * a_bytes;
         uint8_t* b_dst = sB + (size_t)s * b_bytes;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tc::tma_load_2d(a_dst + c * kChunk, &tmA, &full[s], m0 + 32 * c, kb * kBK);
-        for (uint32_t c = 0; c < nchunk_b; ++c) tc::tma_load_2d(b_dst + c * kChunk, &tmB, &full[s], 32 * c, kb * kBK);
+        for (int c = 0; c < kBM / kMN; ++c)
+          tc::tma_load_2d(a_dst + c * kChunk, &tmA, &full[s], m0 + kMN * c, kb * kBK);
+        for (uint32_t c = 0; c < nchunk_b; ++c)
+          tc::tma_load_2d(b_dst + c * kChunk, &tmB, &full[s], kMN * (int)c, kb * kBK);
       }
     }
   } else if (warp == 1) {
@@ -116,11 +124,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_after_sync();
         const uint32_t a_base = tc::smem_u32(sA + (size_t)s * a_bytes);
         const uint32_t b_base = tc::smem_u32(sB + (size_t)s * b_bytes);
+        if constexpr (BF) {
 #pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {  // 8 node rows = two 512 B SW128_32B atoms per chunk
-          const uint64_t da = tc::smem_desc_sw128(a_base + k * 1024, kChunk, 512, 1);
-          const uint64_t db = tc::smem_desc_sw128(b_base + k * 1024, kChunk, 512, 1);
-          tc::mma_tf32(tmem, da, db, p.idesc, (i | k) != 0 ? 1u : 0u);
+          for (int k = 0; k < kBK / 16; ++k) {  // 16 node rows = two 1 KB SW128 atoms per chunk
+            const uint64_t da = tc::smem_desc_sw128(a_base + k * 2048, kChunk, 1024, 2);
+            const uint64_t db = tc::smem_desc_sw128(b_base + k * 2048, kChunk, 1024, 2);
+            tc::mma_bf16(tmem, da, db, p.idesc, (i | k) != 0 ? 1u : 0u);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {  // 8 node rows = two 512 B SW128_32B atoms per chunk
+            const uint64_t da = tc::smem_desc_sw128(a_base + k * 1024, kChunk, 512, 1);
+            const uint64_t db = tc::smem_desc_sw128(b_base + k * 1024, kChunk, 512, 1);
+            tc::mma_tf32(tmem, da, db, p.idesc, (i | k) != 0 ? 1u : 0u);
+          }
         }
         tc::mma_commit(&empty[s]);
       }
@@ -264,15 +281,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-int make_tmap(CUtensorMap* m, const float* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
-              uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+int make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+              uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B, bool bf16 = false) {
   auto fn = encode_fn();
   if (!fn) return fail(MPH_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old or no device)");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld * sizeof(float)};
+  cuuint64_t strides[1] = {ld * (bf16 ? 2 : 4)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+  CUresult r = fn(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                  const_cast<void*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
@@ -314,10 +332,15 @@ int gemm_nt_colsum_rows(int M) { return (int)std::min<int64_t>(ceil_div(M, kBM),
 
 int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
                    const mph_epilogue* epi, cudaStream_t s, int colsum_fill) {
+  return gemm_nt_launch_ex(M, N, K, A, lda, Bt, ldb, C, ldc, epi, s, colsum_fill, false);
+}
+
+int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* Bt, int ldb, float* C, int ldc,
+                      const mph_epilogue* epi, cudaStream_t s, int colsum_fill, bool bf16) {
   if (M < 0 || N <= 0 || K < 0 || !A || !Bt || !C) return fail(MPH_EINVAL, "gemm_nt: bad arguments");
   if (N > 256) return fail(MPH_ENOTSUP, "gemm_nt: N=%d > 256", N);
-  if (lda % 4 || ldb % 4 || ldc % 4 || lda < K || ldb < K || ldc < N)
-    return fail(MPH_EINVAL, "gemm_nt: lda/ldb/ldc must be multiples of 4 with lda, ldb >= K and ldc >= N");
+  if (lda % (bf16 ? 8 : 4) || ldb % (bf16 ? 8 : 4) || ldc % 4 || lda < K || ldb < K || ldc < N)
+    return fail(MPH_EINVAL, "gemm_nt: lda/ldb (multiples of 16 bytes) >= K and ldc (multiple of 4) >= N");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Bt) | reinterpret_cast<uintptr_t>(C)) & 15)
     return fail(MPH_EINVAL, "gemm_nt: A, Bt and C must be 16-byte aligned");
   const uint32_t flags = epi ? epi->flags : 0u;
@@ -335,7 +358,8 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
   p.N = N;
   p.K = K;
   p.BN = BN;
-  p.num_kb = (int)ceil_div(K, kBK);
+  const int kelems = bf16 ? 64 : kBK;  // K elements per 128-byte k-block
+  p.num_kb = (int)ceil_div(K, kelems);
   p.n_tiles = (int)ceil_div(M, kBM);
   p.colsum_rows = colsum_fill ? p.n_tiles : 0;  // rows beyond the grid are zero-filled only for the ABI
   const size_t stage_bytes = kATileBytes + (size_t)BN * kBK * 4;
@@ -347,7 +371,7 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
                        (size_t)(2 * 8 + 4 + p.n_epi * kEpiBufs) * 8 + 16 + 4 * (size_t)BN * sizeof(float);
   constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
   p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, (kMaxSmem - fixed) / stage_bytes));
-  p.idesc = tc::idesc_tf32(kBM, BN, 0, 0);
+  p.idesc = bf16 ? tc::idesc_bf16(kBM, BN, 0, 0) : tc::idesc_tf32(kBM, BN, 0, 0);
   p.tmem_cols = tmem_cols_for(2 * BN);
   p.epi.flags = flags;
   p.epi.row_scale = epi ? epi->row_scale : nullptr;
@@ -360,21 +384,26 @@ int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt
   p.epi.row0 = epi ? epi->row0 : 0;
   if (p.epi.drop.threshold == 0) p.epi.flags &= ~MPH_EPI_DROPOUT;
   CUtensorMap ta, tb, tcm, tm;
-  MPH_TRY(make_tmap(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kBK, kBM));
-  MPH_TRY(make_tmap(&tb, Bt, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kBK, (uint32_t)BN));
+  MPH_TRY(make_tmap(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kelems, kBM, CU_TENSOR_MAP_SWIZZLE_128B, bf16));
+  MPH_TRY(make_tmap(&tb, Bt, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kelems, (uint32_t)BN, CU_TENSOR_MAP_SWIZZLE_128B,
+                    bf16));
   MPH_TRY(make_tmap(&tcm, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, 32, 32));
   if (flags & MPH_EPI_MASK)
     MPH_TRY(make_tmap(&tm, epi->mask_src, (uint64_t)N, (uint64_t)M, (uint64_t)epi->ld_mask, 32, 32));
   else
     tm = tcm;
   const size_t smem = fixed + (size_t)p.stages * stage_bytes;
-  static size_t configured = 0;
-  if (smem > configured) {
-    MPH_CUDA_TRY(cudaFuncSetAttribute(k_gemm_nt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
+  static size_t configured[2] = {0, 0};
+  if (smem > configured[bf16]) {
+    MPH_CUDA_TRY(cudaFuncSetAttribute(bf16 ? k_gemm_nt<true> : k_gemm_nt<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[bf16] = smem;
   }
   const int grid = std::min(p.n_tiles, sms);
-  k_gemm_nt<<<grid, 64 + 32 * p.n_epi, smem, s>>>(ta, tb, tcm, tm, p);
+  if (bf16)
+    k_gemm_nt<true><<<grid, 64 + 32 * p.n_epi, smem, s>>>(ta, tb, tcm, tm, p);
+  else
+    k_gemm_nt<false><<<grid, 64 + 32 * p.n_epi, smem, s>>>(ta, tb, tcm, tm, p);
   count_launch();
   return launch_check("gemm_nt");
 }
@@ -386,16 +415,21 @@ size_t gemm_tn_ws_bytes(int M, int N, int K) {
 
 int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc, void* ws,
                    size_t ws_bytes, cudaStream_t s, const GradMirror* mirror) {
+  return gemm_tn_launch_ex(M, N, K, A, lda, B, ldb, C, ldc, ws, ws_bytes, s, mirror, false);
+}
+
+int gemm_tn_launch_ex(int M, int N, int K, const void* A, int lda, const void* B, int ldb, float* C, int ldc,
+                      void* ws, size_t ws_bytes, cudaStream_t s, const GradMirror* mirror, bool bf16) {
   if (M <= 0 || N <= 0 || K < 0 || !A || !B || !C) return fail(MPH_EINVAL, "gemm_tn: bad arguments");
   if (N > 256) return fail(MPH_ENOTSUP, "gemm_tn: N=%d > 256", N);
-  if (lda % 4 || ldb % 4 || lda < M || ldb < N || ldc < N)
-    return fail(MPH_EINVAL, "gemm_tn: lda/ldb must be multiples of 4 with lda >= M, ldb >= N, ldc >= N");
+  if (lda % (bf16 ? 8 : 4) || ldb % (bf16 ? 8 : 4) || lda < M || ldb < N || ldc < N)
+    return fail(MPH_EINVAL, "gemm_tn: lda/ldb (multiples of 16 bytes) >= M, N and ldc >= N");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15)
     return fail(MPH_EINVAL, "gemm_tn: A and B must be 16-byte aligned");
   const size_t need = gemm_tn_ws_bytes(M, N, K);
   if (!ws || ws_bytes < need) return fail(MPH_EINVAL, "gemm_tn: workspace %zu < %zu bytes", ws_bytes, need);
   if (reinterpret_cast<uintptr_t>(ws) & 15) return fail(MPH_EINVAL, "gemm_tn: workspace must be 16-byte aligned");
-  const int BN = round_up(N, 32);
+  const int BN = round_up(N, bf16 ? 64 : 32);
   TnParams p{};
   p.M = M;
   p.N = N;
@@ -404,24 +438,28 @@ int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B,
   p.num_kb = (int)ceil_div(K, kBK);
   const int splits = gemm_tn_splits(M, N, K);
   p.kb_per_split = (int)ceil_div(std::max(p.num_kb, 1), splits);
-  const size_t stage_bytes = (size_t)4 * kBK * 128 + (size_t)(BN / 32) * kBK * 128;
+  const int kmn = bf16 ? 64 : 32;
+  const size_t stage_bytes = (size_t)(kBM / kmn) * kBK * 128 + (size_t)(BN / kmn) * kBK * 128;
   p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, kSmemBudget / stage_bytes));
   p.ws = reinterpret_cast<float*>(ws);
-  p.idesc = tc::idesc_tf32(kBM, BN, 1, 1);
+  p.idesc = bf16 ? tc::idesc_bf16(kBM, BN, 1, 1) : tc::idesc_tf32(kBM, BN, 1, 1);
   p.tmem_cols = tmem_cols_for(BN);
   CUtensorMap ta, tb;
-  MPH_TRY(make_tmap(&ta, A, (uint64_t)M, (uint64_t)std::max(K, 1), (uint64_t)lda, 32, kBK,
-                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
-  MPH_TRY(make_tmap(&tb, B, (uint64_t)N, (uint64_t)std::max(K, 1), (uint64_t)ldb, 32, kBK,
-                    CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  const CUtensorMapSwizzle swz = bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  MPH_TRY(make_tmap(&ta, A, (uint64_t)M, (uint64_t)std::max(K, 1), (uint64_t)lda, kmn, kBK, swz, bf16));
+  MPH_TRY(make_tmap(&tb, B, (uint64_t)N, (uint64_t)std::max(K, 1), (uint64_t)ldb, kmn, kBK, swz, bf16));
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + (2 * p.stages + 1) * 8 + 16;
-  static size_t configured = 0;
-  if (smem > configured) {
-    MPH_CUDA_TRY(cudaFuncSetAttribute(k_gemm_tn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
+  static size_t configured[2] = {0, 0};
+  if (smem > configured[bf16]) {
+    MPH_CUDA_TRY(cudaFuncSetAttribute(bf16 ? k_gemm_tn<true> : k_gemm_tn<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[bf16] = smem;
   }
   dim3 grid((unsigned)ceil_div(M, kBM), (unsigned)splits);
-  k_gemm_tn<<<grid, kThreads, smem, s>>>(ta, tb, p);
+  if (bf16)
+    k_gemm_tn<true><<<grid, kThreads, smem, s>>>(ta, tb, p);
+  else
+    k_gemm_tn<false><<<grid, kThreads, smem, s>>>(ta, tb, p);
   count_launch();
   MPH_TRY(launch_check("gemm_tn"));
   const int64_t total = (int64_t)M * N;
@@ -469,7 +507,8 @@ extern "C" int mph_gemm(int32_t M, int32_t N, int32_t K, const float* A_d, int32
                         const float* B_d, int32_t ldb, int32_t transB, float* C_d, int32_t ldc, int32_t precision,
                         uint32_t epilogue_flags, void* stream) {
   using namespace mph;
-  if (precision != 0) return fail(MPH_ENOTSUP, "mph_gemm: precision %d (only 0 = TF32 is implemented)", precision);
+  if (precision != 0 && precision != 1) return fail(MPH_ENOTSUP, "mph_gemm: precision %d (0 TF32, 1 BF16)", precision);
+  const bool bf16 = precision == 1;
   cudaStream_t s = (cudaStream_t)stream;
   if (transA == 0 && transB == 1) {
     if (epilogue_flags & ~(uint32_t)(MPH_EPI_RELU | MPH_EPI_TF32))
@@ -477,14 +516,14 @@ extern "C" int mph_gemm(int32_t M, int32_t N, int32_t K, const float* A_d, int32
     mph_epilogue e{};
     e.flags = epilogue_flags;
     e.mask_scale = 1.0f;
-    return gemm_nt_launch(M, N, K, A_d, lda, B_d, ldb, C_d, ldc, &e, s);
+    return gemm_nt_launch_ex(M, N, K, A_d, lda, B_d, ldb, C_d, ldc, &e, s, 1, bf16);
   }
   if (transA == 1 && transB == 0) {
     if (epilogue_flags) return fail(MPH_EINVAL, "mph_gemm: no epilogue on the transposed-A shape");
     const size_t ws_bytes = gemm_tn_ws_bytes(M, N, K);
     void* ws = nullptr;
     if (ws_bytes) MPH_CUDA_TRY(cudaMallocAsync(&ws, ws_bytes, s));
-    const int rc = gemm_tn_launch(M, N, K, A_d, lda, B_d, ldb, C_d, ldc, ws, ws_bytes, s);
+    const int rc = gemm_tn_launch_ex(M, N, K, A_d, lda, B_d, ldb, C_d, ldc, ws, ws_bytes, s, nullptr, bf16);
     if (ws) cudaFreeAsync(ws, s);
     return rc;
   }

@@ -163,9 +163,14 @@ int pack_rows(const int32_t* ids, int64_t n, const float* buf, int ld, int w, fl
 int gemm_nt_launch(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
                    const mph_epilogue* epi, cudaStream_t s, int colsum_fill = 1);
 int gemm_nt_colsum_rows(int M);
+// The same with BF16 operands when bf16 (A [M][lda], Bt [N][ldb] as uint16 bf16; lda, ldb % 8 == 0).
+int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* Bt, int ldb, float* C, int ldc,
+                      const mph_epilogue* epi, cudaStream_t s, int colsum_fill, bool bf16);
 size_t gemm_tn_ws_bytes(int M, int N, int K);
 int gemm_tn_launch(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
                    void* ws, size_t ws_bytes, cudaStream_t s, const GradMirror* mirror = nullptr);
+int gemm_tn_launch_ex(int M, int N, int K, const void* A, int lda, const void* B, int ldb, float* C, int ldc,
+                      void* ws, size_t ws_bytes, cudaStream_t s, const GradMirror* mirror, bool bf16);
 int reduce_rows_launch(const float* in, int rows, int cols, int ld, float* out, int accumulate, cudaStream_t s);
 
 size_t softmax_ce_ws_bytes(int N, int C);

@@ -67,7 +67,7 @@ def test_mph_gemm_generic(P, M, N, K):
     mph_gemm(M2, N2, K2, a2_d.data_ptr(), M2, 1, b2_d.data_ptr(), N2, 0, c2.data_ptr(), N2, 0, 0, s)
     torch.cuda.synchronize()
     assert_gemm_close(c2.cpu().numpy(), A2.T, B2, what="mph_gemm TN")
-    for bad in ((0, 0, 0), (1, 1, 0), (0, 1, 1)):   # (transA, transB, precision)
+    for bad in ((0, 0, 0), (1, 1, 0), (0, 1, 2)):   # (transA, transB, precision)
         with pytest.raises(MorphlingError) as e:
             mph_gemm(M, N, K, a_d.data_ptr(), K, bad[0], bt_d.data_ptr(), K, bad[1], c.data_ptr(), N, bad[2], 0, s)
         assert e.value.code == -9   # MPH_ENOTSUP
@@ -138,3 +138,33 @@ def test_set_allocator_torch(P):
         assert len(live) == 0
     finally:
         P.use_torch_allocator(False)
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 48, 104), (3001, 256, 64), (777, 128, 608), (4099, 40, 256)])
+def test_mph_gemm_bf16(P, M, N, K):
+    """precision 1 (BF16 operands, kind::f16, FP32 accumulate) on both GEMM shapes: against the FP64
+    product of the same BF16 values, so only the FP32 accumulation error remains (1e-5 bound)."""
+    from paper_2512_01678_b200._lib import mph_gemm
+    rng = np.random.default_rng(M + K)
+    s = torch.cuda.current_stream().cuda_stream
+    ldk = (K + 7) // 8 * 8
+    A = torch.zeros((M, ldk), dtype=torch.bfloat16, device="cuda")
+    Bt = torch.zeros((N, ldk), dtype=torch.bfloat16, device="cuda")
+    A[:, :K] = torch.from_numpy(rng.standard_normal((M, K)).astype(np.float32)).to(torch.bfloat16)
+    Bt[:, :K] = torch.from_numpy(rng.standard_normal((N, K)).astype(np.float32)).to(torch.bfloat16)
+    c = torch.zeros((M, N), device="cuda")
+    mph_gemm(M, N, K, A.data_ptr(), ldk, 0, Bt.data_ptr(), ldk, 1, c.data_ptr(), N, 1, 0, s)
+    torch.cuda.synchronize()
+    a64, b64 = A[:, :K].double().cpu().numpy(), Bt[:, :K].double().cpu().numpy()
+    ref, bound = a64 @ b64.T, np.abs(a64) @ np.abs(b64).T
+    assert np.all(np.abs(c.double().cpu().numpy() - ref) <= 1e-5 * bound + 1e-30)
+    # transposed-A shape, contraction over K2 "nodes" with MN-major BF16 tiles
+    K2, M2, N2 = 7001, (K + 7) // 8 * 8, (N + 7) // 8 * 8
+    A2 = torch.from_numpy(rng.standard_normal((K2, M2)).astype(np.float32)).to(torch.bfloat16).cuda()
+    B2 = torch.from_numpy(rng.standard_normal((K2, N2)).astype(np.float32)).to(torch.bfloat16).cuda()
+    c2 = torch.zeros((M2, N2), device="cuda")
+    mph_gemm(M2, N2, K2, A2.data_ptr(), M2, 1, B2.data_ptr(), N2, 0, c2.data_ptr(), N2, 1, 0, s)
+    torch.cuda.synchronize()
+    a2, b2 = A2.double().cpu().numpy(), B2.double().cpu().numpy()
+    ref2, bound2 = a2.T @ b2, np.abs(a2).T @ np.abs(b2)
+    assert np.all(np.abs(c2.double().cpu().numpy() - ref2) <= 1e-5 * bound2 + 1e-30)
