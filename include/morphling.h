@@ -136,6 +136,10 @@ int mph_features_destroy(mph_features* f);
 #define MPH_EPI_COLSUM 32u   /* per-CTA column sums of the value before ROWSCALE -> colsum_out */
 #define MPH_EPI_TF32 64u     /* round the stored value to TF32 (cvt.rna), for outputs that only feed
                                 tensor-core GEMMs: unbiased operand rounding (reading R2) */
+#define MPH_EPI_BF16 128u    /* store the output as bfloat16 (round to nearest even; the output pointer
+                                holds bf16, ld in elements): outputs that only feed BF16 GEMMs.
+                                mph_gemm_nt and mph_spmm (whole rows, part -1) */
+#define MPH_EPI_MASK_BF16 256u /* mask_src holds bfloat16 values (ld_mask in elements); mph_gemm_nt */
 
 typedef struct {
   uint32_t flags;
@@ -386,7 +390,17 @@ typedef struct {
                             dense-mode features and a single GPU only, else MPH_ENOTSUP) */
   int32_t comm_mode;     /* P > 1 only: MPH_COMM_NCCL (0, default: pack + grouped ncclSend/Recv,
                             ncclAllReduce) or MPH_COMM_P2P (1: NVLink peer memory, see below) */
+  int32_t precision;     /* GEMM operands: MPH_PREC_TF32 (0, default: FP32 storage, operands rounded
+                            to TF32) or MPH_PREC_BF16 (1: the tensors that only feed tensor-core
+                            GEMMs — hidden H, backward G, Y_1, dZ_1, the copies of X and W — are
+                            stored as bfloat16 and the GEMMs run kind::f16; aggregation, loss and
+                            optimizer stay FP32).  BF16: single GPU, gcn/sum/mean aggregators, not a
+                            one-layer aggregate-first model (else MPH_ENOTSUP); mph_gcn_tensor views
+                            of those tensors hold bf16. */
 } mph_gcn_desc;
+
+#define MPH_PREC_TF32 0
+#define MPH_PREC_BF16 1
 
 #define MPH_COMM_NCCL 0
 #define MPH_COMM_P2P 1
@@ -452,7 +466,7 @@ int mph_gcn_graph_state(const mph_gcn* m, int32_t** t_d, double** loss_d);
  * or dZ_1 for an AF layer 1), 3 = aggregate-first Y_1, 4 = transform output T'_l = dinv ⊙ (H·W)
  * (n_cols rows incl. ghosts), 5 = dZ'_l (dinv-prescaled gradient, n_cols rows; AF layer 1: dZ_1). */
 int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, const float** ptr_d, int32_t* rows_h,
-                   int32_t* width_h, int32_t* ld_h);
+                   int32_t* width_h, int32_t* ld_h, int32_t* elem_bytes_h /* nullable: 4 float32, 2 bfloat16 */);
 /* ---- NEXT-1: NVLink peer-memory halo exchange and gradient sum (
  * halo P:517-523, gradient sum P:525-532, overlap P:765).
  * A model created with comm_mode = MPH_COMM_P2P on a localized graph keeps every buffer a peer

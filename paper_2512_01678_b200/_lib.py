@@ -19,6 +19,7 @@ STATUS = {0: "MPH_OK", -1: "MPH_EINVAL", -2: "MPH_ERANGE", -3: "MPH_EDEGENERATE"
           -10: "MPH_ETIMEOUT"}
 
 EPI_BIAS, EPI_RELU, EPI_ROWSCALE, EPI_MASK, EPI_DROPOUT, EPI_COLSUM, EPI_TF32 = 1, 2, 4, 8, 16, 32, 64
+EPI_BF16, EPI_MASK_BF16 = 128, 256
 AGG = {"gcn": 0, "sum": 1, "mean": 2, "max": 3}            # MPH_AGG_*
 OPT = {"adam": 0, "sgd": 1, "adamw": 2}                    # MPH_OPT_*
 
@@ -49,7 +50,7 @@ class OptimCfg(C.Structure):
 class GcnDesc(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("dims_h", C.POINTER(C.c_int32)), ("dropout_p", C.c_float),
                 ("dropout_seed", C.c_uint64), ("order_policy", C.c_int32), ("aggregator", C.c_int32),
-                ("comm_mode", C.c_int32)]
+                ("comm_mode", C.c_int32), ("precision", C.c_int32)]
 
 
 if not os.path.exists(LIB_PATH):
@@ -132,7 +133,7 @@ _SIGS = {
     "mph_gcn_graph_capture_opt": [P, C.POINTER(OptimCfg), i32, P],
     "mph_gcn_graph_replay": [P, P],
     "mph_gcn_graph_state": [P, PP, PP],
-    "mph_gcn_tensor": [P, i32, i32, PP, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
+    "mph_gcn_tensor": [P, i32, i32, PP, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
     "mph_gcn_info": [P, P, C.POINTER(i32)],
     "mph_set_allocator": [P, P, P],
     "mph_graph_localize": [P, P, i32, i32, P, PP],
@@ -148,6 +149,7 @@ _SIGS = {
 }
 
 COMM = {"nccl": 0, "p2p": 1}
+PREC = {"tf32": 0, "bf16": 1}
 P2P_BLOB_BYTES = 512
 
 EXPORTED = ["mph_version", "mph_last_error"] + list(_SIGS)

@@ -42,7 +42,8 @@ class _CAI:
                                          "version": 3, "strides": None}
 
 
-_TYPESTR = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8", torch.uint8: "|u1"}
+_TYPESTR = {torch.float32: "<f4", torch.float64: "<f8", torch.int32: "<i4", torch.int64: "<i8", torch.uint8: "|u1",
+            torch.int16: "<i2"}
 
 
 def device_view(ptr: int, shape, dtype) -> torch.Tensor:
@@ -354,7 +355,7 @@ class GCN:
 
     def __init__(self, graph: Graph, features: Features, dims, dropout_p: float = 0.0, dropout_seed: int = 0,
                  order_policy: int = 0, comm: "Comm | str | None" = None, stream=None, aggregator: str = "gcn",
-                 pg=None):
+                 pg=None, precision: str = "tf32"):
         """comm: None (one GPU), a Comm (NCCL halo + all-reduce) or "p2p" (NVLink peer memory,
         NEXT-1): the ranks' arena descriptors are all-gathered over the torch.distributed group
         `pg` (plumbing only) and mapped by mph_gcn_p2p_open."""
@@ -368,8 +369,9 @@ class GCN:
         self.L = len(self.dims) - 1
         self.aggregator = aggregator
         arr = (C.c_int32 * len(self.dims))(*self.dims)
+        self.precision = precision
         desc = GcnDesc(self.L, arr, float(dropout_p), int(dropout_seed), int(order_policy), L.AGG[aggregator],
-                       L.COMM[self.comm_mode])
+                       L.COMM[self.comm_mode], L.PREC[precision])
         h = _out_ptr()
         L.mph_gcn_create(graph.h, features.h, C.byref(desc), self.comm.h if self.comm is not None else None,
                          stream_ptr(stream), C.byref(h))
@@ -520,10 +522,15 @@ class GCN:
         return self.graph_loss
 
     def tensor(self, kind: int, layer: int) -> torch.Tensor:
-        p, rows, width, ld = C.c_void_p(), C.c_int32(), C.c_int32(), C.c_int32()
-        L.mph_gcn_tensor(self.h, kind, layer, C.byref(p), C.byref(rows), C.byref(width), C.byref(ld))
+        """Borrowed view of an activation (mph_gcn_tensor): float32, or bfloat16 for the GEMM-only
+        tensors of a BF16-precision model."""
+        p, rows, width, ld, eb = C.c_void_p(), C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        L.mph_gcn_tensor(self.h, kind, layer, C.byref(p), C.byref(rows), C.byref(width), C.byref(ld), C.byref(eb))
         if not p.value:
             return None
+        if eb.value == 2:
+            raw = device_view(p.value, (rows.value, ld.value), torch.int16)
+            return raw.view(torch.bfloat16)[:, :width.value]
         return device_view(p.value, (rows.value, ld.value), torch.float32)[:, :width.value]
 
     def __del__(self):

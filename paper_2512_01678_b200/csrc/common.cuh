@@ -141,6 +141,13 @@ __device__ __forceinline__ bool p2p_wait_all(const uint64_t* flags_row, int worl
   return true;
 }
 
+// Two floats -> two bfloat16 (round to nearest even) packed lo | hi << 16: BF16 GEMM operands.
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // Philox4x32-10 (Salmon et al., SC'11) — the dropout mask of reading Q10.
 struct PhiloxOut {
   uint32_t v[4];

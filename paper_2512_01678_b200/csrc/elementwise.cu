@@ -1,5 +1,7 @@
 // a5 loss, a9 Adam, Xavier init, weight transposes, and the sparse-feature kernels of the
 // density switch (a2 sparse X_csr·W, a7 sparse X_csc^T·G).
+#include <cuda_bf16.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -431,28 +433,44 @@ int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int laye
 // ------------------------------------------------------------------ weight copies / row scale
 // The tensor-core operand copies of W_l: dst_t = round_tf32(W^T) (K-major B of the forward
 // GEMM) and dst_r = round_tf32(W) (B of the dH GEMM).  The FP32 master copy stays in params.
-__global__ void k_weight_copies(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,
+// BF: the copies are bfloat16 (dst_t / dst_r hold uint16, ld in elements) for BF16 GEMMs.
+template <bool BF>
+__global__ void k_weight_copies(const float* src, int rows, int cols, int ld_src, void* dst_t, int ld_t, void* dst_r,
                                 int ld_r) {
   __shared__ float tile[32][33];
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
-    const float v = (r < rows && c < cols) ? tf32_rna(src[(int64_t)r * ld_src + c]) : 0.0f;
+    const float x = (r < rows && c < cols) ? src[(int64_t)r * ld_src + c] : 0.0f;
+    const float v = BF ? x : tf32_rna(x);
     tile[i][threadIdx.x] = v;
-    if (dst_r && r < rows && c < cols) dst_r[(int64_t)r * ld_r + c] = v;
+    if (dst_r && r < rows && c < cols) {
+      if (BF)
+        static_cast<uint16_t*>(dst_r)[(int64_t)r * ld_r + c] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+      else
+        static_cast<float*>(dst_r)[(int64_t)r * ld_r + c] = v;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int c = c0 + i, r = r0 + threadIdx.x;
-    if (c < cols && r < rows) dst_t[(int64_t)c * ld_t + r] = tile[threadIdx.x][i];
+    if (c < cols && r < rows) {
+      if (BF)
+        static_cast<uint16_t*>(dst_t)[(int64_t)c * ld_t + r] = __bfloat16_as_ushort(__float2bfloat16_rn(tile[threadIdx.x][i]));
+      else
+        static_cast<float*>(dst_t)[(int64_t)c * ld_t + r] = tile[threadIdx.x][i];
+    }
   }
 }
 
 int weight_copies_launch(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,
-                         int ld_r, cudaStream_t s) {
+                         int ld_r, cudaStream_t s, bool bf16) {
   if (rows <= 0 || cols <= 0) return MPH_OK;
   dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
-  k_weight_copies<<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld_src, dst_t, ld_t, dst_r, ld_r);
+  if (bf16)
+    k_weight_copies<true><<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld_src, dst_t, ld_t, dst_r, ld_r);
+  else
+    k_weight_copies<false><<<grid, dim3(32, 8), 0, s>>>(src, rows, cols, ld_src, dst_t, ld_t, dst_r, ld_r);
   count_launch();
   return launch_check("weight_copies");
 }
@@ -466,7 +484,10 @@ __global__ void k_rowscale(const float* in, int ld_in, const float* scale, int r
     const int c = (int)(t - i * w);
     float v = in[i * ld_in + c];
     if (scale) v *= scale[i];
-    out[i * ld_out + c] = round ? tf32_rna(v) : v;
+    if (round == 2)  // bfloat16 output (BF16 GEMM operand copy)
+      reinterpret_cast<uint16_t*>(out)[i * ld_out + c] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+    else
+      out[i * ld_out + c] = round ? tf32_rna(v) : v;
   }
 }
 

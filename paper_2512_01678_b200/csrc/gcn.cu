@@ -47,6 +47,9 @@ struct mph_gcn {
   int world = 1;
   int L = 0;
   int agg = MPH_AGG_GCN;  // aggregation scheme (NEXT-4)
+  // MPH_PREC_BF16: every tensor that only feeds tensor-core GEMMs (hidden H, backward G, Y_1, dZ_1,
+  // the copies of X and W) is stored as bfloat16 and the GEMMs run kind::f16 (FP32 accumulate)
+  bool bf16 = false;
   // diagonal scales of a linear scheme: forward AGG = diag(fpost)·Ã·diag(fpre), adjoint
   // diag(bpost)·Ã·diag(bpre); nullptr = 1 (aggregate.cu)
   const float *fpre = nullptr, *fpost = nullptr, *bpre = nullptr, *bpost = nullptr;
@@ -122,10 +125,17 @@ static void gcn_free(mph_gcn* m) {
   delete m;
 }
 
+// element `off` of a buffer that holds bf16 (BF16 mode) or float values
+static float* elem(const mph_gcn* m, float* base, int64_t off) {
+  return m->bf16 ? reinterpret_cast<float*>(reinterpret_cast<uint16_t*>(base) + off) : base + off;
+}
+// the bf16-or-tf32 stored-output epilogue flag for tensors that only feed GEMMs
+static uint32_t gemm_operand_flag(const mph_gcn* m) { return m->bf16 ? MPH_EPI_BF16 : MPH_EPI_TF32; }
+
 static int refresh_wt(mph_gcn* m, cudaStream_t s) {
   for (auto& l : m->layers)
-    MPH_TRY(weight_copies_launch(m->params + l.off_w, l.pin, l.pout, l.pout, m->wt + l.off_wt, l.pin, m->wr + l.off_w,
-                                 l.pout, s));
+    MPH_TRY(weight_copies_launch(m->params + l.off_w, l.pin, l.pout, l.pout, elem(m, m->wt, l.off_wt), l.pin,
+                                 elem(m, m->wr, l.off_w), l.pout, s, m->bf16));
   return MPH_OK;
 }
 
@@ -198,16 +208,19 @@ static int grad_allreduce_async(mph_gcn* m, int li, cudaStream_t s, bool dw_mirr
   return mph_allreduce_sum(m->comm, m->grads + a, b - a, 0, m->cs);
 }
 static int gemm_nt_p(int M, int N, int K, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc,
-                     const mph_epilogue* e, cudaStream_t s, int colsum_fill = 1) {
-  double extra = (e && (e->flags & MPH_EPI_MASK)) ? 4.0 * M * N : 0.0;
-  prof::Scope sc(MPH_PROF_GEMM_NT, s, 4.0 * ((double)M * K + (double)N * K + (double)M * N) + extra,
+                     const mph_epilogue* e, cudaStream_t s, int colsum_fill = 1, bool bf16 = false) {
+  const uint32_t f = e ? e->flags : 0u;
+  const double in_b = bf16 ? 2.0 : 4.0, out_b = (f & MPH_EPI_BF16) ? 2.0 : 4.0;
+  const double extra = (f & MPH_EPI_MASK) ? ((f & MPH_EPI_MASK_BF16) ? 2.0 : 4.0) * M * N : 0.0;
+  prof::Scope sc(MPH_PROF_GEMM_NT, s, in_b * ((double)M * K + (double)N * K) + out_b * M * N + extra,
                  2.0 * M * N * K);
-  return gemm_nt_launch(M, N, K, A, lda, Bt, ldb, C, ldc, e, s, colsum_fill);
+  return gemm_nt_launch_ex(M, N, K, A, lda, Bt, ldb, C, ldc, e, s, colsum_fill, bf16);
 }
 static int gemm_tn_p(int M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C, int ldc,
-                     void* ws, size_t wsb, cudaStream_t s, const GradMirror* mirror = nullptr) {
-  prof::Scope sc(MPH_PROF_GEMM_TN, s, 4.0 * ((double)K * M + (double)K * N + (double)M * N), 2.0 * M * N * K);
-  return gemm_tn_launch(M, N, K, A, lda, B, ldb, C, ldc, ws, wsb, s, mirror);
+                     void* ws, size_t wsb, cudaStream_t s, const GradMirror* mirror = nullptr, bool bf16 = false) {
+  prof::Scope sc(MPH_PROF_GEMM_TN, s, (bf16 ? 2.0 : 4.0) * ((double)K * M + (double)K * N) + 4.0 * M * N,
+                 2.0 * M * N * K);
+  return gemm_tn_launch_ex(M, N, K, A, lda, B, ldb, C, ldc, ws, wsb, s, mirror, bf16);
 }
 
 static mph_epilogue epi_none() {
@@ -246,7 +259,7 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
   const bool hidden = lnum < m->L;
   mph_epilogue eo = epi_none();
   // hidden outputs only feed tensor-core GEMMs (and the ReLU-mask sign test): store them as TF32
-  eo.flags = MPH_EPI_BIAS | (hidden ? (MPH_EPI_RELU | MPH_EPI_TF32) : 0u);
+  eo.flags = MPH_EPI_BIAS | (hidden ? (MPH_EPI_RELU | gemm_operand_flag(m)) : 0u);
   eo.bias = m->params + l.off_b;
   if (hidden && m->dropout_p > 0.0f) {
     eo.flags |= MPH_EPI_DROPOUT;
@@ -275,16 +288,18 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
       mph_epilogue et = epi_none();
       et.flags = m->fpre ? MPH_EPI_ROWSCALE : 0u;
       et.row_scale = m->fpre;
-      MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, A, lda, m->wt + l.off_wt, l.pin, l.T, l.pout, &et, s));
+      MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, A, lda, elem(m, m->wt, l.off_wt), l.pin, l.T, l.pout, &et, s, 1,
+                        m->bf16));
     }
     // a10 + a3: ghost rows of T' from their owners; Z = Â·T + b, ReLU (dropout) fused
     MPH_TRY(spmm_halo(m, l.T, l.pout, l.out, &eo, m->fpost, li, buf_T(li), s));
   } else {
     // aggregate-first layer 1: Y = Â·X (on dinv ⊙ X), Z = Y·W + b with the epilogue fused in the GEMM
     mph_epilogue en = epi_none();
-    en.flags = MPH_EPI_TF32;  // Y only feeds the GEMMs
+    en.flags = gemm_operand_flag(m);  // Y only feeds the GEMMs
     MPH_TRY(spmm_p(g, m->Xs, l.pin, l.pin, l.Y, l.pin, &en, m->fpost, s));
-    MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, l.Y, l.pin, m->wt + l.off_wt, l.pin, l.out, l.pout, &eo, s));
+    MPH_TRY(gemm_nt_p(g->n_rows, l.pout, l.pin, l.Y, l.pin, elem(m, m->wt, l.off_wt), l.pin, l.out, l.pout, &eo, s, 1,
+                      m->bf16));
   }
   return MPH_OK;
 }
@@ -338,7 +353,9 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
     if (l.order == 0) {
       // a10 + a6: G = AGGᵀ·dZ = bpost ⊙ Ã·dZ' (Â symmetric: the forward kernel)
       mph_epilogue en = epi_none();
-      en.flags = MPH_EPI_TF32;  // G only feeds the dW and dH GEMMs
+      // G only feeds the dW and dH GEMMs (sparse layer 1: the CUDA-core X_cscᵀ·G gather, FP32 input)
+      const bool sparse_l1 = li == 0 && m->f->mode == 1;
+      en.flags = sparse_l1 ? MPH_EPI_TF32 : gemm_operand_flag(m);
       // exchange indices must increase within a generation (the flags are monotone counters):
       // forward layers 0..L-1, then backward layers L-1..0
       MPH_TRY(spmm_halo(m, l.dZ, l.pout, l.G, &en, m->bpost, 2 * m->L - 1 - li, buf_dZ(li), s));
@@ -352,14 +369,14 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       } else {
         MPH_TRY(grad_mirror(m, li, &mir, &mirp));
         MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, Hin, ld_in, l.G, l.pout, m->grads + l.off_w, l.pout, m->ws,
-                          m->ws_bytes, s, mirp));
+                          m->ws_bytes, s, mirp, m->bf16));
       }
     } else {
       // AF layer 1: dZ_1 (unscaled) is the gradient of Z = Y·W + b
       Gsrc = l.dZ;
       MPH_TRY(grad_mirror(m, li, &mir, &mirp));
       MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, l.Y, l.pin, l.dZ, l.pout, m->grads + l.off_w, l.pout, m->ws,
-                        m->ws_bytes, s, mirp));
+                        m->ws_bytes, s, mirp, m->bf16));
     }
     // [dW_l | db_l] complete (db_l came from the loss or the layer above): reduce it across ranks
     // while this layer's dH and the layers below proceed (a11)
@@ -370,15 +387,15 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       Layer& pl = m->layers[li - 1];
       mph_epilogue ed = epi_none();
       // TF: dZ' feeds the FP32 SpMM (keep FP32); AF: dZ_1 feeds only the dW GEMM (TF32)
-      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM |
-                 (pl.order == 0 ? (m->bpre ? MPH_EPI_ROWSCALE : 0u) : MPH_EPI_TF32);
+      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM | (m->bf16 ? MPH_EPI_MASK_BF16 : 0u) |
+                 (pl.order == 0 ? (m->bpre ? MPH_EPI_ROWSCALE : 0u) : gemm_operand_flag(m));
       ed.mask_src = pl.out;
       ed.ld_mask = pl.pout;
       ed.mask_scale = dropout_scale(m->dropout_p);
       ed.colsum_out = pl.colsum;
       ed.row_scale = m->bpre;
-      MPH_TRY(gemm_nt_p(g->n_rows, pl.pout, l.pout, Gsrc, l.pout, m->wr + l.off_w, l.pout, pl.dZ, pl.pout, &ed,
-                        s, /*colsum_fill=*/0));
+      MPH_TRY(gemm_nt_p(g->n_rows, pl.pout, l.pout, Gsrc, l.pout, elem(m, m->wr, l.off_w), l.pout, pl.dZ, pl.pout,
+                        &ed, s, /*colsum_fill=*/0, m->bf16));
       // db_{l-1}: the GEMM wrote one column-sum row per persistent CTA
       MPH_TRY(reduce_rows_launch(pl.colsum, gemm_nt_colsum_rows(g->n_rows), pl.pout, pl.pout, m->grads + pl.off_b, 0,
                                  s));
@@ -409,6 +426,12 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     return fail(MPH_EINVAL, "unknown aggregator %d", desc->aggregator);
   if (desc->comm_mode != MPH_COMM_NCCL && desc->comm_mode != MPH_COMM_P2P)
     return fail(MPH_EINVAL, "unknown comm_mode %d", desc->comm_mode);
+  if (desc->precision != MPH_PREC_TF32 && desc->precision != MPH_PREC_BF16)
+    return fail(MPH_EINVAL, "unknown precision %d", desc->precision);
+  if (desc->precision == MPH_PREC_BF16 && (g->world > 1 || desc->aggregator == MPH_AGG_MAX))
+    return fail(MPH_ENOTSUP, "BF16 GEMM operands: single GPU and a linear aggregator only");
+  if (desc->precision == MPH_PREC_BF16 && f->mode == 0 && f->P % 8)
+    return fail(MPH_ENOTSUP, "BF16 GEMM operands: dense features need a padded width multiple of 8 (F > 4)");
   const bool p2p = desc->comm_mode == MPH_COMM_P2P && g->local && g->world > 1;
   int world = 1;
   if (p2p) {
@@ -438,6 +461,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   m->dropout_p = desc->dropout_p;
   m->dropout_seed = desc->dropout_seed;
   m->agg = desc->aggregator;
+  m->bf16 = desc->precision == MPH_PREC_BF16;
   if (!max_agg) {
     MPH_TRY(agg_scales(g, m->agg, 0, &m->fpre, &m->fpost));
     MPH_TRY(agg_scales(g, m->agg, 1, &m->bpre, &m->bpost));
@@ -448,8 +472,10 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     Layer& l = m->layers[li];
     l.fin = desc->dims_h[li];
     l.fout = desc->dims_h[li + 1];
-    l.pin = li == 0 ? (f->mode == 0 ? f->P : pad_width(f->F)) : pad_width(l.fin);
-    l.pout = pad_width(l.fout);
+    // BF16 operands need 16-byte rows: widths padded to multiples of 8 (pad_width gives 4 for w <= 4)
+    auto padw = [&](int w) { return m->bf16 ? round_up(w, 8) : pad_width(w); };
+    l.pin = li == 0 ? (f->mode == 0 ? f->P : pad_width(f->F)) : padw(l.fin);
+    l.pout = padw(l.fout);
     // reading Q7: TF iff F_out <= F_in, or layer 1 in Sparse mode; AF only ever needed on layer 1
     l.order = (desc->order_policy == 1 || l.fout <= l.fin || (li == 0 && f->mode == 1) || li > 0) ? 0 : 1;
     if (max_agg) l.order = 1;  // max is taken before the transform on every layer (R7)
@@ -462,6 +488,10 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   }
   m->n_params = off;
   m->n_wt = offt;
+  if (m->bf16 && m->L == 1 && m->layers[0].order == 1) {
+    gcn_free(m);
+    return fail(MPH_ENOTSUP, "BF16: a one-layer aggregate-first model (its loss gradient feeds a GEMM directly)");
+  }
   int rc = MPH_OK;
   auto bail = [&](int code) {
     gcn_free(m);
@@ -569,7 +599,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
   if (m->layers[0].order == 0 && f->mode == 0 && !max_agg) {
     // TF32-rounded copy of X: the A operand of the layer-1 transform and of its dW GEMM
     if ((rc = dev_alloc(&m->Xr, (size_t)nr * f->P))) return bail(rc);
-    if ((rc = rowscale_launch(f->X, f->P, nullptr, (int)nr, f->P, m->Xr, f->P, 1, s))) return bail(rc);
+    if ((rc = rowscale_launch(f->X, f->P, nullptr, (int)nr, f->P, m->Xr, f->P, m->bf16 ? 2 : 1, s))) return bail(rc);
   }
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create: %s", cudaGetErrorString(e)));
@@ -687,7 +717,7 @@ static int derive_from_features(mph_gcn* m, cudaStream_t s) {
       MPH_TRY(mph_halo_exchange(m->g, m->comm, m->Xs, l.pin, l.pin, s));
     }
   } else {
-    MPH_TRY(rowscale_launch(f->X, f->P, nullptr, m->g->n_rows, f->P, m->Xr, f->P, 1, s));
+    MPH_TRY(rowscale_launch(f->X, f->P, nullptr, m->g->n_rows, f->P, m->Xr, f->P, m->bf16 ? 2 : 1, s));
   }
   return MPH_OK;
 }
@@ -881,11 +911,12 @@ extern "C" int mph_gcn_graph_state(const mph_gcn* m, int32_t** t_d, double** los
 }
 
 extern "C" int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, const float** ptr_d, int32_t* rows_h,
-                              int32_t* width_h, int32_t* ld_h) {
+                              int32_t* width_h, int32_t* ld_h, int32_t* elem_bytes_h) {
   if (!m || layer < 1 || layer > m->L) return fail(MPH_EINVAL, "gcn_tensor arguments");
   const Layer& l = m->layers[layer - 1];
   const float* p = nullptr;
   int rows = m->g->n_rows, width = 0, ld = 0;
+  bool bf = false;  // BF16 mode: the tensors that only feed GEMMs are bfloat16
   switch (kind) {
     case 0:
       if (layer == 1) {
@@ -896,22 +927,26 @@ extern "C" int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, con
         p = m->layers[layer - 2].out;
         width = l.fin;
         ld = l.pin;
+        bf = m->bf16;
       }
       break;
     case 1:
       p = l.out;
       width = l.fout;
       ld = l.pout;
+      bf = m->bf16 && layer < m->L;
       break;
     case 2:
       p = l.order == 0 ? l.G : l.dZ;
       width = l.fout;
       ld = l.pout;
+      bf = m->bf16 && !(layer == 1 && m->f->mode == 1);
       break;
     case 3:
       p = l.Y;
       width = l.fin;
       ld = l.pin;
+      bf = m->bf16;
       break;
     case 4:
       p = l.T;
@@ -928,10 +963,12 @@ extern "C" int mph_gcn_tensor(const mph_gcn* m, int32_t kind, int32_t layer, con
     default:
       return fail(MPH_EINVAL, "unknown tensor kind %d", kind);
   }
+  if (kind == 5 && l.order == 1) bf = m->bf16;  // dZ_1 of an aggregate-first layer 1
   if (ptr_d) *ptr_d = p;
   if (rows_h) *rows_h = rows;
   if (width_h) *width_h = width;
   if (ld_h) *ld_h = ld;
+  if (elem_bytes_h) *elem_bytes_h = bf ? 2 : 4;
   return MPH_OK;
 }
 

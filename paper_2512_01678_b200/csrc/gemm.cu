@@ -339,8 +339,12 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
                       const mph_epilogue* epi, cudaStream_t s, int colsum_fill, bool bf16) {
   if (M < 0 || N <= 0 || K < 0 || !A || !Bt || !C) return fail(MPH_EINVAL, "gemm_nt: bad arguments");
   if (N > 256) return fail(MPH_ENOTSUP, "gemm_nt: N=%d > 256", N);
-  if (lda % (bf16 ? 8 : 4) || ldb % (bf16 ? 8 : 4) || ldc % 4 || lda < K || ldb < K || ldc < N)
-    return fail(MPH_EINVAL, "gemm_nt: lda/ldb (multiples of 16 bytes) >= K and ldc (multiple of 4) >= N");
+  const uint32_t f0 = epi ? epi->flags : 0u;
+  if (lda % (bf16 ? 8 : 4) || ldb % (bf16 ? 8 : 4) || ldc % ((f0 & MPH_EPI_BF16) ? 8 : 4) || lda < K || ldb < K ||
+      ldc < N)
+    return fail(MPH_EINVAL, "gemm_nt: lda/ldb/ldc must be multiples of 16 bytes with lda, ldb >= K, ldc >= N");
+  if ((f0 & MPH_EPI_MASK_BF16) && (!(f0 & MPH_EPI_MASK) || (epi->ld_mask % 8)))
+    return fail(MPH_EINVAL, "gemm_nt: MASK_BF16 needs MASK and ld_mask %% 8 == 0");
   if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Bt) | reinterpret_cast<uintptr_t>(C)) & 15)
     return fail(MPH_EINVAL, "gemm_nt: A, Bt and C must be 16-byte aligned");
   const uint32_t flags = epi ? epi->flags : 0u;
@@ -387,9 +391,12 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   MPH_TRY(make_tmap(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, kelems, kBM, CU_TENSOR_MAP_SWIZZLE_128B, bf16));
   MPH_TRY(make_tmap(&tb, Bt, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kelems, (uint32_t)BN, CU_TENSOR_MAP_SWIZZLE_128B,
                     bf16));
-  MPH_TRY(make_tmap(&tcm, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, 32, 32));
+  const bool out_bf = (flags & MPH_EPI_BF16) != 0, mask_bf = (flags & MPH_EPI_MASK_BF16) != 0;
+  MPH_TRY(make_tmap(&tcm, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, 32, 32,
+                    out_bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, out_bf));
   if (flags & MPH_EPI_MASK)
-    MPH_TRY(make_tmap(&tm, epi->mask_src, (uint64_t)N, (uint64_t)M, (uint64_t)epi->ld_mask, 32, 32));
+    MPH_TRY(make_tmap(&tm, epi->mask_src, (uint64_t)N, (uint64_t)M, (uint64_t)epi->ld_mask, 32, 32,
+                      mask_bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, mask_bf));
   else
     tm = tcm;
   const size_t smem = fixed + (size_t)p.stages * stage_bytes;

@@ -190,7 +190,7 @@ int optim_sum_launch(float* p, float* grads, float* m, float* v, int64_t n, cons
 int xavier_launch(float* W, int f_in, int f_out, int ld, uint64_t seed, int layer, cudaStream_t s);
 // dst_t[j*ld_t + i] = tf32(src[i*ld_src + j]), dst_r[i*ld_r + j] = tf32(src[i*ld_src + j]) (dst_r nullable)
 int weight_copies_launch(const float* src, int rows, int cols, int ld_src, float* dst_t, int ld_t, float* dst_r,
-                         int ld_r, cudaStream_t s);
+                         int ld_r, cudaStream_t s, bool bf16 = false);
 int sparse_xw_launch(const mph_features* f, const float* W, int F_out, int ldw, const float* row_scale, float* T,
                      int ldt, cudaStream_t s);
 int sparse_xtg_launch(const mph_features* f, const float* G, int F_out, int ldg, float* dW, int lddw, cudaStream_t s);

@@ -106,7 +106,12 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, c
       v.z *= rs;
       v.w *= rs;
     }
-    st_f4_hint(orow + c4, to_tf32 ? f4_tf32(v) : v, pol);
+    if (a.epi.flags & MPH_EPI_BF16) {  // BF16 row (only feeds BF16 GEMMs); out/ld_out in bf16 elements
+      uint2* o16 = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + (int64_t)row * a.ld_out);
+      o16[c4] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    } else {
+      st_f4_hint(orow + c4, to_tf32 ? f4_tf32(v) : v, pol);
+    }
   }
 }
 
@@ -504,8 +509,11 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(MPH_EINVAL, "spmm: operands must be 16-byte aligned");
   if (part != -1 && !g->local) return fail(MPH_EINVAL, "spmm: row parts need a localized graph");
-  const uint32_t allowed = MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE | MPH_EPI_TF32;
+  const uint32_t allowed =
+      MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE | MPH_EPI_TF32 | MPH_EPI_BF16;
   if (epi && (epi->flags & ~allowed)) return fail(MPH_EINVAL, "spmm: unsupported epilogue flags 0x%x", epi->flags);
+  if (epi && (epi->flags & MPH_EPI_BF16) && part != -1)
+    return fail(MPH_ENOTSUP, "spmm: BF16 output needs whole rows (part -1)");
   if (epi && (epi->flags & MPH_EPI_BIAS) && (!epi->bias || (reinterpret_cast<uintptr_t>(epi->bias) & 15)))
     return fail(MPH_EINVAL, "spmm: bias must be non-null and 16-byte aligned");
   if (epi && (epi->flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "spmm: null row_scale");
@@ -552,7 +560,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
     for (int c0 = 0; c0 < w; c0 += slab) {
       SpmmArgs b = a;
       b.in = in + c0;
-      b.out = out + c0;
+      b.out = (a.epi.flags & MPH_EPI_BF16) ? reinterpret_cast<float*>(reinterpret_cast<uint16_t*>(out) + c0) : out + c0;
       b.nv4 = std::min(slab, w - c0) / 4;
       if (b.epi.bias) b.epi.bias = a.epi.bias + c0;
       b.epi.c4_0 = c0 / 4;
