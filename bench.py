@@ -203,7 +203,7 @@ def _relabel_workload(P, torch, w, world, how):
     return out, bounds
 
 
-def _build_model(P, torch, w, world, rank, comm, bounds=None):
+def _build_model(P, torch, w, world, rank, comm, bounds=None, precision="tf32"):
     cfg = w["cfg"]
     n = cfg.num_nodes
     X = w["X"]
@@ -218,7 +218,7 @@ def _build_model(P, torch, w, world, rank, comm, bounds=None):
     if world == 1:
         g = P.Graph(w["src"], w["dst"], n)
         f = features(0, n)
-        m = P.GCN(g, f, cfg.dims)
+        m = P.GCN(g, f, cfg.dims, precision=precision)
         y = torch.from_numpy(w["y"]).cuda()
         own = (0, n)
         extra = {}
@@ -233,7 +233,7 @@ def _build_model(P, torch, w, world, rank, comm, bounds=None):
         g = P.Graph.from_plan(plan)
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         f = features(r0, r1)
-        m = P.GCN(g, f, cfg.dims, comm=comm)
+        m = P.GCN(g, f, cfg.dims, comm=comm, precision=precision)
         y = torch.from_numpy(np.ascontiguousarray(w["y"][r0:r1])).cuda()
         own = (r0, r1)
         extra = {"n_ghost": plan.n_ghost, "halo_rows_sent": plan.n_send}
@@ -300,7 +300,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     bounds = None
     if world > 1 and args.partition != "1d":
         w, bounds = _relabel_workload(P, torch, w, world, args.partition)
-    g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm, bounds)
+    g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm, bounds, args.precision)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     cfg = w["cfg"]
@@ -453,6 +453,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         "value": ms, "ms_per_step": ms,
         "config": {**_config_common(argparse.Namespace(**{**vars(args), "config": config}), world),
                    "layer_order": ["AF" if o else "TF" for o in m.order],
+                   "gemm_precision": args.precision,
                    "cuda_graph": use_graph,
                    "l2": "inputs larger than L2 (X and col_idx > 126 MB); no flush" if cfg.num_nodes > 100000
                    else "small workload: operands L2-resident across epochs (no flush)",
@@ -552,7 +553,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": main["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": main["ms_per_step"], "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (SpMM, loss, Adam) + tf32 tensor-core GEMMs",
+            "scaling": "strong", "vs_baseline": None, "dtype": f"f32 (SpMM, loss, Adam) + {args.precision} tensor-core GEMM operands",
             "data": "synthetic", "config": main["config"], "roofline": main["roofline"],
             "cpu_baseline": main["cpu_baseline"], "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
             "clocks": main["clocks"], "kernels": main["kernels"], "final_loss": main["final_loss"],
@@ -579,6 +580,9 @@ def main():
     ap.add_argument("--comm", default="p2p", choices=["nccl", "p2p"],
                     help="N > 1: NVLink peer-memory halo pulls with the gradient sum fused into the optimizer "
                          "(default; SURVEY §8(f) NEXT-1), or NCCL grouped send/recv + all-reduce")
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16"],
+                    help="GEMM operands: TF32 (FP32 storage) or BF16 (GEMM-only tensors stored as bfloat16); "
+                         "aggregation, loss and Adam are FP32 either way")
     ap.add_argument("--share-device", action="store_true",
                     help="testing only: run every rank on cuda:0 (gloo plumbing, --comm p2p) to exercise the "
                          "N > 1 path on a one-GPU box; the timings are not meaningful")
