@@ -127,3 +127,28 @@ def test_products_forward_loss(P):
     ref_loss, _ = oracle.softmax_ce(Z, w["y"])
     assert math.isfinite(loss)
     assert abs(loss - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss)), (loss, ref_loss)
+
+
+@pytest.mark.parametrize("name", ["reddit", "products"])
+def test_bf16_fullsize_epoch1_loss(P, name):
+    """BF16 GEMM operands at BASELINE.json's full sizes: the epoch-1 loss against the exact FP64
+    oracle forward (north star bar 1e-3), then a finite second epoch."""
+    import psutil
+    if name == "products" and psutil.virtual_memory().available < 48 * 2 ** 30:
+        pytest.skip("needs ~48 GB host RAM for the FP64 oracle at products scale")
+    w = make_workload(name)
+    cfg = w["cfg"]
+    g = P.Graph(w["src"], w["dst"], cfg.num_nodes)
+    f = P.Features(torch.from_numpy(w["X"]).cuda())
+    m = P.GCN(g, f, cfg.dims, precision="bf16")
+    m.init_xavier(42)
+    m.set_labels(torch.from_numpy(w["y"]).cuda())
+    loss1 = m.train_epoch(1).item()
+    loss2 = m.train_epoch(2).item()
+    torch.cuda.synchronize()
+    ref_g = oracle.graph_build(w["src"], w["dst"], cfg.num_nodes)
+    Ws, bs = oracle.xavier_init(cfg.dims, 42)
+    Z, _ = oracle.forward(ref_g, w["X"], Ws, bs)
+    ref_loss, _ = oracle.softmax_ce(Z, w["y"])
+    assert abs(loss1 - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss)), (loss1, ref_loss)
+    assert math.isfinite(loss2) and loss2 < loss1
