@@ -394,7 +394,7 @@ typedef struct {
                             to TF32) or MPH_PREC_BF16 (1: the tensors that only feed tensor-core
                             GEMMs — hidden H, backward G, Y_1, dZ_1, the copies of X and W — are
                             stored as bfloat16 and the GEMMs run kind::f16; aggregation, loss and
-                            optimizer stay FP32).  BF16: single GPU, gcn/sum/mean aggregators, not a
+                            optimizer stay FP32).  BF16: gcn/sum/mean aggregators, not a
                             one-layer aggregate-first model (else MPH_ENOTSUP); mph_gcn_tensor views
                             of those tensors hold bf16. */
 } mph_gcn_desc;

@@ -50,6 +50,7 @@ struct mph_gcn {
   // MPH_PREC_BF16: every tensor that only feeds tensor-core GEMMs (hidden H, backward G, Y_1, dZ_1,
   // the copies of X and W) is stored as bfloat16 and the GEMMs run kind::f16 (FP32 accumulate)
   bool bf16 = false;
+  float* part0 = nullptr;  // BF16 with P > 1: FP32 owned-edge sums between the two SpMM parts
   // diagonal scales of a linear scheme: forward AGG = diag(fpost)·Ã·diag(fpre), adjoint
   // diag(bpost)·Ã·diag(bpre); nullptr = 1 (aggregate.cu)
   const float *fpre = nullptr, *fpost = nullptr, *bpre = nullptr, *bpost = nullptr;
@@ -112,6 +113,7 @@ static void gcn_free(mph_gcn* m) {
   dev_free(m->wt);
   dev_free(m->wr);
   dev_free(m->Xr);
+  dev_free(m->part0);
   if (!in_arena(m, m->Xs)) dev_free(m->Xs);
   if (m->own_ws) dev_free(m->ws);
   for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss, m->ev_copied, m->ev_derived})
@@ -181,9 +183,11 @@ static int spmm_halo(mph_gcn* m, float* in, int w, float* out, const mph_epilogu
   }
   MPH_CUDA_TRY(cudaEventRecord(m->ev_halo, m->cs));
   prof::Scope sc(MPH_PROF_SPMM, s, spmm_bytes(g, w), 2.0 * (double)g->nnz * w);
-  MPH_TRY(spmm_launch(g, 0, in, w, w, out, w, nullptr, post, s));
+  // a BF16 output cannot hold part 0's raw sums: they go to an FP32 scratch (part0)
+  const bool bf_out = e && (e->flags & MPH_EPI_BF16);
+  MPH_TRY(spmm_launch(g, 0, in, w, w, bf_out ? m->part0 : out, w, nullptr, post, s));
   MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_halo, 0));
-  return spmm_launch(g, 1, in, w, w, out, w, e, post, s);
+  return spmm_launch(g, 1, in, w, w, out, w, e, post, s, bf_out ? m->part0 : nullptr);
 }
 
 // a11: all-reduce one layer's [dW_l | b_l] gradient segment on the comm stream as soon as it is
@@ -428,8 +432,8 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     return fail(MPH_EINVAL, "unknown comm_mode %d", desc->comm_mode);
   if (desc->precision != MPH_PREC_TF32 && desc->precision != MPH_PREC_BF16)
     return fail(MPH_EINVAL, "unknown precision %d", desc->precision);
-  if (desc->precision == MPH_PREC_BF16 && (g->world > 1 || desc->aggregator == MPH_AGG_MAX))
-    return fail(MPH_ENOTSUP, "BF16 GEMM operands: single GPU and a linear aggregator only");
+  if (desc->precision == MPH_PREC_BF16 && desc->aggregator == MPH_AGG_MAX)
+    return fail(MPH_ENOTSUP, "BF16 GEMM operands: linear aggregators only");
   if (desc->precision == MPH_PREC_BF16 && f->mode == 0 && f->P % 8)
     return fail(MPH_ENOTSUP, "BF16 GEMM operands: dense features need a padded width multiple of 8 (F > 4)");
   const bool p2p = desc->comm_mode == MPH_COMM_P2P && g->local && g->world > 1;
@@ -595,6 +599,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     int wmax = m->layers[0].pin;
     for (const auto& l : m->layers) wmax = std::max(wmax, l.pout);
     if (!p2p && (rc = halo_reserve(g, wmax))) return bail(rc);  // no reallocation while sends are in flight
+    if (m->bf16 && (rc = dev_alloc(&m->part0, (size_t)nr * wmax))) return bail(rc);
   }
   if (m->layers[0].order == 0 && f->mode == 0 && !max_agg) {
     // TF32-rounded copy of X: the A operand of the layer-1 transform and of its dW GEMM

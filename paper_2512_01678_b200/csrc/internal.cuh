@@ -133,8 +133,10 @@ int launch_dinv(const int32_t* deg, float* dinv, float* dinv1, int64_t n, cudaSt
 // SpMM driver (spmm.cu). part: -1 whole row, 0 owned columns (raw sums, no epilogue),
 // 1 ghost columns accumulated onto out + epilogue.
 // post: the output row scale (D̃^{-1/2} for the GCN's Â, D̃^{-1} for mean, nullptr for sum).
+// partial (part 1 only, nullable): where part 0 left its raw FP32 sums (row stride w) when the
+// output itself is BF16; nullptr = they are in out.
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
-                const mph_epilogue* epi, const float* post, cudaStream_t s);
+                const mph_epilogue* epi, const float* post, cudaStream_t s, const float* partial = nullptr);
 int ensure_graph_items(const mph_graph* g, cudaStream_t s);
 // aggregate.cu (NEXT-4): scheme scales, max aggregation and its adjoint, chunked column sums
 int agg_scales(const mph_graph* g, int scheme, int transpose, const float** pre, const float** post);

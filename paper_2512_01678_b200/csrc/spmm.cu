@@ -50,6 +50,7 @@ struct SpmmArgs {
   int n_items;
   int ld_in, ld_out, n_rows, nv4, part;
   int row_slots;  // 1: narrow rows of a low-degree graph -> k_spmm_rows
+  const float* partial;  // part 1 with a BF16 output: part 0's FP32 sums (row stride nv4·4), else nullptr
   EpiDev epi;
 };
 
@@ -84,7 +85,8 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, c
     const int c4 = sub + j * LPR;
     if (c4 >= a.nv4) continue;
     float4 v = acc[j];
-    if (a.part == 1) v = f4_add(v, orow[c4]);
+    if (a.part == 1)
+      v = f4_add(v, a.partial ? reinterpret_cast<const float4*>(a.partial + (int64_t)row * a.nv4 * 4)[c4] : orow[c4]);
     v.x *= du;
     v.y *= du;
     v.z *= du;
@@ -501,7 +503,7 @@ static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
 }
 
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
-                const mph_epilogue* epi, const float* post, cudaStream_t s) {
+                const mph_epilogue* epi, const float* post, cudaStream_t s, const float* partial) {
   if (!g || !in || !out) return fail(MPH_EINVAL, "spmm: null argument");
   if (w <= 0 || w % 4 || ld_in % 4 || ld_out % 4 || ld_in < w || ld_out < w)
     return fail(MPH_EINVAL, "spmm: w, ld_in, ld_out must be multiples of 4 with ld >= w (w=%d)", w);
@@ -512,8 +514,8 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   const uint32_t allowed =
       MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE | MPH_EPI_TF32 | MPH_EPI_BF16;
   if (epi && (epi->flags & ~allowed)) return fail(MPH_EINVAL, "spmm: unsupported epilogue flags 0x%x", epi->flags);
-  if (epi && (epi->flags & MPH_EPI_BF16) && part != -1)
-    return fail(MPH_ENOTSUP, "spmm: BF16 output needs whole rows (part -1)");
+  if (epi && (epi->flags & MPH_EPI_BF16) && part != -1 && !(part == 1 && partial))
+    return fail(MPH_ENOTSUP, "spmm: BF16 output needs whole rows (part -1), or part 1 over FP32 partial sums");
   if (epi && (epi->flags & MPH_EPI_BIAS) && (!epi->bias || (reinterpret_cast<uintptr_t>(epi->bias) & 15)))
     return fail(MPH_EINVAL, "spmm: bias must be non-null and 16-byte aligned");
   if (epi && (epi->flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "spmm: null row_scale");
@@ -535,6 +537,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.n_rows = g->n_rows;
   a.nv4 = w / 4;
   a.part = part;
+  a.partial = part == 1 ? partial : nullptr;
   a.epi.flags = epi ? epi->flags : 0u;
   a.epi.bias = epi ? epi->bias : nullptr;
   a.epi.row_scale = epi ? epi->row_scale : nullptr;

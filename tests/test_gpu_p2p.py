@@ -34,7 +34,15 @@ CASES = {
     "af_layer1_w3": (3, dict(n=3500, nnz_a=40000, f=24, c=6, seed=4, alpha=2.3, mu=0.4), (24, 64, 48, 6), 0, 0.0, 6),
     "sparse_dropout_w2": (2, dict(n=2500, nnz_a=20000, f=300, c=4, kind="binary", density=0.03, seed=5),
                           (300, 40, 4), 1, 0.25, 6),
+    # BF16 GEMM operands: hidden H / backward G stored bf16, the two SpMM parts meet in FP32 scratch
+    "bf16_af_w3": (3, dict(n=3500, nnz_a=40000, f=24, c=6, seed=4, alpha=2.3, mu=0.4), (24, 64, 48, 6), 0, 0.1, 6,
+                   "bf16"),
 }
+
+
+def _case(case):
+    c = CASES[case]
+    return c[:6] + ((c[6] if len(c) > 6 else "tf32"),)
 
 
 def _free_port():
@@ -51,7 +59,7 @@ def _worker(rank, world, port, case, result_q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         import paper_2512_01678_b200 as P
-        _, kw, dims, force_mode, p_drop, epochs = CASES[case]
+        _, kw, dims, force_mode, p_drop, epochs, prec = _case(case)
         w = make_small(**kw)
         n = kw["n"]
         gfull = P.Graph(w["src"], w["dst"], n)
@@ -64,7 +72,7 @@ def _worker(rank, world, port, case, result_q):
 
         def model():
             f = P.Features(torch.from_numpy(np.ascontiguousarray(w["X"][r0:r1])).cuda(), force_mode=force_mode)
-            m = P.GCN(g, f, dims, dropout_p=p_drop, dropout_seed=11, comm="p2p")
+            m = P.GCN(g, f, dims, dropout_p=p_drop, dropout_seed=11, comm="p2p", precision=prec)
             m.init_xavier(42)
             m.set_labels(y, n_lab_global=n)
             return f, m
@@ -133,7 +141,7 @@ def _unpack(flat, offsets, ld_w, dims):
 
 @pytest.mark.parametrize("case", list(CASES))
 def test_p2p_epochs_match_oracle(case):
-    world, kw, dims, force_mode, p_drop, epochs = CASES[case]
+    world, kw, dims, force_mode, p_drop, epochs, prec = _case(case)
     res = _run(case)
     for r in res:
         assert r["status"] == (0, 0), f"rank {r['rank']}: a peer-memory wait timed out"
@@ -157,7 +165,7 @@ def test_p2p_epochs_match_oracle(case):
     got = np.array(res[0]["losses"])
     assert np.all(np.abs(got - ref_losses) <= 1e-3 * np.abs(ref_losses)), (got, ref_losses)
     Ws, bs = oracle.xavier_init(dims, 42)
-    Z, cache = oracle.forward(g, w["X"], Ws, bs, p_drop, 11, 1)
+    Z, cache = oracle.forward(g, w["X"], Ws, bs, p_drop, 11, 1, operand_rounding=None if prec == "tf32" else "bf16")
     _, dZ = oracle.softmax_ce(Z, w["y"])
     dWs, dbs = oracle.backward(g, cache, Ws, dZ)
     gW, gb = _unpack(res[0]["grads1"], res[0]["offsets"], res[0]["ld_w"], dims)
