@@ -35,7 +35,7 @@ CASES = {
     "sparse_dropout_w2": (2, dict(n=2500, nnz_a=20000, f=300, c=4, kind="binary", density=0.03, seed=5),
                           (300, 40, 4), 1, 0.25, 6),
     # BF16 GEMM operands: hidden H / backward G stored bf16, the two SpMM parts meet in FP32 scratch
-    "bf16_af_w3": (3, dict(n=3500, nnz_a=40000, f=24, c=6, seed=4, alpha=2.3, mu=0.4), (24, 64, 48, 6), 0, 0.1, 6,
+    "bf16_tf_w3": (3, dict(n=3500, nnz_a=40000, f=40, c=5, seed=6, alpha=2.3, mu=0.4), (40, 32, 16, 5), 0, 0.1, 6,
                    "bf16"),
 }
 
