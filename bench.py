@@ -290,11 +290,17 @@ def _max_over_ranks(torch, dist, v: float) -> float:
     return tt.item()
 
 
+_WORKLOADS = {}
+
+
 def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full: bool):
     """Build one workload and time it.  full=False skips e2e and the CPU baseline (secondary)."""
     t_setup = time.perf_counter()
     from synth.generate import make_workload
-    w = make_workload(config)
+    if config not in _WORKLOADS:   # one generation per config per run (secondary lines reuse it)
+        _WORKLOADS.clear()
+        _WORKLOADS[config] = make_workload(config)
+    w = _WORKLOADS[config]
     t_gen = time.perf_counter() - t_setup
     t0 = time.perf_counter()
     bounds = None
@@ -528,11 +534,14 @@ def run_ours(args):
     comm = (P.Comm(world, rank) if args.comm == "nccl" else "p2p") if world > 1 else None
     main = _measure(P, L, torch, dist, C, args, args.config, world, rank, local, comm, full=True)
     secondary = {}
-    for cfgname in ([] if args.secondary == "none" else args.secondary.split(",")):
-        if cfgname and cfgname != args.config:
-            r = _measure(P, L, torch, dist, C, args, cfgname, world, rank, local, comm, full=False)
-            secondary[cfgname] = {k: r[k] for k in ("value", "config", "roofline", "kernels", "gpu_launches",
-                                                    "final_loss", "clocks", "epoch_ms", "_spmm_geometry")}
+    for spec in ([] if args.secondary == "none" else args.secondary.split(",")):
+        cfgname, _, prec = spec.partition(":")   # "products" or "reddit:bf16" (GEMM operand precision)
+        prec = prec or args.precision
+        if cfgname and (cfgname != args.config or prec != args.precision):
+            sargs = argparse.Namespace(**{**vars(args), "precision": prec})
+            r = _measure(P, L, torch, dist, C, sargs, cfgname, world, rank, local, comm, full=False)
+            secondary[spec] = {k: r[k] for k in ("value", "config", "roofline", "kernels", "gpu_launches",
+                                                 "final_loss", "clocks", "epoch_ms", "_spmm_geometry")}
     peaks = _gather_peaks(L, torch) if (world == 1 and not args.no_probe) else None
     peak_hbm = _peaks()[0]
     l2g = peaks["l2_resident_64MB"] if peaks else None
@@ -590,8 +599,9 @@ def main():
     ap.add_argument("--no-probe", action="store_true", help="skip the gather-bandwidth probe")
     ap.add_argument("--graph", action="store_true",
                     help="time CUDA-graph replays of a captured epoch (1 GPU; launch-bound configs)")
-    ap.add_argument("--secondary", default="products",
-                    help="comma-separated extra workloads timed in the same run (device time + roofline), or none")
+    ap.add_argument("--secondary", default="reddit:bf16,products,products:bf16",
+                    help="comma-separated extra workloads timed in the same run (device time + roofline), each "
+                         "'config' or 'config:precision', or none")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
