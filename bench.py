@@ -446,6 +446,8 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                                           if dom == "sparse_feat" else "A + B + C bytes once"),
                     "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_ms": kd["avg_launch_ms"],
                     "share_of_epoch": kd["ms_per_epoch"] / ms}
+        if "halo" in kernels:   # SURVEY d.4: halo bytes per rank / time / 900 GB/s (NVLink 5, one direction)
+            roofline["halo_frac_of_nvlink_900GBps"] = kernels["halo"]["algorithmic_GBps"] / 900.0
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
