@@ -367,9 +367,12 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   p.n_tiles = (int)ceil_div(M, kBM);
   p.colsum_rows = colsum_fill ? p.n_tiles : 0;  // rows beyond the grid are zero-filled only for the ABI
   const size_t stage_bytes = kATileBytes + (size_t)BN * kBK * 4;
-  // small K: the mainloop is short and the epilogue (C tile out, mask tile in) is the long pole,
-  // so it gets 8 warps; otherwise 4 warps leave room for a deeper operand ring
-  p.n_epi = (p.num_kb <= 4 && BN >= 64) ? 8 : 4;
+  // the epilogue (C tile out, mask tile in) is the long pole of these HBM-bound GEMMs: 8 warps
+  // (two per TMEM lane quarter) whenever there are at least two 32-column chunks per quarter.
+  // Measured on products: K <= 128 launches -10..-25 %, K = 256 launches -3 % even with the
+  // operand ring cut to 2 stages.  MPH_GEMM_EPI=4 restores 4 warps (experiments).
+  p.n_epi = BN >= 64 ? 8 : 4;
+  if (const char* ev = getenv("MPH_GEMM_EPI")) p.n_epi = (atoi(ev) == 8 && BN >= 64) ? 8 : 4;
   const size_t epi_bytes = (size_t)p.n_epi * kEpiBufs * kEpiChunkBytes;
   const size_t fixed = 1024 + epi_bytes + (size_t)BN * sizeof(float) +
                        (size_t)(2 * 8 + 4 + p.n_epi * kEpiBufs) * 8 + 16 + 4 * (size_t)BN * sizeof(float);
