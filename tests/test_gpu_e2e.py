@@ -254,3 +254,30 @@ def test_async_feature_upload_matches_sync(P, dims, agg):
         runs.append(([x.item() for x in losses], m.params_flat.clone()))
     assert runs[0][0] == runs[1][0]
     assert torch.equal(runs[0][1], runs[1][1])
+
+
+@pytest.mark.parametrize("case", ["single_node", "isolated_af", "isolated_bf16", "one_layer"])
+def test_degenerate_models(P, case):
+    """Degenerate shapes the method admits: a one-node graph without edges, many isolated nodes
+    (rows holding only the self loop) with an aggregate-first layer 1, the same in BF16, a
+    one-layer model; N not a multiple of any tile.  10-epoch trajectory against the oracle."""
+    rng = np.random.default_rng(hash(case) % 2 ** 31)
+    if case == "single_node":
+        n, dims, src, dst, prec = 1, (3, 2), np.zeros(0, np.int32), np.zeros(0, np.int32), "tf32"
+    else:
+        n = 131
+        src = rng.integers(0, 31, 60).astype(np.int32)          # nodes 31..130 stay isolated
+        dst = rng.integers(0, 31, 60).astype(np.int32)
+        dims, prec = {"isolated_af": ((5, 8, 3), "tf32"), "isolated_bf16": ((16, 24, 3), "bf16"),
+                      "one_layer": ((6, 4), "tf32")}[case]
+    X = (rng.integers(-64, 64, (n, dims[0])) / 64.0).astype(np.float32)
+    y = rng.integers(0, dims[-1], n).astype(np.int32)
+    g = P.Graph(src, dst, n)
+    f = P.Features(cuda(X), force_mode=0)
+    m = P.GCN(g, f, dims, precision=prec)
+    m.init_xavier(42)
+    m.set_labels(cuda(y))
+    got = _gpu_losses(m, 10)
+    ref_g = oracle.graph_build(src, dst, n)
+    ref, _ = oracle.train(ref_g, X, y, dims, epochs=10, seed=42)
+    _check_traj(got, ref)
