@@ -547,9 +547,10 @@ def run_ours(args):
     peaks = _gather_peaks(L, torch) if (world == 1 and not args.no_probe) else None
     peak_hbm = _peaks()[0]
     l2g = peaks["l2_resident_64MB"] if peaks else None
+    l2_bytes = int(getattr(torch.cuda.get_device_properties(local), "L2_cache_size", 126 * 2 ** 20))
     for r in [main] + list(secondary.values()):
         if r.get("roofline") is not None:
-            fr = _spmm_fractions(r, peak_hbm, l2g)
+            fr = _spmm_fractions(r, peak_hbm, l2g, l2_bytes)
             if fr:
                 r["roofline"]["spmm_fractions"] = fr
         r.pop("_spmm_geometry", None)
@@ -570,6 +571,9 @@ def run_ours(args):
             "clocks": main["clocks"], "kernels": main["kernels"], "final_loss": main["final_loss"],
             "epoch_ms": main["epoch_ms"],
             "setup_s": main["setup_s"], "secondary": secondary or None,
+            # SURVEY d.4: the nominal figures beside the measured ones, and the L2 size read at run time
+            "device": {"l2_bytes": l2_bytes, "nominal": {"hbm_TBps": 8.0, "nvlink_GBps_per_direction": 900,
+                                                         "tf32_dense_PFLOPs": 1.1, "bf16_dense_PFLOPs": 2.25}},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
