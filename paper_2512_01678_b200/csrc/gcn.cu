@@ -72,6 +72,10 @@ struct mph_gcn {
   bool fwd_done = false, loss_done = false;
   // P > 1: NCCL runs on its own stream, ordered against the compute stream by events
   cudaStream_t cs = nullptr;
+  // weight-gradient GEMMs run on a side stream: off the critical path G_l -> dH -> next SpMM, their
+  // HBM traffic overlaps the (L2- or latency-bound) backward aggregations
+  cudaStream_t ss = nullptr;
+  cudaEvent_t ev_g = nullptr, ev_ss = nullptr;
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_grad = nullptr, ev_comm_done = nullptr, ev_loss = nullptr;
   cudaEvent_t ev_copied = nullptr, ev_derived = nullptr;  // mph_gcn_upload_features_async pipeline
   // CUDA-graph replay of one epoch: step counter and loss live in device memory
@@ -119,6 +123,9 @@ static void gcn_free(mph_gcn* m) {
   for (cudaEvent_t e : {m->ev_pack, m->ev_halo, m->ev_grad, m->ev_comm_done, m->ev_loss, m->ev_copied, m->ev_derived})
     if (e) cudaEventDestroy(e);
   if (m->cs) cudaStreamDestroy(m->cs);
+  if (m->ss) cudaStreamDestroy(m->ss);
+  for (cudaEvent_t e : {m->ev_g, m->ev_ss})
+    if (e) cudaEventDestroy(e);
   if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
   if (m->graph) cudaGraphDestroy(m->graph);
   dev_free(m->t_dev);
@@ -351,6 +358,7 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
     Layer& l = m->layers[li];
     GradMirror mir{};
     const GradMirror* mirp = nullptr;  // set when this layer's dW GEMM writes every rank's slab itself
+    cudaStream_t gs = s;               // the stream that finishes [dW_l | db_l]
     const float* Hin = li == 0 ? m->Xr : m->layers[li - 1].out;
     const int ld_in = li == 0 ? m->f->P : m->layers[li - 1].pout;
     const float* Gsrc;  // gradient w.r.t. the transform output (TF) or Z (AF)
@@ -372,19 +380,25 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
         MPH_TRY(sparse_xtg_launch(m->f, l.G, l.pout, l.pout, m->grads + l.off_w, l.pout, s));
       } else {
         MPH_TRY(grad_mirror(m, li, &mir, &mirp));
+        MPH_CUDA_TRY(cudaEventRecord(m->ev_g, s));  // G_l (and db_l) are final
+        MPH_CUDA_TRY(cudaStreamWaitEvent(m->ss, m->ev_g, 0));
+        gs = m->ss;
         MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, Hin, ld_in, l.G, l.pout, m->grads + l.off_w, l.pout, m->ws,
-                          m->ws_bytes, s, mirp, m->bf16));
+                          m->ws_bytes, gs, mirp, m->bf16));
       }
     } else {
       // AF layer 1: dZ_1 (unscaled) is the gradient of Z = Y·W + b
       Gsrc = l.dZ;
       MPH_TRY(grad_mirror(m, li, &mir, &mirp));
+      MPH_CUDA_TRY(cudaEventRecord(m->ev_g, s));
+      MPH_CUDA_TRY(cudaStreamWaitEvent(m->ss, m->ev_g, 0));
+      gs = m->ss;
       MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, l.Y, l.pin, l.dZ, l.pout, m->grads + l.off_w, l.pout, m->ws,
-                        m->ws_bytes, s, mirp, m->bf16));
+                        m->ws_bytes, gs, mirp, m->bf16));
     }
     // [dW_l | db_l] complete (db_l came from the loss or the layer above): reduce it across ranks
     // while this layer's dH and the layers below proceed (a11)
-    MPH_TRY(grad_allreduce_async(m, li, s, mirp != nullptr));
+    MPH_TRY(grad_allreduce_async(m, li, gs, mirp != nullptr));
     if (li > 0) {
       // a8: dZ_{l-1} = (G·W^T) ⊙ 1[H_{l-1} > 0] (/(1-p)), db_{l-1} as column sums, then the dinv
       // pre-scale for the next backward SpMM (TF) — all in one GEMM epilogue.
@@ -405,6 +419,9 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
                                  s));
     }
   }
+  // the optimizer needs every dW: join the side stream
+  MPH_CUDA_TRY(cudaEventRecord(m->ev_ss, m->ss));
+  MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_ss, 0));
   if (m->world > 1) {  // Adam needs every summed gradient segment
     if (m->p2p) MPH_TRY(p2p_signal(m->p2p, kSlotGrad, true, 1, 0, m->cs));  // all my slabs are pushed
     MPH_CUDA_TRY(cudaEventRecord(m->ev_comm_done, m->cs));
@@ -591,6 +608,10 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     // P2P: the ghost rows of dinv ⊙ X arrive in mph_gcn_p2p_open, once the peers are mapped
     if (world > 1 && !p2p && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
   }
+  e = cudaStreamCreateWithFlags(&m->ss, cudaStreamNonBlocking);
+  for (cudaEvent_t* ev : {&m->ev_g, &m->ev_ss})
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create side stream: %s", cudaGetErrorString(e)));
   if (world > 1) {
     e = cudaStreamCreateWithFlags(&m->cs, cudaStreamNonBlocking);
     for (cudaEvent_t* ev : {&m->ev_pack, &m->ev_halo, &m->ev_grad, &m->ev_comm_done, &m->ev_loss})
