@@ -76,6 +76,7 @@ struct mph_gcn {
   // HBM traffic overlaps the (L2- or latency-bound) backward aggregations
   cudaStream_t ss = nullptr;
   cudaEvent_t ev_g = nullptr, ev_ss = nullptr;
+  bool side_tn = false;  // set at create: only when the aggregation operands are small (see there)
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_grad = nullptr, ev_comm_done = nullptr, ev_loss = nullptr;
   cudaEvent_t ev_copied = nullptr, ev_derived = nullptr;  // mph_gcn_upload_features_async pipeline
   // CUDA-graph replay of one epoch: step counter and loss live in device memory
@@ -340,6 +341,7 @@ static int do_loss(mph_gcn* m, double* loss_d, cudaStream_t s) {
 
 static int do_backward(mph_gcn* m, cudaStream_t s) {
   if (!m->loss_done) return fail(MPH_ESTATE, "backward without a matching forward+loss (S:353)");
+  bool forked = false;  // weight-gradient GEMMs sent to the side stream this pass
   const mph_graph* g = m->g;
   for (int li = m->L - 1; li >= 0 && m->agg == MPH_AGG_MAX; --li) {
     // R7: Z = Y·W + b:  dW = Yᵀ·dZ;  dY = dZ·Wᵀ;  dZ_{l-1} = route(dY, arg) ⊙ ReLU'(H_{l-1}) (/(1-p))
@@ -380,9 +382,12 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
         MPH_TRY(sparse_xtg_launch(m->f, l.G, l.pout, l.pout, m->grads + l.off_w, l.pout, s));
       } else {
         MPH_TRY(grad_mirror(m, li, &mir, &mirp));
-        MPH_CUDA_TRY(cudaEventRecord(m->ev_g, s));  // G_l (and db_l) are final
-        MPH_CUDA_TRY(cudaStreamWaitEvent(m->ss, m->ev_g, 0));
-        gs = m->ss;
+        if (m->side_tn) {
+          MPH_CUDA_TRY(cudaEventRecord(m->ev_g, s));  // G_l (and db_l) are final
+          MPH_CUDA_TRY(cudaStreamWaitEvent(m->ss, m->ev_g, 0));
+          gs = m->ss;
+          forked = true;
+        }
         MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, Hin, ld_in, l.G, l.pout, m->grads + l.off_w, l.pout, m->ws,
                           m->ws_bytes, gs, mirp, m->bf16));
       }
@@ -390,9 +395,12 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       // AF layer 1: dZ_1 (unscaled) is the gradient of Z = Y·W + b
       Gsrc = l.dZ;
       MPH_TRY(grad_mirror(m, li, &mir, &mirp));
-      MPH_CUDA_TRY(cudaEventRecord(m->ev_g, s));
-      MPH_CUDA_TRY(cudaStreamWaitEvent(m->ss, m->ev_g, 0));
-      gs = m->ss;
+      if (m->side_tn) {
+        MPH_CUDA_TRY(cudaEventRecord(m->ev_g, s));
+        MPH_CUDA_TRY(cudaStreamWaitEvent(m->ss, m->ev_g, 0));
+        gs = m->ss;
+        forked = true;
+      }
       MPH_TRY(gemm_tn_p(l.pin, l.pout, g->n_rows, l.Y, l.pin, l.dZ, l.pout, m->grads + l.off_w, l.pout, m->ws,
                         m->ws_bytes, gs, mirp, m->bf16));
     }
@@ -419,9 +427,10 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
                                  s));
     }
   }
-  // the optimizer needs every dW: join the side stream
-  MPH_CUDA_TRY(cudaEventRecord(m->ev_ss, m->ss));
-  MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_ss, 0));
+  if (forked) {  // the optimizer needs every dW: join the side stream
+    MPH_CUDA_TRY(cudaEventRecord(m->ev_ss, m->ss));
+    MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_ss, 0));
+  }
   if (m->world > 1) {  // Adam needs every summed gradient segment
     if (m->p2p) MPH_TRY(p2p_signal(m->p2p, kSlotGrad, true, 1, 0, m->cs));  // all my slabs are pushed
     MPH_CUDA_TRY(cudaEventRecord(m->ev_comm_done, m->cs));
@@ -607,6 +616,14 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     if ((rc = rowscale_launch(f->X, f->P, m->fpre, (int)nr, l.pin, m->Xs, l.pin, 0, s))) return bail(rc);
     // P2P: the ghost rows of dinv ⊙ X arrive in mph_gcn_p2p_open, once the peers are mapped
     if (world > 1 && !p2p && (rc = mph_halo_exchange(g, comm, m->Xs, l.pin, l.pin, s))) return bail(rc);
+  }
+  // Side-stream weight gradients pay off when the backward aggregations leave HBM idle (operands
+  // L2-resident or small: reddit -0.3 %, arxiv -4 %); next to HBM-bound aggregations (products,
+  // 2.5 GB operands) the two compete and the epoch gets slower (+3 %), so they stay in line there.
+  {
+    int wmax2 = 0;
+    for (const auto& l : m->layers) wmax2 = std::max(wmax2, l.pout);
+    m->side_tn = (double)nc * wmax2 * 4.0 <= 512.0 * (1 << 20);
   }
   e = cudaStreamCreateWithFlags(&m->ss, cudaStreamNonBlocking);
   for (cudaEvent_t* ev : {&m->ev_g, &m->ev_ss})
