@@ -49,7 +49,8 @@ struct SpmmArgs {
   int* counter;
   int n_items;
   int ld_in, ld_out, n_rows, nv4, part;
-  int row_slots;  // 1: narrow rows of a low-degree graph -> k_spmm_rows
+  int row_slots;   // 1: narrow rows of a low-degree graph -> k_spmm_rows
+  int mid_degree;  // 1: mean degree in [16, 64) (dispatch of 48-wide rows)
   const float* partial;  // part 1 with a BF16 output: part 0's FP32 sums (row stride nv4·4), else nullptr
   EpiDev epi;
 };
@@ -494,7 +495,13 @@ static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
   if (nv4 <= 2) return launch_spmm<2, 1, HAS_VAL>(a, s);
   if (nv4 <= 4) return launch_spmm<4, 1, HAS_VAL>(a, s);
   if (nv4 <= 8) return launch_spmm<8, 1, HAS_VAL>(a, s);
-  if (nv4 <= 12) return launch_spmm_u<4, 3, HAS_VAL>(a, s);
+  if (nv4 <= 12) {
+    // 48-wide rows: 4 lanes x 3 float4 (8 edge slots) where rows are long (reddit: the shuffle
+    // reduction is amortised), 16 lanes x 1 float4 with 12 active (2 slots, a third of the
+    // cross-slot reduction) at moderate degree (products, mean 26: -1.7 % epoch)
+    if (a.mid_degree) return launch_spmm_u<16, 1, HAS_VAL>(a, s);
+    return launch_spmm_u<4, 3, HAS_VAL>(a, s);
+  }
   if (nv4 <= 16) return launch_spmm_u<16, 1, HAS_VAL>(a, s);
   if (nv4 <= 32) return launch_spmm_u<32, 1, HAS_VAL>(a, s);
   if (nv4 <= 64) return launch_spmm_u<32, 2, HAS_VAL>(a, s);
@@ -550,6 +557,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
     const char* rs_env = getenv("MPH_SPMM_ROWS");
     const bool low_degree = g->nnz < kRowSlotMaxDegree * (int64_t)g->n_rows;
     a.row_slots = rs_env ? (atoi(rs_env) != 0) : low_degree;
+    a.mid_degree = !low_degree && g->nnz < 64 * (int64_t)g->n_rows;
   }
   // Column slabs: on graphs with a mean degree >= 16, rows of w = 128 / 256 are aggregated as two
   // halves, one launch each, so the slab of the gathered operand that a community of rows
