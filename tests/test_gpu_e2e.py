@@ -217,11 +217,13 @@ def test_cuda_graph_replay_bitwise_equals_eager(P, dropout_p):
     assert mb.graph_step.item() == 6
 
 
-@pytest.mark.parametrize("dims,agg", [((24, 32, 5), "gcn"), ((24, 16, 5), "gcn"), ((24, 16, 5), "max")])
-def test_async_feature_upload_matches_sync(P, dims, agg):
+@pytest.mark.parametrize("dims,agg,prec", [((24, 32, 5), "gcn", "tf32"), ((24, 16, 5), "gcn", "tf32"),
+                                            ((24, 16, 5), "max", "tf32"), ((24, 16, 5), "gcn", "bf16")])
+def test_async_feature_upload_matches_sync(P, dims, agg, prec):
     """mph_gcn_upload_features_async (copy stream, prefetch of the next step's X while an epoch
     runs) gives bitwise the same training as the synchronous upload, for an aggregate-first layer 1
-    (pre-scaled copy), a transform-first one (TF32 copy) and max aggregation (MAX(X))."""
+    (pre-scaled copy), a transform-first one (TF32 / BF16 operand copy, double-buffered and derived
+    on the copy stream) and max aggregation (MAX(X))."""
     from paper_2512_01678_b200 import _lib as L
     w = make_small(3000, 20000, 24, 5, seed=12)
     Pw = P.pad_width(24)
@@ -235,7 +237,7 @@ def test_async_feature_upload_matches_sync(P, dims, agg):
     for mode in ("sync", "async"):
         g = P.Graph(w["src"], w["dst"], 3000)
         f = P.Features(cuda(w["X"]), force_mode=0)
-        m = P.GCN(g, f, dims, aggregator=agg)
+        m = P.GCN(g, f, dims, aggregator=agg, precision=prec)
         m.init_xavier(42)
         m.set_labels(cuda(w["y"].astype(np.int32)))
         cs = torch.cuda.Stream()
