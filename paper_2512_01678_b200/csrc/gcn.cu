@@ -79,11 +79,6 @@ struct mph_gcn {
   bool side_tn = false;  // set at create: only when the aggregation operands are small (see there)
   cudaEvent_t ev_pack = nullptr, ev_halo = nullptr, ev_grad = nullptr, ev_comm_done = nullptr, ev_loss = nullptr;
   cudaEvent_t ev_copied = nullptr, ev_derived = nullptr;  // mph_gcn_upload_features_async pipeline
-  // double-buffered operand copy of X (transform-first dense layer 1): the next step's copy is
-  // derived on the copy stream while the current epoch still reads the other buffer
-  float* Xr_buf[2] = {nullptr, nullptr};
-  cudaEvent_t ev_xr_free[2] = {nullptr, nullptr};
-  int xr_cur = 0;
   // CUDA-graph replay of one epoch: step counter and loss live in device memory
   int32_t* t_dev = nullptr;
   double* loss_dev = nullptr;
@@ -122,14 +117,7 @@ static void gcn_free(mph_gcn* m) {
   if (m->own_v) dev_free(m->v);
   dev_free(m->wt);
   dev_free(m->wr);
-  if (m->Xr_buf[0] || m->Xr_buf[1]) {
-    dev_free(m->Xr_buf[0]);
-    dev_free(m->Xr_buf[1]);
-  } else {
-    dev_free(m->Xr);
-  }
-  for (cudaEvent_t e : m->ev_xr_free)
-    if (e) cudaEventDestroy(e);
+  dev_free(m->Xr);
   dev_free(m->part0);
   if (!in_arena(m, m->Xs)) dev_free(m->Xs);
   if (m->own_ws) dev_free(m->ws);
@@ -794,34 +782,6 @@ extern "C" int mph_gcn_upload_features_async(mph_gcn* m, const float* X_h, int32
     MPH_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_copied, cudaEventDisableTiming));
     MPH_CUDA_TRY(cudaEventCreateWithFlags(&m->ev_derived, cudaEventDisableTiming));
     MPH_CUDA_TRY(cudaEventRecord(m->ev_derived, s));
-  }
-  const bool xr_only = m->agg != MPH_AGG_MAX && m->layers[0].order == 0 && m->Xr && !m->graph_exec;
-  if (xr_only) {
-    // the copy and the derivation of the operand copy run on the copy stream, into the buffer
-    // the current epoch does not read; the compute stream switches buffers behind it
-    if (!m->Xr_buf[1]) {
-      const size_t n = (size_t)m->g->n_rows * m->f->P;
-      float* b = nullptr;
-      MPH_TRY(dev_alloc(&b, n));
-      MPH_CUDA_TRY(cudaMemsetAsync(b, 0, n * 4, s));
-      for (cudaEvent_t* ev : {&m->ev_xr_free[0], &m->ev_xr_free[1]})
-        MPH_CUDA_TRY(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
-      m->Xr_buf[0] = m->Xr;
-      m->Xr_buf[1] = b;
-      m->xr_cur = 0;
-      MPH_CUDA_TRY(cudaEventRecord(m->ev_xr_free[1], s));
-    }
-    const int nxt = 1 - m->xr_cur;
-    MPH_CUDA_TRY(cudaEventRecord(m->ev_xr_free[m->xr_cur], s));  // after every epoch enqueued so far
-    MPH_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev_xr_free[nxt], 0));  // its last reader has finished
-    MPH_TRY(copy_features(m->f, X_h, ld_h, cs));
-    MPH_TRY(rowscale_launch(m->f->X, m->f->P, nullptr, m->g->n_rows, m->f->P, m->Xr_buf[nxt], m->f->P,
-                            m->bf16 ? 2 : 1, cs));
-    MPH_CUDA_TRY(cudaEventRecord(m->ev_copied, cs));
-    MPH_CUDA_TRY(cudaStreamWaitEvent(s, m->ev_copied, 0));
-    m->Xr = m->Xr_buf[nxt];
-    m->xr_cur = nxt;
-    return MPH_OK;
   }
   MPH_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev_derived, 0));  // the previous upload has been consumed
   MPH_TRY(copy_features(m->f, X_h, ld_h, cs));

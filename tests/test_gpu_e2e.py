@@ -222,8 +222,7 @@ def test_cuda_graph_replay_bitwise_equals_eager(P, dropout_p):
 def test_async_feature_upload_matches_sync(P, dims, agg, prec):
     """mph_gcn_upload_features_async (copy stream, prefetch of the next step's X while an epoch
     runs) gives bitwise the same training as the synchronous upload, for an aggregate-first layer 1
-    (pre-scaled copy), a transform-first one (TF32 / BF16 operand copy, double-buffered and derived
-    on the copy stream) and max aggregation (MAX(X))."""
+    (pre-scaled copy), a transform-first one (TF32 / BF16 operand copy) and max aggregation (MAX(X))."""
     from paper_2512_01678_b200 import _lib as L
     w = make_small(3000, 20000, 24, 5, seed=12)
     Pw = P.pad_width(24)
