@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="reddit")
 ap.add_argument("--epochs", type=int, default=3)
 ap.add_argument("--agg", default="gcn", choices=["gcn", "sum", "mean", "max"])
+ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16"])
 a = ap.parse_args()
 w = make_workload(a.config)
 cfg = w["cfg"]
@@ -23,7 +24,7 @@ if w["X"] is not None:
 else:
     ptr, idx, val = w["X_csr"]
     f = P.Features.from_csr(ptr, idx, val, (cfg.num_nodes, cfg.num_features))
-m = P.GCN(g, f, cfg.dims, aggregator=a.agg)
+m = P.GCN(g, f, cfg.dims, aggregator=a.agg, precision=a.precision)
 m.init_xavier(42)
 m.set_labels(torch.from_numpy(w["y"]).cuda())
 torch.cuda.synchronize()
