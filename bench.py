@@ -203,7 +203,7 @@ def _relabel_workload(P, torch, w, world, how):
     return out, bounds
 
 
-def _build_model(P, torch, w, world, rank, comm, bounds=None, precision="tf32"):
+def _build_model(P, torch, w, world, rank, comm, bounds=None, precision="tf32", aggregator="gcn"):
     cfg = w["cfg"]
     n = cfg.num_nodes
     X = w["X"]
@@ -218,7 +218,7 @@ def _build_model(P, torch, w, world, rank, comm, bounds=None, precision="tf32"):
     if world == 1:
         g = P.Graph(w["src"], w["dst"], n)
         f = features(0, n)
-        m = P.GCN(g, f, cfg.dims, precision=precision)
+        m = P.GCN(g, f, cfg.dims, precision=precision, aggregator=aggregator)
         y = torch.from_numpy(w["y"]).cuda()
         own = (0, n)
         extra = {}
@@ -233,7 +233,7 @@ def _build_model(P, torch, w, world, rank, comm, bounds=None, precision="tf32"):
         g = P.Graph.from_plan(plan)
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
         f = features(r0, r1)
-        m = P.GCN(g, f, cfg.dims, comm=comm, precision=precision)
+        m = P.GCN(g, f, cfg.dims, comm=comm, precision=precision, aggregator=aggregator)
         y = torch.from_numpy(np.ascontiguousarray(w["y"][r0:r1])).cuda()
         own = (r0, r1)
         extra = {"n_ghost": plan.n_ghost, "halo_rows_sent": plan.n_send}
@@ -306,7 +306,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
     bounds = None
     if world > 1 and args.partition != "1d":
         w, bounds = _relabel_workload(P, torch, w, world, args.partition)
-    g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm, bounds, args.precision)
+    g, f, m, y, own, extra = _build_model(P, torch, w, world, rank, comm, bounds, args.precision, args.aggregator)
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     cfg = w["cfg"]
@@ -462,6 +462,7 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         "config": {**_config_common(argparse.Namespace(**{**vars(args), "config": config}), world),
                    "layer_order": ["AF" if o else "TF" for o in m.order],
                    "gemm_precision": args.precision,
+                   "aggregator": args.aggregator,
                    "cuda_graph": use_graph,
                    "l2": "inputs larger than L2 (X and col_idx > 126 MB); no flush" if cfg.num_nodes > 100000
                    else "small workload: operands L2-resident across epochs (no flush)",
@@ -595,6 +596,8 @@ def main():
     ap.add_argument("--comm", default="p2p", choices=["nccl", "p2p"],
                     help="N > 1: NVLink peer-memory halo pulls with the gradient sum fused into the optimizer "
                          "(default; SURVEY §8(f) NEXT-1), or NCCL grouped send/recv + all-reduce")
+    ap.add_argument("--aggregator", default="gcn", choices=["gcn", "sum", "mean", "max"],
+                    help="aggregation scheme (SURVEY §8(f) NEXT-4; the north star's workloads are gcn)")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16"],
                     help="GEMM operands: TF32 (FP32 storage) or BF16 (GEMM-only tensors stored as bfloat16); "
                          "aggregation, loss and Adam are FP32 either way")

@@ -51,7 +51,9 @@ __device__ __forceinline__ void max_merge(float& b, int& a, float b2, int a2) {
   }
 }
 
-template <int LPR, int VPL>
+// U gathers per slot in flight per round (the max merge and the routed sum take them in ascending
+// edge order, so U changes nothing but the memory-level parallelism)
+template <int LPR, int VPL, int U>
 __device__ __forceinline__ void max_row(const MaxArgs& a, int row, int lane) {
   constexpr int ES = 32 / LPR;
   const int slot = lane / LPR, sub = lane % LPR;
@@ -66,11 +68,11 @@ __device__ __forceinline__ void max_row(const MaxArgs& a, int row, int lane) {
   for (int64_t base = s; base < e; base += 32) {
     const int nb = (int)min((int64_t)32, e - base);
     const int my_c = (base + lane < e) ? ldg_stream_i32(a.col + base + lane) : 0;
-    for (int k0 = 0; k0 < nb; k0 += 2 * ES) {
-      float4 x[2][VPL];
-      int cc[2];
+    for (int k0 = 0; k0 < nb; k0 += U * ES) {
+      float4 x[U][VPL];
+      int cc[U];
 #pragma unroll
-      for (int uu = 0; uu < 2; ++uu) {  // both gathers in flight before either is used
+      for (int uu = 0; uu < U; ++uu) {  // all U gathers in flight before any is used
         const int k = k0 + uu * ES + slot;
         const int c = __shfl_sync(0xffffffffu, my_c, k & 31);  // all lanes shuffle
         cc[uu] = k < nb ? c : INT_MAX;
@@ -79,7 +81,7 @@ __device__ __forceinline__ void max_row(const MaxArgs& a, int row, int lane) {
         for (int j = 0; j < VPL; ++j) x[uu][j] = (k < nb && sub + j * LPR < a.nv4) ? ldg_f4(p + j * LPR) : f4_zero();
       }
 #pragma unroll
-      for (int uu = 0; uu < 2; ++uu) {
+      for (int uu = 0; uu < U; ++uu) {
         if (cc[uu] == INT_MAX) continue;
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
@@ -115,7 +117,7 @@ __device__ __forceinline__ void max_row(const MaxArgs& a, int row, int lane) {
   }
 }
 
-template <int LPR, int VPL>
+template <int LPR, int VPL, int U>
 __device__ __forceinline__ void maxbwd_row(const MaxArgs& a, int row, int lane) {
   constexpr int ES = 32 / LPR;
   const int slot = lane / LPR, sub = lane % LPR;
@@ -126,11 +128,11 @@ __device__ __forceinline__ void maxbwd_row(const MaxArgs& a, int row, int lane) 
   for (int64_t base = s; base < e; base += 32) {
     const int nb = (int)min((int64_t)32, e - base);
     const int my_c = (base + lane < e) ? ldg_stream_i32(a.col + base + lane) : 0;
-    for (int k0 = 0; k0 < nb; k0 += 2 * ES) {
-      float4 x[2][VPL];
-      int4 ar[2][VPL];
+    for (int k0 = 0; k0 < nb; k0 += U * ES) {
+      float4 x[U][VPL];
+      int4 ar[U][VPL];
 #pragma unroll
-      for (int uu = 0; uu < 2; ++uu) {
+      for (int uu = 0; uu < U; ++uu) {
         const int k = k0 + uu * ES + slot;
         const int u = __shfl_sync(0xffffffffu, my_c, k & 31);
         const float4* p = reinterpret_cast<const float4*>(a.in + (int64_t)u * a.ld_in) + sub;
@@ -143,7 +145,7 @@ __device__ __forceinline__ void maxbwd_row(const MaxArgs& a, int row, int lane) 
         }
       }
 #pragma unroll
-      for (int uu = 0; uu < 2; ++uu)
+      for (int uu = 0; uu < U; ++uu)
 #pragma unroll
         for (int j = 0; j < VPL; ++j) {
           acc[j].x += ar[uu][j].x == row ? x[uu][j].x : 0.0f;
@@ -189,11 +191,12 @@ __global__ void __launch_bounds__(256) k_aggmax(MaxArgs a) {
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
+    constexpr int U = VPL == 1 ? 8 : (VPL == 2 ? 4 : 2);
     for (int row = rr.x; row < rr.y; ++row) {
       if (BWD)
-        maxbwd_row<LPR, VPL>(a, row, lane);
+        maxbwd_row<LPR, VPL, U>(a, row, lane);
       else
-        max_row<LPR, VPL>(a, row, lane);
+        max_row<LPR, VPL, U>(a, row, lane);
     }
   }
 }
