@@ -274,3 +274,23 @@ def test_p2p_reddit_fullsize_world2():
     Z, _ = oracle.forward(g, w["X"], Ws, bs)
     ref_loss, _ = oracle.softmax_ce(Z, w["y"])
     assert abs(res[0]["loss1"] - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss)), (res[0]["loss1"], ref_loss)
+
+
+@pytest.mark.slow
+def test_bench_two_ranks_share_device():
+    """bench.py's N > 1 code path end to end (torchrun, 2 ranks, P2P transport, max-over-ranks
+    timing, e2e) on one GPU via --share-device; the JSON line comes from rank 0."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(_free_port()), os.path.join(root, "bench.py"), "--gpus", "2",
+           "--share-device", "--comm", "p2p", "--config", "arxiv", "--steps", "3", "--warmup", "3",
+           "--secondary", "none", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
+    assert np.isfinite(line["final_loss"]) and line["e2e"]["value"] > 0
+    assert "comm p2p" in line["config"]["parallelism"]
