@@ -395,11 +395,15 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   MPH_TRY(make_tmap(&tb, Bt, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, kelems, (uint32_t)BN, CU_TENSOR_MAP_SWIZZLE_128B,
                     bf16));
   const bool out_bf = (flags & MPH_EPI_BF16) != 0, mask_bf = (flags & MPH_EPI_MASK_BF16) != 0;
-  MPH_TRY(make_tmap(&tcm, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, 32, 32,
-                    out_bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, out_bf));
+  // BF16 output in 64-column units (full 128-byte smem rows, half the TMA stores), when the width
+  // allows and a mask, if any, is BF16 too
+  p.wide = (out_bf && BN % 64 == 0 && (!(flags & MPH_EPI_MASK) || mask_bf)) ? 1 : 0;
+  const uint32_t cw = p.wide ? 64 : 32;
+  MPH_TRY(make_tmap(&tcm, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, cw, 32,
+                    (out_bf && !p.wide) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, out_bf));
   if (flags & MPH_EPI_MASK)
-    MPH_TRY(make_tmap(&tm, epi->mask_src, (uint64_t)N, (uint64_t)M, (uint64_t)epi->ld_mask, 32, 32,
-                      mask_bf ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, mask_bf));
+    MPH_TRY(make_tmap(&tm, epi->mask_src, (uint64_t)N, (uint64_t)M, (uint64_t)epi->ld_mask, cw, 32,
+                      (mask_bf && !p.wide) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, mask_bf));
   else
     tm = tcm;
   const size_t smem = fixed + (size_t)p.stages * stage_bytes;
