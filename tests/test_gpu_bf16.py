@@ -107,3 +107,17 @@ def test_bf16_graph_replay_and_refusals(P):
     with pytest.raises(MorphlingError) as e:
         P.GCN(g, f, dims, aggregator="max", precision="bf16")
     assert e.value.code == -9
+
+
+def test_bf16_aggregate_first_dropout_trajectory(P):
+    """BF16 with an aggregate-first layer 1 and dropout: the GEMM epilogue writes H_1 as 64-column
+    BF16 units (bias, ReLU, dropout) and reads the BF16 ReLU mask of dZ_1 the same way."""
+    w = make_small(2500, 30000, 40, 5, seed=9, alpha=2.2, mu=0.3)
+    dims = (40, 64, 32, 5)
+    _, _, m, _ = _model(P, w, dims, force_mode=0, dropout_p=0.2)
+    assert m.order[0] == 1
+    got = [m.train_epoch(t).item() for t in range(1, 11)]
+    ref_g = oracle.graph_build(w["src"], w["dst"], w["X"].shape[0])
+    ref, _ = oracle.train(ref_g, w["X"], w["y"], dims, epochs=10, seed=42, dropout_p=0.2, dropout_seed=3)
+    for t, (a, b) in enumerate(zip(got, ref), 1):
+        assert abs(a - b) <= 1e-3 * max(1.0, abs(b)), f"epoch {t}: gpu {a} vs oracle {b}"
