@@ -37,12 +37,21 @@ CASES = {
     # BF16 GEMM operands: hidden H / backward G stored bf16, the two SpMM parts meet in FP32 scratch
     "bf16_tf_w3": (3, dict(n=3500, nnz_a=40000, f=40, c=5, seed=6, alpha=2.3, mu=0.4), (40, 32, 16, 5), 0, 0.1, 6,
                    "bf16"),
+    # SGD with momentum and weight decay through the fused slab-sum optimizer
+    "sgd_w2": (2, dict(n=3000, nnz_a=36000, f=40, c=5, seed=7, alpha=2.1, mu=0.3), (40, 32, 5), 0, 0.0, 6, "tf32",
+               ("sgd", 0.05, 0.9, 1e-4)),
 }
 
 
 def _case(case):
     c = CASES[case]
     return c[:6] + ((c[6] if len(c) > 6 else "tf32"),)
+
+
+def _opt(case):
+    """(kind, lr, momentum, weight_decay) or None (Adam, the default)."""
+    c = CASES[case]
+    return c[7] if len(c) > 7 else None
 
 
 def _free_port():
@@ -79,14 +88,16 @@ def _worker(rank, world, port, case, result_q):
 
         fa, ma = model()
         losses, grads1 = [], None
+        spec = _opt(case)
+        cfg = P.optimizer(spec[0], lr=spec[1], momentum=spec[2], weight_decay=spec[3]) if spec else P.api.DEFAULT_ADAM
         for t in range(1, epochs + 1):
-            losses.append(ma.train_epoch(t).item())
+            losses.append(ma.train_epoch(t, cfg).item())
             if t == 1:
                 grads1 = ma.grads_flat.cpu().numpy().copy()   # the summed gradient of epoch 1
         # the same job as one eager epoch + a captured epoch replayed epochs-1 times
         fb, mb = model()
-        replayed = [mb.train_epoch(1).item()]
-        mb.graph_capture(2)
+        replayed = [mb.train_epoch(1, cfg).item()]
+        mb.graph_capture(2, cfg)
         for _ in range(epochs - 1):
             replayed.append(mb.replay().item())
         torch.cuda.synchronize()
@@ -160,8 +171,10 @@ def test_p2p_epochs_match_oracle(case):
     # distribution transparency against the single-graph FP64 oracle
     w = make_small(**kw)
     g = oracle.graph_build(w["src"], w["dst"], kw["n"])
+    spec = _opt(case)
+    okw = dict(optimizer=spec[0], lr=spec[1], momentum=spec[2], weight_decay=spec[3]) if spec else {}
     ref_losses, _ = oracle.train(g, w["X"], w["y"], dims, epochs=epochs, seed=42, dropout_p=p_drop,
-                                 dropout_seed=11)
+                                 dropout_seed=11, **okw)
     got = np.array(res[0]["losses"])
     assert np.all(np.abs(got - ref_losses) <= 1e-3 * np.abs(ref_losses)), (got, ref_losses)
     Ws, bs = oracle.xavier_init(dims, 42)
