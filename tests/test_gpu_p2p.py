@@ -188,7 +188,7 @@ def test_p2p_epochs_match_oracle(case):
             assert rel <= 2e-3, (case, l, rel)
 
 
-def _worker_reddit(rank, world, port, rows_per_rank, result_q):
+def _worker_fullsize(rank, world, port, rows_per_rank, result_q, config="reddit"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -197,7 +197,7 @@ def _worker_reddit(rank, world, port, rows_per_rank, result_q):
         torch.cuda.set_device(0)
         import paper_2512_01678_b200 as P
         from synth.generate import make_workload
-        w = make_workload("reddit")
+        w = make_workload(config)
         cfg = w["cfg"]
         n = cfg.num_nodes
         gfull = P.Graph(w["src"], w["dst"], n)
@@ -235,18 +235,23 @@ def _worker_reddit(rank, world, port, rows_per_rank, result_q):
 
 
 @pytest.mark.slow
-def test_p2p_reddit_fullsize_world2():
-    """The Reddit-shaped workload at full size as a 2-rank P2P job (each rank half the rows, ~120k
-    ghost rows pulled per exchange): epoch-1 loss against the FP64 oracle forward, sampled H_1
-    rows (aggregating ghost neighbours) against the oracle within the TF32 bound composed through
-    the aggregation, replicas bitwise identical after an Adam step."""
+@pytest.mark.parametrize("config", ["reddit", "products"])
+def test_p2p_fullsize_world2(config):
+    """BASELINE.json's full-size workloads as 2-rank P2P jobs (each rank half the rows; reddit
+    ~120k ghost rows per exchange, products an aggregate-first layer 1 whose dinv ⊙ X ghost rows
+    move at open): epoch-1 loss against the FP64 oracle forward, sampled H_1 rows (aggregating
+    ghost neighbours) against the oracle within the TF32 bound composed through the aggregation,
+    replicas bitwise identical after an optimizer step."""
+    import psutil
+    if config == "products" and psutil.virtual_memory().available < 64 * 2 ** 30:
+        pytest.skip("needs ~64 GB host RAM (two generators + the FP64 oracle at products scale)")
     import torch.multiprocessing as mp
     from synth.generate import make_workload
     world, per = 2, 24
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_reddit, args=(r, world, port, per, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker_fullsize, args=(r, world, port, per, q, config)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
@@ -263,10 +268,10 @@ def test_p2p_reddit_fullsize_world2():
     assert not errs, errs[0]
     res = [out[r] for r in range(world)]
     for r in res:
-        assert r["status"] == 0 and r["n_ghost"] > 100000
+        assert r["status"] == 0 and r["n_ghost"] > 50000
     assert res[0]["loss1"] == res[1]["loss1"] and res[0]["loss2"] == res[1]["loss2"]
     assert np.array_equal(res[0]["params"], res[1]["params"])
-    w = make_workload("reddit")
+    w = make_workload(config)
     cfg = w["cfg"]
     g = oracle.graph_build(w["src"], w["dst"], cfg.num_nodes)
     Ws, bs = oracle.xavier_init(cfg.dims, 42)
