@@ -446,8 +446,12 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                                           if dom == "sparse_feat" else "A + B + C bytes once"),
                     "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_ms": kd["avg_launch_ms"],
                     "share_of_epoch": kd["ms_per_epoch"] / ms}
-        if "halo" in kernels:   # SURVEY d.4: halo bytes per rank / time / 900 GB/s (NVLink 5, one direction)
-            roofline["halo_frac_of_nvlink_900GBps"] = kernels["halo"]["algorithmic_GBps"] / 900.0
+        if "halo" in kernels:   # SURVEY d.4: halo bytes per rank / time / NVLink (measured peer copy, 770 GB/s)
+            roofline["halo_frac_of_nvlink_peer_copy_770GBps"] = kernels["halo"]["algorithmic_GBps"] / 770.0
+        if dom == "spmm" and roofline["frac"] > 1.2:
+            roofline["note"] = ("frac > 1: the gathered operand is L2-resident, so the no-reuse algorithmic bytes "
+                                "(SURVEY d.3) exceed the DRAM traffic (see traffic); the binding ceiling is the L2 "
+                                "gather rate: frac_of_l2_gather_peak and spmm_fractions.time_efficiency_E")
 
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None

@@ -10,17 +10,17 @@ Per configuration and P (contiguous 1D partition, the bench default):
   * aggregation: T_spmm(1) · max_r Σd̃_r / Σd̃ (work ∝ edges of the busiest rank, P:550-555);
     the local-edge part (1 − cut fraction) overlaps the halo pull;
   * dense / elementwise kernels: T(1) · max_r n_r / N;
-  * halo: per exchange max_r ghost_r · 4·w bytes at NVLink 900 GB/s (one direction), exchanges of
+  * halo: per exchange max_r ghost_r · 4·w bytes at 770 GB/s (measured peer copy), exchanges of
     the epoch = the transform-first aggregation calls (an aggregate-first layer 1 exchanges its
     constant input once, at setup); exposed part = max(0, T_halo − T_local_part);
-  * gradient sum: every rank stores |θ| floats into every other rank's slab (P2P), at 900 GB/s.
+  * gradient sum: every rank stores |θ| floats into every other rank's slab (P2P), at 770 GB/s.
 """
 from __future__ import annotations
 
 import argparse
 import json
 
-NVLINK_GBPS = 900.0
+NVLINK_GBPS = 770.0  # measured peer copy per direction on this pool (B200_PROFILING.md); 900 nominal
 WIDTHS = {"reddit": ([128, 48], [0, 0]), "products": ([256, 256, 48], [1, 0, 0])}  # pout per layer, order
 PARAMS = {"reddit": 602 * 128 + 128 + 128 * 48 + 48, "products": 104 * 256 + 256 + 256 * 256 + 256 + 256 * 48 + 48}
 
