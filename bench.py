@@ -537,6 +537,16 @@ def run_ours(args):
     from paper_2512_01678_b200 import _lib as L
 
     L.mph_device_check(C.byref(C.c_int32()))
+    if world > 1 and args.comm == "p2p" and not args.share_device:
+        # peer memory needs every pair of the job's GPUs to reach each other (NVLink/NVSwitch); on a
+        # box without peer access the halo and gradient sum go through NCCL instead (said in config)
+        ok = all(torch.cuda.can_device_access_peer(local, d) for d in range(world) if d != local)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not int(flag.item()):
+            if rank == 0:
+                print("no peer access between the GPUs: --comm nccl", file=sys.stderr)
+            args.comm = "nccl"
     # N > 1: NCCL halo/all-reduce, or NVLink peer memory (NEXT-1: the model maps its peers itself)
     comm = (P.Comm(world, rank) if args.comm == "nccl" else "p2p") if world > 1 else None
     main = _measure(P, L, torch, dist, C, args, args.config, world, rank, local, comm, full=True)
