@@ -58,6 +58,20 @@ def test_no_cpu_fallback_without_gpu():
     assert e.value.name == "MPH_ECUDA"
 
 
+def test_package_refuses_to_import_without_the_library(tmp_path):
+    """No CPU fallback: a copy of the package without libmorphling.so fails at import."""
+    import shutil
+    import subprocess
+    import sys
+    pkg = os.path.join(ROOT, "paper_2512_01678_b200")
+    dst = tmp_path / "paper_2512_01678_b200"
+    shutil.copytree(pkg, dst, ignore=shutil.ignore_patterns("lib", "csrc", "__pycache__"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2512_01678_b200"], cwd=tmp_path,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "ImportError" in r.stderr and "not built" in r.stderr, r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("seed,n,m", [(0, 50, 300), (1, 400, 3000), (2, 1000, 4000)])
 def test_partition_matches_oracle(seed, n, m):
     from paper_2512_01678_b200 import partition_1d
