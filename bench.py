@@ -46,9 +46,15 @@ def _env_int(name, default):
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return float(d.get("hbm_gbs", FALLBACK_HBM_GBS)), "measured"
+        try:   # driver-written; tolerate {"hbm_gbs": 7100.0} or {"hbm_gbs": {"value": 7100.0, ...}}
+            with open(p) as f:
+                v = json.load(f).get("hbm_gbs")
+            if isinstance(v, dict):
+                v = v.get("value", v.get("gbs", v.get("burst")))
+            if v is not None and float(v) > 0:
+                return float(v), "measured"
+        except (OSError, ValueError, TypeError, AttributeError):
+            pass
     return FALLBACK_HBM_GBS, "fallback"
 
 
@@ -439,7 +445,8 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                 traffic = json.load(fh).get(dom, {}).get("dram_bytes_per_launch")
         roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": peak, "unit": "GB/s",
                     "frac": kd["algorithmic_GBps"] / peak, "traffic": traffic,
-                    "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                    "peak_source": ("MEASURED_PEAKS.json hbm_gbs (of measured)" if peak_kind == "measured" else
+                                    "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"),
                     "algorithmic_bytes": ("SURVEY 8(d) d.3 no-reuse count: per edge 4 + 4*w B, per row 12 + 4*w B"
                                           if dom == "spmm" else
                                           "no-reuse count: per nonzero of X 8 + 4*w B, per row/column 8 + 4*w B"
