@@ -99,8 +99,40 @@ def a_hat_values(g: Graph) -> np.ndarray:
 
 
 def _a_hat_csr(g: Graph) -> sp.csr_matrix:
-    return sp.csr_matrix((a_hat_values(g), g.col_idx.astype(np.int64), g.row_ptr),
-                         shape=(g.num_nodes, g.num_nodes))
+    # built once per graph (a pure function of the graph; the graph is never mutated)
+    A = getattr(g, "_a_hat", None)
+    if A is None:
+        A = sp.csr_matrix((a_hat_values(g), g.col_idx.astype(np.int64), g.row_ptr),
+                          shape=(g.num_nodes, g.num_nodes))
+        object.__setattr__(g, "_a_hat", A)
+    return A
+
+
+def _threads() -> int:
+    import os
+    return max(1, int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1)))
+
+
+def csr_matmul(A: sp.csr_matrix, P: np.ndarray) -> np.ndarray:
+    """A·P for a CSR A, the output rows cut into contiguous chunks computed on host threads
+    (scipy's CSR product releases the GIL).  Each output row is the same sum, in the same CSR
+    order, as the single-threaded product: the result is bit-identical to `A @ P` (SURVEY
+    §8(c) c.1 allows parallelism over output rows; no blocking or reordering of any sum)."""
+    P = np.asarray(P)
+    n = A.shape[0]
+    t = min(_threads(), max(1, n // 4096))
+    if t <= 1 or P.ndim != 2:
+        return np.asarray(A @ P)
+    from concurrent.futures import ThreadPoolExecutor
+    cuts = [n * i // t for i in range(t + 1)]
+    out = np.empty((n, P.shape[1]), dtype=np.result_type(A.dtype, P.dtype))
+
+    def run(i):
+        out[cuts[i]:cuts[i + 1]] = A[cuts[i]:cuts[i + 1]] @ P
+
+    with ThreadPoolExecutor(t) as ex:
+        list(ex.map(run, range(t)))
+    return out
 
 
 def a_hat_dense_from_csr(g: Graph) -> np.ndarray:
@@ -111,7 +143,7 @@ def aggregate(g: Graph, P: np.ndarray) -> np.ndarray:
     """Y = Â·P in FP64 (F2 / B2).  Alg. 3 P:373-384 computes the same sum
     Y[u,f] = Σ_{ei∈row u} val[ei]·X[col[ei], f]; here val = â (Q1)."""
     P = np.asarray(P, dtype=np.float64)
-    return np.asarray(_a_hat_csr(g) @ P)
+    return csr_matmul(_a_hat_csr(g), P)
 
 
 def aggregate_rows(g: Graph, P: np.ndarray, rows) -> np.ndarray:
@@ -138,8 +170,12 @@ AGGREGATORS = ("gcn", "sum", "mean", "max")
 
 def _a_tilde_csr(g: Graph) -> sp.csr_matrix:
     """Ã = A + I as a 0/1 CSR (the graph's pattern, diagonal included)."""
-    return sp.csr_matrix((np.ones(g.nnz), g.col_idx.astype(np.int64), g.row_ptr),
-                         shape=(g.num_nodes, g.num_nodes))
+    A = getattr(g, "_a_tilde", None)
+    if A is None:
+        A = sp.csr_matrix((np.ones(g.nnz), g.col_idx.astype(np.int64), g.row_ptr),
+                          shape=(g.num_nodes, g.num_nodes))
+        object.__setattr__(g, "_a_tilde", A)
+    return A
 
 
 def aggregate_scheme(g: Graph, P: np.ndarray, scheme: str, transpose: bool = False) -> np.ndarray:
@@ -150,10 +186,10 @@ def aggregate_scheme(g: Graph, P: np.ndarray, scheme: str, transpose: bool = Fal
         return aggregate(g, P)
     At = _a_tilde_csr(g)
     if scheme == "sum":
-        return np.asarray(At @ P)
+        return csr_matmul(At, P)
     if scheme == "mean":
         d = g.deg.astype(np.float64)[:, None]
-        return np.asarray(At @ (P / d)) if transpose else np.asarray(At @ P) / d
+        return csr_matmul(At, P / d) if transpose else csr_matmul(At, P) / d
     raise ValueError(f"not a linear aggregation scheme: {scheme}")
 
 
@@ -424,11 +460,14 @@ def softmax_ce(Z, labels, mask=None, n_lab: int | None = None):
 
 
 def backward(g: Graph, cache, Ws, dZ):
-    """B1-B4: returns (dWs, dbs)."""
+    """B1-B4: returns (dWs, dbs).  The upstream gradient of every layer, dZ_l = ∂loss/∂Z_l, is
+    recorded in cache["dZ"][l-1] (an output for bounds in tests; no extra arithmetic)."""
     L = len(Ws)
     dWs, dbs = [None] * L, [None] * L
     agg = cache.get("aggregator", "gcn")
+    cache["dZ"] = [None] * L
     for l in range(L, 0, -1):
+        cache["dZ"][l - 1] = dZ
         dbs[l - 1] = dZ.sum(axis=0)                                     # B1
         r = cache.get("rounding")
         W = np.asarray(Ws[l - 1], dtype=np.float64)
@@ -596,12 +635,19 @@ def partition_greedy(g: Graph, world: int) -> np.ndarray:
     return part
 
 
+PHASE2_BALANCE_PCT = 105   # reading R10: Phase II is kept iff max bin ≤ 1.05 · mean and no bin is empty
+
+
 def partition_hierarchical(g: Graph, world: int):
-    """Alg. 4 without Phase I: Phase II when the graph is disconnected, else Phase III.
-    Returns (part, phase)."""
+    """Alg. 4 without Phase I: Phase II when the graph is disconnected AND its bin packing is
+    balanced (every bin non-empty, max load ≤ 1.05·mean in |C| units, decided in integers:
+    100·world·max ≤ 105·N), else Phase III (a giant component or fewer components than ranks
+    falls through, reading R10).  Returns (part, phase)."""
     part, nc = partition_components(g, world)
     if part is not None:
-        return part, 2
+        loads = np.bincount(part, minlength=world)
+        if loads.min() > 0 and 100 * world * int(loads.max()) <= PHASE2_BALANCE_PCT * g.num_nodes:
+            return part, 2
     return partition_greedy(g, world), 3
 
 

@@ -175,6 +175,29 @@ def test_aggregate_identity_and_sqrt_degree():
     assert np.allclose(oracle.aggregate(g, sd), sd, rtol=1e-13, atol=0)
 
 
+def test_aggregate_row_parallel_is_the_same_sum(monkeypatch):
+    """The oracle's row-chunked threaded product (c.1: parallel over output rows only) is
+    bit-identical to scipy's single-threaded CSR product and matches the one-row-at-a-time
+    definition on sampled rows (incl. the largest row)."""
+    monkeypatch.setenv("ORACLE_THREADS", "5")
+    n = 40_000
+    w = make_small(n, 400_000, 9, 4, seed=11)
+    g = oracle.graph_build(w["src"], w["dst"], n)
+    X = w["X"].astype(np.float64)
+    got = oracle.aggregate(g, X)
+    import scipy.sparse as sp
+    A = sp.csr_matrix((oracle.a_hat_values(g), g.col_idx.astype(np.int64), g.row_ptr), shape=(n, n))
+    assert np.array_equal(got, np.asarray(A @ X))
+    rows = [0, 1, n // 3, n - 1, int(np.argmax(np.diff(g.row_ptr)))]
+    assert np.allclose(got[rows], oracle.aggregate_rows(g, X, rows), rtol=0, atol=1e-13)
+    for scheme in ("sum", "mean"):
+        for tr in (False, True):
+            y = oracle.aggregate_scheme(g, X, scheme, transpose=tr)
+            monkeypatch.setenv("ORACLE_THREADS", "1")
+            assert np.array_equal(y, oracle.aggregate_scheme(g, X, scheme, transpose=tr))
+            monkeypatch.setenv("ORACLE_THREADS", "5")
+
+
 # ---------------------------------------------------------------- switch S1-S3
 def _golden():
     with open(os.path.join(GOLDEN, "paper_constants.json")) as f:
