@@ -118,6 +118,15 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, c
   }
 }
 
+// Accumulation budget for long rows (a hub row is summed in at least
+// ⌈deg/256⌉ independent partial sums).  Each slot sums the edges of one block of kHubBlock
+// consecutive CSR entries on its own (a pairwise tree per group of U, then a running sum of
+// ≤ kHubBlock/(ES·U) groups), the finished blocks are added in block order, and the ES slot
+// totals meet in the fixed xor tree: a degree-9,477 Reddit hub (2 slots, U = 8) takes
+// ≈ 16 + 3 + 38 + 1 sequential FP32 additions instead of ≈ 590.  Rows of at most kHubBlock
+// edges keep the plain single-block sum.  Alg. 3 P:373-384 (the per-row sum), P:357 (skew).
+constexpr int64_t kHubBlock = 256;
+
 template <int LPR, int VPL, bool HAS_VAL, int UOV>
 __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   constexpr int ES = 32 / LPR;
@@ -128,14 +137,24 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
   if (a.part == 0) e = a.split[row];
   if (a.part == 1) s = a.split[row];
-  float4 acc[VPL];
+  // acc sums the current block of kHubBlock edges; tot the finished blocks, in block order
+  float4 acc[VPL], tot[VPL];
 #pragma unroll
-  for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
+  for (int j = 0; j < VPL; ++j) acc[j] = tot[j] = f4_zero();
   const uint64_t pol = l2_policy_evict_first();
   const int* vbits = reinterpret_cast<const int*>(a.val);
   int nxt = (s + lane < e) ? ldg_stream_i32_hint(a.col + s + lane, pol) : 0;
   int nxv = (HAS_VAL && s + lane < e) ? ldg_stream_i32_hint(vbits + s + lane, pol) : 0;
+  int64_t blk_end = s + kHubBlock;
   for (int64_t base = s; base < e; base += 32) {
+    if (base == blk_end) {  // close a block (rows longer than kHubBlock edges only)
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        tot[j] = f4_add(tot[j], acc[j]);
+        acc[j] = f4_zero();
+      }
+      blk_end += kHubBlock;
+    }
     const int nb = (int)min((int64_t)32, e - base);
     const int my_c = nxt;
     const float my_v = __int_as_float(nxv);
@@ -171,6 +190,10 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
         acc[j] = f4_add(acc[j], x[0][j]);
       }
     }
+  }
+  if (e - s > kHubBlock) {
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) acc[j] = f4_add(tot[j], acc[j]);
   }
 #pragma unroll
   for (int off = LPR; off < 32; off <<= 1)
@@ -456,28 +479,13 @@ static int env_int(const char* name) {
   return v ? atoi(v) : 0;
 }
 
-// Experiment hook: MPH_SPMM_U_<LPR>_<VPL>=<n> overrides the per-round unroll U of a main shape.
+// Per-shape unroll: 256-wide rows (32 lanes x 2 float4) gain from 8 gathers in flight per slot
+// (measured with the round-1 unroll sweep, arxiv SpMM -8 %); every other shape is best at the
+// default U.
 template <int LPR, int VPL, bool HAS_VAL>
 static int launch_spmm_u(const SpmmArgs& a, cudaStream_t s) {
-  char name[32];
-  snprintf(name, sizeof(name), "MPH_SPMM_U_%d_%d", LPR, VPL);
-  const int u = env_int(name);
-  if (!HAS_VAL) {
-    switch (u) {
-      case 2: return launch_spmm<LPR, VPL, HAS_VAL, 2>(a, s);
-      case 3: return launch_spmm<LPR, VPL, HAS_VAL, 3>(a, s);
-      case 4: return launch_spmm<LPR, VPL, HAS_VAL, 4>(a, s);
-      case 6: return launch_spmm<LPR, VPL, HAS_VAL, 6>(a, s);
-      case 8: return launch_spmm<LPR, VPL, HAS_VAL, 8>(a, s);
-      case 12: return launch_spmm<LPR, VPL, HAS_VAL, 12>(a, s);
-      case 16: return launch_spmm<LPR, VPL, HAS_VAL, 16>(a, s);
-      default: break;
-    }
-  }
-  // measured (tools/spmm_u_sweep.py): 256-wide rows (32 lanes x 2 float4) gain from 8 gathers
-  // in flight per slot (arxiv SpMM -8 %); every other shape is best at the default U
-  if (LPR == 32 && VPL == 2) return launch_spmm<LPR, VPL, HAS_VAL, 8>(a, s);
-  return launch_spmm<LPR, VPL, HAS_VAL>(a, s);
+  if constexpr (LPR == 32 && VPL == 2) return launch_spmm<LPR, VPL, HAS_VAL, 8>(a, s);
+  else return launch_spmm<LPR, VPL, HAS_VAL>(a, s);
 }
 
 template <bool HAS_VAL>

@@ -108,6 +108,41 @@ def test_reddit_graph_layer1_and_loss(P, reddit):
     assert abs(loss - ref_loss) <= 1e-3 * max(1.0, abs(ref_loss)), (loss, ref_loss)
 
 
+@pytest.fixture(scope="module")
+def reddit_graphs(P, reddit):
+    w = reddit
+    n = w["cfg"].num_nodes
+    return P.Graph(w["src"], w["dst"], n), oracle.graph_build(w["src"], w["dst"], n)
+
+
+@pytest.mark.parametrize("w", [48, 64, 128])
+def test_reddit_hub_rows_spmm(P, reddit_graphs, w):
+    """The FP32 aggregation bar 1e-5·(|Â|·|T|) on the full Reddit-shaped graph's 64 largest hubs
+    (degrees up to ~9.5K, where a single running FP32 sum would exceed the bar: SURVEY c.5's
+    accumulation budget, ⌈deg/256⌉ partial sums) plus 64 random rows, in the launch
+    configuration the epoch uses for each width (w = 128 runs as two 64-wide column slabs).
+    Expected values: the oracle's one-row-at-a-time Â·T on the same FP32 inputs."""
+    g, ref = reddit_graphs
+    n = ref.num_nodes
+    deg = np.diff(ref.row_ptr)
+    hubs = np.argsort(deg, kind="stable")[-64:]
+    rng = np.random.default_rng(1000 + w)
+    rows = np.concatenate([hubs, rng.choice(n, 64, replace=False)])
+    print(f"hub degrees {int(deg[hubs].min())}..{int(deg[hubs].max())}")
+    assert deg[hubs].max() > 9000
+    T = rng.standard_normal((n, w)).astype(np.float32)
+    Tp = (ref.dinv[:, None] * T).astype(np.float32)
+    out = torch.zeros((n, w), device="cuda")
+    g.spmm(torch.from_numpy(Tp).cuda(), out, w=w)
+    Z = out.cpu().numpy()[rows]
+    Zref = oracle.aggregate_rows(ref, T, rows)
+    bound = oracle.aggregate_rows(ref, np.abs(T), rows)
+    err = np.abs(Z.astype(np.float64) - Zref)
+    ratio = float((err / (1e-5 * bound + 1e-30)).max())
+    print(f"w={w}: max |err|/(1e-5·|Â||T|) = {ratio:.3g} (hubs {float((err[:64] / (1e-5 * bound[:64])).max()):.3g})")
+    assert ratio <= 1.0
+
+
 def test_products_forward_loss(P):
     import psutil
     if psutil.virtual_memory().available < 48 * 2 ** 30:
