@@ -215,11 +215,16 @@ def _build_model(P, torch, w, world, rank, comm, bounds=None, precision="tf32", 
     X = w["X"]
 
     def features(r0, r1):
+        # the dense/sparse switch is decided on the GLOBAL nonzero count (identical on every rank)
         if X is not None:
-            return P.Features(torch.from_numpy(np.ascontiguousarray(X[r0:r1])).cuda())
+            Xd = torch.from_numpy(np.ascontiguousarray(X[r0:r1])).cuda()
+            mode = P.Features.global_mode(P.Features.count_nnz(Xd), r1 - r0, cfg.num_features) if world > 1 else -1
+            return P.Features(Xd, force_mode=mode)
         ptr, idx, val = w["X_csr"]   # CSR features (NELL): rows r0..r1 of the host CSR, never densified
         b, e = int(ptr[r0]), int(ptr[r1])
-        return P.Features.from_csr(ptr[r0:r1 + 1] - b, idx[b:e], val[b:e], (r1 - r0, cfg.num_features))
+        mode = P.Features.global_mode(e - b, r1 - r0, cfg.num_features) if world > 1 else -1
+        return P.Features.from_csr(ptr[r0:r1 + 1] - b, idx[b:e], val[b:e], (r1 - r0, cfg.num_features),
+                                   force_mode=mode)
 
     if world == 1:
         g = P.Graph(w["src"], w["dst"], n)

@@ -104,6 +104,13 @@ int mph_graph_destroy(mph_graph* g);
 typedef struct mph_features mph_features;
 int mph_features_create(const float* X_d, int32_t N, int32_t F, int32_t ld, int32_t tau_bp,
                         int32_t force_mode, void* stream, mph_features** out);
+/* tau_bp values: the paper's tau = 0.80 (gamma = 0.20 on its testbed), and the crossover
+ * measured on B200 by the paper's own offline protocol (tools/calibrate_gamma.py, DESIGN §9.2:
+ * s* = 0.910 / 0.952 / 0.972 on three shapes, median 0.95) — "tau is fully determined by the
+ * hardware".  The Python binding defaults to the B200 value; the C calls take tau_bp
+ * explicitly. */
+#define MPH_TAU_PAPER_BP 8000
+#define MPH_TAU_B200_BP 9500
 /* Same switch from a HOST CSR matrix, for feature matrices too large to hold densely (NELL:
  * 65,755 x 61,278 at s = 99.21%).  ptr_h[N+1] (int64, ptr_h[0] = 0,
  * monotone), idx_h[ptr_h[N]] (int32 columns in [0,F), strictly ascending within each row: S3),
@@ -115,6 +122,15 @@ int mph_features_create(const float* X_d, int32_t N, int32_t F, int32_t ld, int3
 int mph_features_create_csr(const int64_t* ptr_h, const int32_t* idx_h, const float* val_h, int32_t N,
                             int32_t F, int32_t tau_bp, int32_t force_mode, void* stream, mph_features** out);
 int mph_features_info(const mph_features* f, int64_t* nnz_h, int32_t* mode_h, int32_t* is_binary_h);
+/* The switch for a row-partitioned X (P > 1): every rank must take the SAME decision
+ * (the mode and the layer orders it implies fix which buffers cross ranks), so the caller counts
+ * its local rows' nonzeros with mph_features_count (device X_d [N][ld], synchronises), sums the
+ * counts over the ranks (the process group is plumbing), and mph_features_decide applies Eq. 1 to
+ * the GLOBAL count: *mode_h = 1 (Sparse) iff 10000*nnz <= (10000 - tau_bp)*N*F, N the global row
+ * count.  Pass the result as force_mode on every rank.  mph_gcn_create checks that the ranks
+ * agree (MPH_EINVAL otherwise).  MPH_EINVAL on nnz > N*F or a tau_bp outside [0, 10000]. */
+int mph_features_count(const float* X_d, int32_t N, int32_t F, int32_t ld, void* stream, int64_t* nnz_h);
+int mph_features_decide(int64_t nnz, int64_t N, int64_t F, int32_t tau_bp, int32_t* mode_h);
 /* Borrowed device views (sparse mode only; MPH_ESTATE in dense mode). */
 int mph_features_csr(const mph_features* f, const int64_t** ptr_d, const int32_t** idx_d, const float** val_d);
 int mph_features_csc(const mph_features* f, const int64_t** ptr_d, const int32_t** idx_d, const float** val_d);

@@ -21,6 +21,7 @@ STATUS = {0: "MPH_OK", -1: "MPH_EINVAL", -2: "MPH_ERANGE", -3: "MPH_EDEGENERATE"
 EPI_BIAS, EPI_RELU, EPI_ROWSCALE, EPI_MASK, EPI_DROPOUT, EPI_COLSUM, EPI_TF32 = 1, 2, 4, 8, 16, 32, 64
 EPI_BF16, EPI_MASK_BF16 = 128, 256
 AGG = {"gcn": 0, "sum": 1, "mean": 2, "max": 3}            # MPH_AGG_*
+TAU_PAPER_BP, TAU_B200_BP = 8000, 9500                     # MPH_TAU_PAPER_BP, MPH_TAU_B200_BP
 OPT = {"adam": 0, "sgd": 1, "adamw": 2}                    # MPH_OPT_*
 
 
@@ -73,6 +74,8 @@ _SIGS = {
     "mph_features_create": [P, i32, i32, i32, i32, i32, P, PP],
     "mph_features_create_csr": [P, P, P, i32, i32, i32, i32, P, PP],
     "mph_features_info": [P, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32)],
+    "mph_features_count": [P, i32, i32, i32, P, C.POINTER(i64)],
+    "mph_features_decide": [i64, i64, i64, i32, C.POINTER(i32)],
     "mph_features_csr": [P, PP, PP, PP],
     "mph_features_csc": [P, PP, PP, PP],
     "mph_features_dense": [P, PP, C.POINTER(i32)],

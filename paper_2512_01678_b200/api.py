@@ -1,7 +1,7 @@
 """Python API over the C-ABI (marshalling only; every step runs in libmorphling.so kernels).
 
     g = Graph(src, dst, num_nodes)                         # a0, mph_graph_build
-    f = Features(X_cuda, tau_bp=8000)                      # a1, mph_features_create
+    f = Features(X_cuda)                                   # a1, mph_features_create (tau: B200 value)
     m = GCN(g, f, dims=(602, 128, 41))                     # mph_gcn_create
     m.init_xavier(42); m.set_labels(y_cuda)
     loss = m.train_epoch(t=1)                              # a2..a11 + Adam, loss in a device double
@@ -135,7 +135,7 @@ class Graph:
 class Features:
     """a1 — feature analysis + dense/sparse switch (Alg. 1 Initialize)."""
 
-    def __init__(self, X: torch.Tensor, tau_bp: int = 8000, force_mode: int = -1, stream=None):
+    def __init__(self, X: torch.Tensor, tau_bp: int = L.TAU_B200_BP, force_mode: int = -1, stream=None):
         assert X.is_cuda and X.dtype == torch.float32 and X.dim() == 2 and X.stride(1) == 1
         h = _out_ptr()
         L.mph_features_create(X.data_ptr(), X.shape[0], X.shape[1], X.stride(0), tau_bp, force_mode,
@@ -149,8 +149,32 @@ class Features:
         L.mph_features_info(h, C.byref(nnz), C.byref(mode), C.byref(binary))
         self.nnz, self.mode, self.is_binary = nnz.value, mode.value, bool(binary.value)
 
+    @staticmethod
+    def global_mode(nnz_local: int, n_local: int, F: int, tau_bp: int = L.TAU_B200_BP, pg=None) -> int:
+        """The dense/sparse switch of a row-partitioned X (mph_features_decide on the global
+        count): the per-rank nnz and row counts are summed over the torch.distributed group
+        (plumbing); every rank gets the same mode to pass as force_mode."""
+        import torch.distributed as dist
+        t = torch.tensor([int(nnz_local), int(n_local)], dtype=torch.int64)
+        if dist.is_initialized() and dist.get_world_size(pg) > 1:
+            if dist.get_backend(pg) == "nccl":
+                t = t.cuda()
+            dist.all_reduce(t, group=pg)
+        nnz, n = (int(v) for v in t.cpu().tolist())
+        mode = C.c_int32()
+        L.mph_features_decide(nnz, n, int(F), int(tau_bp), C.byref(mode))
+        return mode.value
+
+    @staticmethod
+    def count_nnz(X: torch.Tensor, stream=None) -> int:
+        """nnz of a device X (mph_features_count; synchronises)."""
+        assert X.is_cuda and X.dtype == torch.float32 and X.dim() == 2 and X.stride(1) == 1
+        n = C.c_int64()
+        L.mph_features_count(X.data_ptr(), X.shape[0], X.shape[1], X.stride(0), stream_ptr(stream), C.byref(n))
+        return n.value
+
     @classmethod
-    def from_csr(cls, ptr: np.ndarray, idx: np.ndarray, val: np.ndarray, shape, tau_bp: int = 8000,
+    def from_csr(cls, ptr: np.ndarray, idx: np.ndarray, val: np.ndarray, shape, tau_bp: int = L.TAU_B200_BP,
                  force_mode: int = -1, stream=None) -> "Features":
         """a1 from a host CSR matrix (mph_features_create_csr): NELL-sized X never densified."""
         p = np.ascontiguousarray(ptr, dtype=np.int64)
@@ -476,6 +500,17 @@ class GCN:
             assert mask.is_cuda and mask.dtype == torch.uint8
         if n_lab_global is None:
             n_lab_global = int(mask.sum().item()) if mask is not None else labels.numel()
+            if self.graph_world() > 1:
+                # the loss is a mean over the GLOBAL labelled rows: sum the local counts
+                import torch.distributed as dist
+                if not dist.is_initialized():
+                    raise ValueError("set_labels on a partitioned graph needs n_lab_global "
+                                     "(or an initialised torch.distributed group to sum the counts)")
+                t = torch.tensor([n_lab_global], dtype=torch.int64)
+                if dist.get_backend() == "nccl":
+                    t = t.cuda()
+                dist.all_reduce(t)
+                n_lab_global = int(t.item())
         self._labels = (labels, mask)  # keep alive
         L.mph_gcn_set_labels(self.h, labels.data_ptr(), mask.data_ptr() if mask is not None else None,
                              int(n_lab_global))

@@ -192,9 +192,52 @@ static void features_free(mph_features* f) {
   delete f;
 }
 
+// S2 (Eq. 1, Alg. 1): Sparse iff s = 1 − nnz/(N·F) ≥ τ, decided in integers
+// (Q11): 10000·nnz ≤ (10000 − τ_bp)·N·F.
+static int32_t decide_mode(int64_t nnz, int64_t N, int64_t F, int32_t tau_bp) {
+  const __int128 lhs = (__int128)10000 * nnz, rhs = (__int128)(10000 - tau_bp) * N * F;
+  return lhs <= rhs ? 1 : 0;
+}
+
 }  // namespace mph
 
 using namespace mph;
+
+extern "C" int mph_features_decide(int64_t nnz, int64_t N, int64_t F, int32_t tau_bp, int32_t* mode_h) {
+  if (!mode_h || nnz < 0 || N <= 0 || F <= 0 || tau_bp < 0 || tau_bp > 10000 || nnz > (__int128)N * F)
+    return fail(MPH_EINVAL, "features_decide arguments");
+  *mode_h = decide_mode(nnz, N, F, tau_bp);
+  return MPH_OK;
+}
+
+extern "C" int mph_features_count(const float* X_d, int32_t N, int32_t F, int32_t ld, void* stream, int64_t* nnz_h) {
+  if (!nnz_h || !X_d || N <= 0 || F <= 0 || ld < F) return fail(MPH_EINVAL, "features_count arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t *row_nnz = nullptr, *row_nu = nullptr, *sums = nullptr;
+  void* tmp = nullptr;
+  auto done = [&](int code) {
+    dev_free(row_nnz);
+    dev_free(row_nu);
+    dev_free(sums);
+    dev_free(tmp);
+    return code;
+  };
+  int rc = MPH_OK;
+  if ((rc = dev_alloc(&row_nnz, (size_t)N)) || (rc = dev_alloc(&row_nu, (size_t)N)) || (rc = dev_alloc(&sums, 1)))
+    return done(rc);
+  const unsigned warps_grid = (unsigned)std::min<int64_t>(ceil_div((int64_t)N * 32, 256), 148 * 32);
+  k_row_counts<<<warps_grid, 256, 0, s>>>(X_d, N, F, ld, row_nnz, row_nu);
+  count_launch();
+  size_t tb = 0;
+  cub::DeviceReduce::Sum(nullptr, tb, row_nnz, sums, N, s);
+  if ((rc = dev_alloc((char**)&tmp, std::max<size_t>(tb, 1)))) return done(rc);
+  cudaError_t e = cub::DeviceReduce::Sum(tmp, tb, row_nnz, sums, N, s);
+  count_launch();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(nnz_h, sums, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return done(fail(MPH_ECUDA, "features_count: %s", cudaGetErrorString(e)));
+  return done(MPH_OK);
+}
 
 extern "C" int mph_features_create(const float* X_d, int32_t N, int32_t F, int32_t ld, int32_t tau_bp,
                                    int32_t force_mode, void* stream, mph_features** out) {
@@ -242,8 +285,7 @@ extern "C" int mph_features_create(const float* X_d, int32_t N, int32_t F, int32
   if (e != cudaSuccess) return cuda_bail(e, "count");
   f->nnz = h_sums[0];
   f->is_binary = (h_sums[1] == 0);
-  const __int128 lhs = (__int128)10000 * f->nnz, rhs = (__int128)(10000 - tau_bp) * N * F;
-  f->mode = force_mode >= 0 ? force_mode : (lhs <= rhs ? 1 : 0);  // S2: s >= tau, decided in integers
+  f->mode = force_mode >= 0 ? force_mode : decide_mode(f->nnz, N, F, tau_bp);  // S2: s >= tau, in integers
 
   if (f->mode == 0) {
     f->P = pad_width(F);
@@ -330,8 +372,7 @@ extern "C" int mph_features_create_csr(const int64_t* ptr_h, const int32_t* idx_
   f->F = F;
   f->nnz = nnz;
   f->is_binary = (nonunit == 0);
-  const __int128 lhs = (__int128)10000 * nnz, rhs = (__int128)(10000 - tau_bp) * N * F;
-  f->mode = force_mode >= 0 ? force_mode : (lhs <= rhs ? 1 : 0);  // S2, as in mph_features_create
+  f->mode = force_mode >= 0 ? force_mode : decide_mode(nnz, N, F, tau_bp);  // S2, as in mph_features_create
   int rc = MPH_OK;
   int64_t* tptr = nullptr;
   int32_t* tidx = nullptr;

@@ -135,6 +135,39 @@ static void gcn_free(mph_gcn* m) {
   delete m;
 }
 
+// The feature mode and every layer's order (Q7) decide which buffers cross ranks and at which
+// widths, so all ranks must take the same decisions (a rank-local dense/sparse switch would give
+// mismatched exchanges).  Bit 0: mode; bit 1 + l: order of layer l.
+static uint32_t layout_signature(const mph_features* f, const std::vector<Layer>& layers) {
+  uint32_t sig = (uint32_t)(f->mode & 1);
+  for (size_t i = 0; i < layers.size() && i < 20; ++i) sig |= (uint32_t)(layers[i].order & 1) << (i + 1);
+  return sig;
+}
+
+// NCCL transport: Σ sig and Σ sig² over the ranks equal world·sig and world·sig² iff every rank
+// has the same signature (exact in FP64: sig < 2^21).  Setup only (synchronises).
+static int check_layout_agrees(mph_comm* c, uint32_t sig, cudaStream_t s) {
+  int32_t world = 1, rank = 0;
+  MPH_TRY(mph_comm_info(c, &world, &rank));
+  if (world <= 1) return MPH_OK;
+  double h[2] = {(double)sig, (double)sig * (double)sig};
+  double* d = nullptr;
+  MPH_TRY(dev_alloc(&d, 2));
+  cudaError_t e = cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, s);
+  int rc = e == cudaSuccess ? mph_allreduce_sum(c, d, 2, 1, s) : fail(MPH_ECUDA, "layout check: %s", cudaGetErrorString(e));
+  if (rc == MPH_OK) e = cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (rc == MPH_OK && e == cudaSuccess) e = cudaStreamSynchronize(s);
+  dev_free(d);
+  MPH_TRY(rc);
+  if (e != cudaSuccess) return fail(MPH_ECUDA, "layout check: %s", cudaGetErrorString(e));
+  if (h[0] != (double)world * sig || h[1] != (double)world * sig * (double)sig)
+    return fail(MPH_EINVAL,
+                "gcn_create: ranks decided different feature modes / layer orders (this rank 0x%x): the dense/sparse "
+                "switch must be global (decide it from the global nnz, mph_features_decide, and pass force_mode)",
+                sig);
+  return MPH_OK;
+}
+
 // element `off` of a buffer that holds bf16 (BF16 mode) or float values
 static float* elem(const mph_gcn* m, float* base, int64_t off) {
   return m->bf16 ? reinterpret_cast<float*>(reinterpret_cast<uint16_t*>(base) + off) : base + off;
@@ -549,6 +582,7 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     m->p2p->n_rows = nr;
     m->p2p->row0 = g->row0;
     m->p2p->off_buf.assign(2 * m->L + 1, -1);
+    m->p2p->layout_sig = layout_signature(f, m->layers);
     int64_t bytes = 0;
     for (const auto& l : m->layers)
       if (l.order == 0) bytes += 2 * shared_bytes(nc, l.pout);
@@ -634,10 +668,13 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     for (cudaEvent_t* ev : {&m->ev_pack, &m->ev_halo, &m->ev_grad, &m->ev_comm_done, &m->ev_loss})
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return bail(fail(MPH_ECUDA, "gcn_create streams: %s", cudaGetErrorString(e)));
-    int wmax = m->layers[0].pin;
-    for (const auto& l : m->layers) wmax = std::max(wmax, l.pout);
+    // widths that cross ranks / leave a split SpMM: T'_l and dZ'_l (pout) of transform-first
+    // layers, and dinv ⊙ X (pin) of an aggregate-first layer 1 (its setup exchange and Y_1)
+    int wmax = 0;
+    for (const auto& l : m->layers) wmax = std::max(wmax, l.order == 0 ? l.pout : l.pin);
     if (!p2p && (rc = halo_reserve(g, wmax))) return bail(rc);  // no reallocation while sends are in flight
     if (m->bf16 && (rc = dev_alloc(&m->part0, (size_t)nr * wmax))) return bail(rc);
+    if (!p2p && (rc = check_layout_agrees(m->comm, layout_signature(f, m->layers), s))) return bail(rc);
   }
   if (m->layers[0].order == 0 && f->mode == 0 && !max_agg) {
     // TF32-rounded copy of X: the A operand of the layer-1 transform and of its dW GEMM

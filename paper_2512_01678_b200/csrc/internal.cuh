@@ -79,6 +79,7 @@ struct P2PState {
   int64_t n_params = 0;
   int64_t n_rows = 0, row0 = 0;
   std::vector<int64_t> off_buf;  // this rank's shared buffers (byte offsets, -1 = absent)
+  uint32_t layout_sig = 0;       // feature mode + per-layer orders; every rank must agree
   // after mph_gcn_p2p_open
   bool opened = false;
   std::vector<char*> peer_base;                 // mapped arenas (own arena at [rank])

@@ -31,7 +31,8 @@ struct Blob {  // MPH_P2P_BLOB_BYTES descriptor exchanged by the caller
   int32_t world, rank;
   int64_t row0, n_rows, n_params;
   int64_t off_flags, off_loss, off_gsum;
-  int32_t n_buf, pad;
+  int32_t n_buf;
+  uint32_t layout_sig;
   int64_t off_buf[40];
 };
 static_assert(sizeof(Blob) <= MPH_P2P_BLOB_BYTES, "blob too large");
@@ -171,6 +172,7 @@ int p2p_export(const P2PState* p, uint8_t* blob_h) {
   b.off_gsum = p->off_gsum;
   if (p->off_buf.size() > 40) return fail(MPH_ENOTSUP, "p2p: too many shared buffers");
   b.n_buf = (int32_t)p->off_buf.size();
+  b.layout_sig = p->layout_sig;
   for (size_t i = 0; i < p->off_buf.size(); ++i) b.off_buf[i] = p->off_buf[i];
   std::memset(blob_h, 0, MPH_P2P_BLOB_BYTES);
   std::memcpy(blob_h, &b, sizeof(b));
@@ -187,6 +189,11 @@ int p2p_open(P2PState* p, const mph_graph* g, const uint8_t* blobs, int world) {
       return fail(MPH_EINVAL, "p2p_open: blob %d is not rank %d's descriptor of a world-%d model", q, q, world);
     if (b[q].n_params != p->n_params || b[q].n_buf != (int32_t)p->off_buf.size())
       return fail(MPH_EINVAL, "p2p_open: rank %d's model has a different layout", q);
+    if (b[q].layout_sig != p->layout_sig)
+      return fail(MPH_EINVAL,
+                  "p2p_open: rank %d decided feature mode / layer orders 0x%x, this rank 0x%x: the dense/sparse "
+                  "switch must be global (decide it from the global nnz, mph_features_decide, and pass force_mode)",
+                  q, b[q].layout_sig, p->layout_sig);
   }
   p->peer_base.assign(world, nullptr);
   p->peer_off.assign(world, {});

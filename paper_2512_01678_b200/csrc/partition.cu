@@ -106,8 +106,16 @@ extern "C" int mph_partition_hierarchical(const int64_t* row_ptr_h, const int32_
   int32_t nc = 0;
   MPH_TRY(mph_partition_components(row_ptr_h, col_idx_h, N, world, part_h, &nc));
   if (nc > 1) {
-    if (phase_h) *phase_h = 2;
-    return MPH_OK;
+    // reading R10: keep Phase II only when its bins are balanced (none empty, the largest within
+    // 5 % of the mean, in |C| units), else fall through to Phase III (a giant component)
+    std::vector<int64_t> load((size_t)world, 0);
+    for (int32_t v = 0; v < N; ++v) ++load[part_h[v]];
+    const int64_t mx = *std::max_element(load.begin(), load.end());
+    const int64_t mn = *std::min_element(load.begin(), load.end());
+    if (mn > 0 && 100 * (int64_t)world * mx <= 105 * (int64_t)N) {
+      if (phase_h) *phase_h = 2;
+      return MPH_OK;
+    }
   }
   if (phase_h) *phase_h = 3;
   return mph_partition_greedy(row_ptr_h, N, world, part_h, nullptr);

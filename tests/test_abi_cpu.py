@@ -123,11 +123,12 @@ def test_plan_rejects_bad_arguments():
 
 
 # ---------------------------------------------------------------- Alg. 4 partitioners (NEXT-3)
-@pytest.mark.parametrize("seed,n,m", [(0, 300, 2500), (1, 1200, 9000), (2, 500, 350)])
+@pytest.mark.parametrize("seed,n,m", [(0, 300, 2500), (1, 1200, 9000), (2, 500, 350), (3, 60, 24), (4, 400, 150)])
 def test_alg4_partitioners_match_oracle_bit_exact(seed, n, m):
     import paper_2512_01678_b200 as P
     w = make_small(n, m, 4, 3, seed=seed, alpha=2.1)
     g = oracle.graph_build(w["src"], w["dst"], n)
+    phases = set()
     for world in (1, 2, 3, 4, 8):
         part, load = P.partition_greedy(g.row_ptr, world)
         ref = oracle.partition_greedy(g, world)
@@ -139,10 +140,12 @@ def test_alg4_partitioners_match_oracle_bit_exact(seed, n, m):
         ph, phase = P.partition_hierarchical(g.row_ptr, g.col_idx, world)
         rh, rphase = oracle.partition_hierarchical(g, world)
         assert phase == rphase and np.array_equal(ph, rh)
+        phases.add(phase)
         new_id, bounds = P.relabel(ph, world)
         rn, rb = oracle.relabel(rh, world)
         assert np.array_equal(new_id, rn) and np.array_equal(bounds, rb)
         assert np.array_equal(P.partition_stats(g.row_ptr, g.col_idx, ph, world), oracle.partition_stats(g, rh, world))
+    print("phases", sorted(phases))
 
 
 def test_relabel_rejects_bad_parts():

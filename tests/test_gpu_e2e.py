@@ -64,7 +64,9 @@ def test_loss_trajectory_small_configs(P, name, mode):
     w = make_workload(name)
     dims = w["cfg"].dims
     _, f, m, _ = _gpu_model(P, w, dims, force_mode=mode)
-    assert f.mode == (1 if mode == -1 else mode)
+    from paper_2512_01678_b200._lib import TAU_B200_BP
+    assert f.mode == (oracle.analyze_features(w["X"], TAU_B200_BP).mode if mode == -1 else mode)
+    assert mode != -1 or f.mode == (1 if name == "cora" else 0)
     got = _gpu_losses(m, 10)
     g = oracle.graph_build(w["src"], w["dst"], w["X"].shape[0])
     ref, _ = oracle.train(g, w["X"], w["y"], dims, epochs=10, seed=42)

@@ -74,7 +74,7 @@ def test_graph_build_errors(P):
 def test_feature_switch_configs(P, name):
     w = make_workload(name)
     X = w["X"]
-    f = P.Features(cuda(X))
+    f = P.Features(cuda(X), tau_bp=8000)               # the paper's tau = 0.80
     ref = oracle.analyze_features(X, 8000)
     assert (f.nnz, f.mode, f.is_binary) == (ref.nnz, ref.mode, ref.is_binary)
     assert f.mode == 1                                 # both are Sparse at tau = 0.80 (SURVEY table)
@@ -82,14 +82,23 @@ def test_feature_switch_configs(P, name):
         assert np.array_equal(got.cpu().numpy(), exp)
     for got, exp in zip(f.csc(), ref.csc):
         assert np.array_equal(got.cpu().numpy(), exp)
+    # the binding's default is the B200-measured tau = 0.95 (reading R5): cora (s = 0.987) stays
+    # Sparse, pubmed (s = 0.90) goes Dense, and the oracle at the same tau agrees
+    from paper_2512_01678_b200._lib import TAU_B200_BP
+    fd = P.Features(cuda(X))
+    rd = oracle.analyze_features(X, TAU_B200_BP)
+    assert (fd.nnz, fd.mode) == (rd.nnz, rd.mode) == (ref.nnz, 1 if name == "cora" else 0)
 
 
 def test_feature_switch_boundary(P):
     X = np.zeros((10, 10), np.float32)
     X.flat[:20] = 2.5                                  # s = 0.80 exactly -> Sparse
-    assert P.Features(cuda(X)).mode == 1
+    assert P.Features(cuda(X), tau_bp=8000).mode == 1
+    X.flat[5] = 0.0                                    # s = 0.81 -> Dense at the B200 tau 0.95
+    assert P.Features(cuda(X)).mode == 0 and P.Features(cuda(X), tau_bp=8100).mode == 1
+    X.flat[5] = 2.5
     X.flat[20] = -1.0                                  # s = 0.79 -> Dense
-    f = P.Features(cuda(X))
+    f = P.Features(cuda(X), tau_bp=8000)
     assert f.mode == 0 and f.nnz == 21
     Xd = f.dense().cpu().numpy()
     assert np.array_equal(Xd[:, :10], X) and np.all(Xd[:, 10:] == 0)
@@ -372,7 +381,7 @@ def test_sparse_feature_kernels(P, name, fo):
     X = w["X"]
     N, F = X.shape
     fo = fo or w["cfg"].dims[1]
-    f = P.Features(cuda(X))
+    f = P.Features(cuda(X), force_mode=1)
     rng = np.random.default_rng(1)
     W = rng.standard_normal((F, fo)).astype(np.float32)
     rs = rng.random(N).astype(np.float32) + 0.5

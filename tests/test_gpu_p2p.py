@@ -312,3 +312,79 @@ def test_bench_two_ranks_share_device():
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] > 0
     assert np.isfinite(line["final_loss"]) and line["e2e"]["value"] > 0
     assert "comm p2p" in line["config"]["parallelism"]
+
+
+def _worker_mismatch(rank, world, port, result_q):
+    """Ranks that decide the dense/sparse switch differently must fail loudly at open (advisor
+    finding: the rank-local switch gave mismatched exchanges); the global decision agrees."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2512_01678_b200 as P
+        n = 2000
+        w = make_small(n, 16000, 16, 4, seed=9)
+        X = w["X"].copy()
+        gfull = P.Graph(w["src"], w["dst"], n)
+        rp, ci = (t.cpu().numpy() for t in gfull.csr()[:2])
+        bounds = P.partition_1d(rp, world)
+        g = P.Graph.from_plan(P.Plan(rp, ci, n, bounds, rank))
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        if rank == 1:
+            X[r0:r1] = 0.0
+            X[r0, 0] = 1.0            # rank 1's rows alone are ~100 % sparse, rank 0's dense
+        Xd = torch.from_numpy(np.ascontiguousarray(X[r0:r1])).cuda()
+        local = P.Features(Xd)         # rank-local switch: rank 0 dense, rank 1 sparse
+        mode = P.Features.global_mode(P.Features.count_nnz(Xd), r1 - r0, 16)
+        err = ""
+        try:
+            P.GCN(g, local, (16, 32, 4), comm="p2p", pg=None)   # 16 -> 32: dense gives AF, sparse TF
+        except Exception as e:
+            err = str(e)
+        glob = P.Features(Xd, force_mode=mode)
+        m = P.GCN(g, glob, (16, 32, 4), comm="p2p")
+        m.init_xavier(42)
+        m.set_labels(torch.from_numpy(np.ascontiguousarray(w["y"][r0:r1])).cuda(), n_lab_global=n)
+        loss = m.train_epoch(1).item()
+        torch.cuda.synchronize()
+        res = dict(rank=rank, local_mode=local.mode, mode=mode, err=err, loss=loss, status=m.p2p_status())
+        dist.barrier()
+        del m
+        dist.barrier()
+        result_q.put(res)
+    except Exception as e:  # pragma: no cover
+        import traceback
+        result_q.put(dict(rank=rank, error=f"{e!r}\n{traceback.format_exc()}"))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_p2p_mismatched_feature_modes_fail_loudly():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_mismatch, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    try:
+        for _ in range(2):
+            r = q.get(timeout=300)
+            out[r["rank"]] = r
+    finally:
+        for p in procs:
+            p.join(timeout=120)
+            if p.is_alive():
+                p.kill()
+    errs = [r["error"] for r in out.values() if "error" in r]
+    assert not errs, errs[0]
+    assert [out[r]["local_mode"] for r in (0, 1)] == [0, 1]
+    for r in (0, 1):
+        assert "feature mode" in out[r]["err"], out[r]["err"]
+        assert out[r]["mode"] == out[0]["mode"] == 0
+        assert out[r]["status"] == 0
+    assert out[0]["loss"] == out[1]["loss"]

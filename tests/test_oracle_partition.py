@@ -46,8 +46,30 @@ def test_components_hand_case_and_ties():
     part, nc = oracle.partition_components(g, 2)
     assert nc == 4
     assert part.tolist() == [0] * 5 + [1] * 3 + [1, 1] + [0, 0]
+    # reading R10: loads [7, 5] exceed 1.05 x the mean 6 -> Phase III
     h, phase = oracle.partition_hierarchical(g, 2)
-    assert phase == 2 and np.array_equal(h, part)
+    assert phase == 3 and np.array_equal(h, oracle.partition_greedy(g, 2))
+    # without {10, 11}: sizes 5, 3, 2 -> [5, 5], balanced -> Phase II keeps the packing
+    g10 = oracle.graph_build(src[:-1], dst[:-1], 10)
+    part10, _ = oracle.partition_components(g10, 2)
+    h, phase = oracle.partition_hierarchical(g10, 2)
+    assert phase == 2 and np.array_equal(h, part10) and part10.tolist() == [0] * 5 + [1] * 5
+
+
+def test_hierarchical_giant_component_and_too_few_components_fall_through():
+    # a giant path 0..19 plus isolated nodes 20, 21: Phase II would put 20 of 22 nodes on one rank
+    src = np.arange(0, 19, dtype=np.int32)
+    g = oracle.graph_build(src, src + 1, 22)
+    assert oracle.connected_components(g)[1] == 3
+    part, phase = oracle.partition_hierarchical(g, 2)
+    assert phase == 3 and np.array_equal(part, oracle.partition_greedy(g, 2))
+    # two equal components but four ranks: two bins would stay empty
+    s2 = np.array([0, 1, 2, 4, 5, 6], np.int32)
+    g2 = oracle.graph_build(s2, s2 + 1, 8)
+    part, phase = oracle.partition_hierarchical(g2, 4)
+    assert phase == 3
+    part, phase = oracle.partition_hierarchical(g2, 2)
+    assert phase == 2 and part.tolist() == [0] * 4 + [1] * 4
 
 
 def test_components_match_scipy_and_connected_fallthrough():
