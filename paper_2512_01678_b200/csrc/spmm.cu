@@ -210,8 +210,10 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   store_row<LPR, VPL>(a, row, sub, acc, du, rs, pol);
 }
 
+// 4 blocks (32 warps) per SM within the 64-register budget for the one-float4-per-lane shapes
+// (the hub-block partials would otherwise cost a block per SM); 3 for the wider register tiles
 template <int LPR, int VPL, bool HAS_VAL, int UOV>
-__global__ void __launch_bounds__(256, 3) k_spmm(SpmmArgs a) {
+__global__ void __launch_bounds__(256, ((VPL == 1 || LPR == 4) ? 4 : 3)) k_spmm(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   while (true) {
     int it = 0;

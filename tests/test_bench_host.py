@@ -50,3 +50,24 @@ def test_config_keys_shared_by_both_arms():
     four = bench._config_common(a, 4)
     assert four["parallelism"] == "1d-row-partition x4, comm p2p"
     assert set(one) == set(four)
+
+
+def test_roofline_bounds(tmp_path, monkeypatch):
+    """The aggregation's gathered (algorithmic, no-reuse) bytes are measured against the L2
+    delivery ceiling of this run (max of the probes); GEMM-dominated epochs against HBM."""
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    peaks = {"hbm_gbs": 6500.0, "hbm_kind": "measured", "l2_stream_GBps": 21000.0,
+             "gather": {"l2_resident_64MB": 16000.0, "hbm_resident_4GB": 5000.0}}
+    k = {"spmm": {"ms_per_epoch": 8.0, "avg_launch_ms": 2.0, "algorithmic_GBps": 19000.0, "bytes_per_launch": 3.8e10},
+         "gemm_nt": {"ms_per_epoch": 0.5, "avg_launch_ms": 0.1, "algorithmic_GBps": 5000.0, "bytes_per_launch": 5e8}}
+    r = bench._roofline(k, 9.0, "reddit", peaks)
+    assert r["bound"] == "l2" and r["kernel"] == "spmm" and r["peak"] == 21000.0
+    assert r["frac"] == pytest.approx(19000.0 / 21000.0)
+    assert r["traffic"] is None and "dram_frac_of_hbm" not in r
+    (tmp_path / "profiles").mkdir()
+    (tmp_path / "profiles" / "ncu_traffic_reddit.json").write_text('{"spmm": {"dram_bytes_per_launch": 1.0e9}}')
+    r = bench._roofline(k, 9.0, "reddit", peaks)
+    assert r["dram_frac_of_hbm"] == pytest.approx(1.0e9 / 2.0e6 / 6500.0)
+    k2 = {"gemm_nt": k["gemm_nt"], "spmm": dict(k["spmm"], ms_per_epoch=0.1)}
+    r = bench._roofline(k2, 1.0, "arxiv", peaks)
+    assert r["bound"] == "hbm" and r["peak"] == 6500.0 and r["frac"] == pytest.approx(5000.0 / 6500.0)
