@@ -31,8 +31,6 @@ import numpy as np  # noqa: E402
 METRIC = "GCN ms/epoch (fwd+bwd+Adam) at 1/2/4/8 B200; SpMM HBM GB/s vs peak"
 UNIT = "ms/epoch"
 FALLBACK_HBM_GBS = 6650.0
-# CPU-oracle sample: the same generator recipe at 1/k scale (same mean degree, widths, classes)
-SAMPLE_SCALE = {"cora": 1, "pubmed": 1, "arxiv": 4, "reddit": 16, "products": 32, "nell": 2}
 PROF_KINDS = {0: "spmm", 1: "gemm_nt", 2: "gemm_tn", 3: "softmax_ce", 4: "adam", 5: "sparse_feat", 6: "halo"}
 
 
@@ -104,51 +102,65 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-# ---------------------------------------------------------------------------------- oracle sample
-def _oracle_sample(name: str, seed_offset: int = 0):
-    """The same workload recipe at 1/k scale, for the CPU oracle (bounded sample)."""
-    from synth.generate import CONFIGS, make_features, make_features_csr, make_graph, make_labels
-    cfg = CONFIGS[name]
-    k = SAMPLE_SCALE[name]
-    n = max(64, cfg.num_nodes // k)
-    nnz = cfg.nnz_a // k
-    y = make_labels(n, cfg.num_classes)
-    src, dst = make_graph(n, nnz, cfg.num_classes, cfg.alpha, cfg.mu, cfg.seed + seed_offset)
-    if cfg.feature_kind == "binary_csr":
-        import scipy.sparse as sp
-        ptr, idx, val = make_features_csr(n, cfg.num_features, y, cfg.num_classes, cfg.density, cfg.seed)
-        X = sp.csr_matrix((val, idx, ptr), shape=(n, cfg.num_features))
-    else:
-        X = make_features(n, cfg.num_features, y, cfg.num_classes, cfg.feature_kind, cfg.density, cfg.seed)
-    return {"src": src, "dst": dst, "X": X, "y": y, "n": n, "nnz_a": nnz, "k": k, "cfg": cfg}
-
-
-def _oracle_epoch_ms(sample, epochs: int):
-    """Time `epochs` epochs of the oracle (as it stands) on the sample; return per-epoch ms scaled to
-    the full workload (x k: every step is linear in N at fixed mean degree)."""
+# ---------------------------------------------------------------------------------- CPU oracle
+def _oracle_inputs(w):
+    """The oracle's view of the SAME workload the GPU arm trains (full size, no scaling): its own
+    CSR build (setup, untimed) and the cached Â operator."""
     import oracle
-    g = oracle.graph_build(sample["src"], sample["dst"], sample["n"])
+    cfg = w["cfg"]
+    g = oracle.graph_build(w["src"], w["dst"], cfg.num_nodes)
+    oracle.prepare(g)
+    if w.get("X") is not None:
+        X = w["X"]
+    else:
+        import scipy.sparse as sp
+        ptr, idx, val = w["X_csr"]
+        X = sp.csr_matrix((val, idx, ptr), shape=(cfg.num_nodes, cfg.num_features))
+    return g, X
+
+
+def _oracle_epochs_ms(w, g, X, epochs: int):
+    """Time `epochs` full epochs of the oracle as it stands (forward, softmax-CE, backward, Adam on
+    the whole graph, Listing 1) on the full workload; per-epoch wall ms."""
+    import oracle
+    cfg = w["cfg"]
+    dims = cfg.dims
+    Ws, bs = oracle.xavier_init(dims, 42)
+    params = [np.asarray(a, np.float64).copy() for a in Ws] + [np.asarray(b, np.float64).copy() for b in bs]
+    L_ = len(Ws)
+    m = [np.zeros_like(p) for p in params]
+    v = [np.zeros_like(p) for p in params]
     times = []
-    for e in range(epochs):
+    for t in range(1, epochs + 1):
         t0 = time.perf_counter()
-        oracle.train(g, sample["X"], sample["y"], sample["cfg"].dims, epochs=1, seed=42)
-        times.append(time.perf_counter() - t0)
-    return [t * 1e3 * sample["k"] for t in times]
+        Z, cache = oracle.forward(g, X, params[:L_], params[L_:], epoch=t)
+        _, dZ = oracle.softmax_ce(Z, w["y"])
+        dW, db = oracle.backward(g, cache, params[:L_], dZ)
+        oracle.adam_step(params, dW + db, m, v, t)
+        times.append((time.perf_counter() - t0) * 1e3)
+        del Z, cache, dZ
+    return times
 
 
 def _cpu_threads():
+    """Threads the oracle actually uses: its row-parallel sparse products (oracle.threads_used)
+    and the BLAS pool of its dense products (threadpoolctl)."""
+    import oracle
+    blas = 1
     try:
         from threadpoolctl import threadpool_info
-        n = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
-        return int(n)
+        blas = max((int(i.get("num_threads", 1)) for i in threadpool_info()), default=1)
     except Exception:
-        return os.cpu_count() or 1
+        pass
+    return max(oracle.threads_used(), blas), {"sparse_products": oracle.threads_used(), "blas": blas,
+                                             "host_cpus": os.cpu_count()}
 
 
-def _sample_desc(sample):
-    c = sample["cfg"]
-    return (f"oracle (FP64 numpy/scipy) full epoch on a {c.name}-shaped graph at 1/{sample['k']} scale "
-            f"(N={sample['n']}, nnz(A)={sample['nnz_a']}, dims={list(c.dims)}), time x{sample['k']}")
+def _sample_desc(w, epochs):
+    c = w["cfg"]
+    return (f"oracle (FP64 numpy/scipy, row-parallel sparse products) on the full {c.name}-shaped workload "
+            f"(N={c.num_nodes}, nnz(A)={c.nnz_a}, dims={list(c.dims)}): {epochs} whole epoch(s) "
+            f"(forward + softmax-CE + backward + Adam), no scaling")
 
 
 def _config_common(args, world):
@@ -163,22 +175,27 @@ def _config_common(args, world):
 
 
 def run_reference(args):
+    """The reference arm of this tier is the oracle (task ③/④): the SAME full-size workload as our
+    arm, each step one whole oracle epoch, W warm-up + K timed steps on the host cores."""
     rank = _env_int("RANK", 0)
     if rank != 0:
         return 0
-    sample = _oracle_sample(args.config)
-    for _ in range(args.warmup):
-        _oracle_epoch_ms(sample, 1)
-    ms = _oracle_epoch_ms(sample, args.steps)
+    from synth.generate import make_workload
+    w = make_workload(args.config)
+    g, X = _oracle_inputs(w)
+    ms_all = _oracle_epochs_ms(w, g, X, args.warmup + args.steps)
+    ms = ms_all[args.warmup:]
     v = statistics.median(ms)
-    cores = _cpu_threads()
+    cores, detail = _cpu_threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {**_config_common(args, args.gpus), "oracle_scale": f"1/{sample['k']}"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": _sample_desc(sample)},
+        "config": {**_config_common(args, args.gpus), "oracle_scale": "1/1 (full size)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "threads": detail, "kind": "oracle",
+                         "sample": _sample_desc(w, args.steps)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "epoch_ms": {"median": v, "min": min(ms), "max": max(ms), "timed_region_s": sum(ms) / 1e3},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -292,6 +309,65 @@ def _spmm_fractions(r, peak_hbm, l2_gather_gbps, l2_bytes=126 * 2 ** 20):
     if traffic:
         out["dram_frac_of_hbm"] = traffic / (k["avg_launch_ms"] * 1e6) / peak_hbm
     return out
+
+
+PEAKS = {}   # filled by run_ours before any workload is timed (probes + MEASURED_PEAKS.json)
+
+
+def _l2_ceiling(peaks):
+    """The L2 delivery ceiling measured in this run: the larger of the L2 streaming probe
+    (ld.global.cg over an L2-resident buffer) and the L2-resident random-row gather probe."""
+    cands = [peaks.get("l2_stream_GBps"), (peaks.get("gather") or {}).get("l2_resident_64MB")]
+    cands = [c for c in cands if c]
+    return max(cands) if cands else None
+
+
+def _roofline(kernels, ms, config, peaks):
+    """Roofline of the epoch's dominant kernel (task ④).
+
+    Aggregation SpMM: achieved = SURVEY §8(d) d.3's per-edge algorithmic bytes (4 B id + 4·w B
+    gathered row, the no-reuse amount Alg. 3 reads) plus per-row bytes, x the launch's
+    edges, / its CUDA-event launch time.  Every one of those bytes is delivered to the SMs by L2
+    (or hits L1), so the ceiling is the L2 delivery rate measured in this run (bound "l2"), not
+    HBM: DRAM only sees the misses (`traffic`, from the ncu capture of this code).  The
+    north star's literal "SpMM HBM GB/s vs peak" is dram_frac_of_hbm = traffic / time / HBM peak.
+    Other kernels: algorithmic bytes (A + B + C once) / time against the HBM copy peak."""
+    hbm, hbm_kind = peaks.get("hbm_gbs"), peaks.get("hbm_kind")
+    dom = max((k for k in ("spmm", "gemm_nt", "gemm_tn", "sparse_feat") if k in kernels),
+              key=lambda k: kernels[k]["ms_per_epoch"], default=None)
+    if dom is None:
+        return None
+    kd = kernels[dom]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(dom, {}).get("dram_bytes_per_launch")
+    hbm_src = ("MEASURED_PEAKS.json hbm_gbs (of measured)" if hbm_kind == "measured" else
+               "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)")
+    l2 = _l2_ceiling(peaks)
+    gathering = dom in ("spmm", "sparse_feat")
+    if gathering and l2:
+        r = {"bound": "l2", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": l2, "unit": "GB/s",
+             "frac": kd["algorithmic_GBps"] / l2, "traffic": traffic,
+             "peak_source": ("measured in this run: max(L2 streaming-read probe over a 50 MB L2-resident buffer with "
+                             "ld.global.cg, L2-resident random 512-byte-row gather probe) = "
+                             f"{l2:.0f} GB/s; the gathered bytes reach the SMs from L2, not from DRAM")}
+    else:
+        r = {"bound": "hbm", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": hbm, "unit": "GB/s",
+             "frac": kd["algorithmic_GBps"] / hbm, "traffic": traffic, "peak_source": hbm_src}
+    r["algorithmic_bytes"] = ("SURVEY 8(d) d.3 per edge of A-hat 4 + 4*w_pad B (id + gathered row, no reuse), "
+                              "per row 12 + 4*w_pad B" if dom == "spmm" else
+                              "per nonzero of X 8 + 4*w B, per row/column 8 + 4*w B" if dom == "sparse_feat" else
+                              "A + B + C bytes once")
+    r.update({"bytes_per_launch": kd["bytes_per_launch"], "avg_launch_ms": kd["avg_launch_ms"],
+              "share_of_epoch": kd["ms_per_epoch"] / ms, "hbm_peak": hbm, "hbm_peak_source": hbm_src})
+    if traffic:
+        r["dram_frac_of_hbm"] = traffic / (kd["avg_launch_ms"] * 1e6) / hbm
+        r["traffic_source"] = f"profiles/ncu_traffic_{config}.json (ncu --set full of this code, per launch)"
+    if "halo" in kernels:   # SURVEY d.4: halo bytes per rank / time / NVLink (measured peer copy, 770 GB/s)
+        r["halo_frac_of_nvlink_peer_copy_770GBps"] = kernels["halo"]["algorithmic_GBps"] / 770.0
+    return r
 
 
 def _max_over_ranks(torch, dist, v: float) -> float:
@@ -436,42 +512,16 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                          "host waits for each step's loss"}
 
     # ---------------- roofline of the dominant kernel
-    peak, peak_kind = _peaks()
-    dom = max((k for k in ("spmm", "gemm_nt", "gemm_tn", "sparse_feat") if k in kernels),
-              key=lambda k: kernels[k]["ms_per_epoch"],
-              default=None)
-    roofline = None
-    if dom is not None:
-        kd = kernels[dom]
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", f"ncu_traffic_{config}.json")
-        if os.path.exists(tp):
-            with open(tp) as fh:
-                traffic = json.load(fh).get(dom, {}).get("dram_bytes_per_launch")
-        roofline = {"bound": "hbm", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": peak, "unit": "GB/s",
-                    "frac": kd["algorithmic_GBps"] / peak, "traffic": traffic,
-                    "peak_source": ("MEASURED_PEAKS.json hbm_gbs (of measured)" if peak_kind == "measured" else
-                                    "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"),
-                    "algorithmic_bytes": ("SURVEY 8(d) d.3 no-reuse count: per edge 4 + 4*w B, per row 12 + 4*w B"
-                                          if dom == "spmm" else
-                                          "no-reuse count: per nonzero of X 8 + 4*w B, per row/column 8 + 4*w B"
-                                          if dom == "sparse_feat" else "A + B + C bytes once"),
-                    "bytes_per_launch": kd["bytes_per_launch"], "avg_launch_ms": kd["avg_launch_ms"],
-                    "share_of_epoch": kd["ms_per_epoch"] / ms}
-        if "halo" in kernels:   # SURVEY d.4: halo bytes per rank / time / NVLink (measured peer copy, 770 GB/s)
-            roofline["halo_frac_of_nvlink_peer_copy_770GBps"] = kernels["halo"]["algorithmic_GBps"] / 770.0
-        if dom == "spmm" and roofline["frac"] > 1.2:
-            roofline["note"] = ("frac > 1: the gathered operand is L2-resident, so the no-reuse algorithmic bytes "
-                                "(SURVEY d.3) exceed the DRAM traffic (see traffic); the binding ceiling is the L2 "
-                                "gather rate: frac_of_l2_gather_peak and spmm_fractions.time_efficiency_E")
-
+    roofline = _roofline(kernels, ms, config, PEAKS)
     # ---------------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
     if full and world == 1 and rank == 0 and not args.no_cpu_baseline:
-        sample = _oracle_sample(config)
-        ms_cpu = _oracle_epoch_ms(sample, 1)
-        cpu = {"value": statistics.median(ms_cpu), "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
-               "sample": _sample_desc(sample)}
+        og, oX = _oracle_inputs(w)
+        ms_cpu = _oracle_epochs_ms(w, og, oX, 1)
+        del og, oX
+        cores, detail = _cpu_threads()
+        cpu = {"value": statistics.median(ms_cpu), "unit": UNIT, "cores": cores, "threads": detail, "kind": "oracle",
+               "sample": _sample_desc(w, 1)}
 
     out = {
         "value": ms, "ms_per_step": ms,
@@ -520,6 +570,29 @@ def _gather_peaks(L, torch):
     return res
 
 
+def _l2_stream_peak(L, torch):
+    """L2 delivery ceiling: streaming reads (no L1) of a ~50 MB L2-resident buffer, best of 5."""
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    unit = 8 * sms
+    n = (50 << 20) // 4 // unit * unit
+    buf = torch.ones(n, device="cuda")
+    out = torch.empty(2 * sms * 512 * 4, device="cuda")
+    s = torch.cuda.current_stream()
+    passes, best = 20, None
+    L.mph_probe_l2_stream(buf.data_ptr(), n, 2, out.data_ptr(), s.cuda_stream)   # warm: buffer into L2
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        L.mph_probe_l2_stream(buf.data_ptr(), n, passes, out.data_ptr(), s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    del buf, out
+    torch.cuda.empty_cache()
+    return passes * n * 4 / best / 1e6
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -561,6 +634,11 @@ def run_ours(args):
             args.comm = "nccl"
     # N > 1: NCCL halo/all-reduce, or NVLink peer memory (NEXT-1: the model maps its peers itself)
     comm = (P.Comm(world, rank) if args.comm == "nccl" else "p2p") if world > 1 else None
+    hbm, hbm_kind = _peaks()
+    PEAKS.update({"hbm_gbs": hbm, "hbm_kind": hbm_kind})
+    if not args.no_probe:   # measured before any workload: the ceilings the roofline divides by
+        PEAKS["gather"] = _gather_peaks(L, torch)
+        PEAKS["l2_stream_GBps"] = _l2_stream_peak(L, torch)
     main = _measure(P, L, torch, dist, C, args, args.config, world, rank, local, comm, full=True)
     secondary = {}
     for spec in ([] if args.secondary == "none" else args.secondary.split(",")):
@@ -571,22 +649,16 @@ def run_ours(args):
             r = _measure(P, L, torch, dist, C, sargs, cfgname, world, rank, local, comm, full=False)
             secondary[spec] = {k: r[k] for k in ("value", "config", "roofline", "kernels", "gpu_launches",
                                                  "final_loss", "clocks", "epoch_ms", "_spmm_geometry")}
-    peaks = _gather_peaks(L, torch) if (world == 1 and not args.no_probe) else None
-    peak_hbm = _peaks()[0]
-    l2g = peaks["l2_resident_64MB"] if peaks else None
+    l2g = _l2_ceiling(PEAKS)
     l2_bytes = int(getattr(torch.cuda.get_device_properties(local), "L2_cache_size", 126 * 2 ** 20))
     for r in [main] + list(secondary.values()):
         if r.get("roofline") is not None:
-            fr = _spmm_fractions(r, peak_hbm, l2g, l2_bytes)
+            fr = _spmm_fractions(r, hbm, l2g, l2_bytes)
             if fr:
                 r["roofline"]["spmm_fractions"] = fr
+            if PEAKS.get("gather"):
+                r["roofline"]["measured_probe_GBps"] = {**PEAKS["gather"], "l2_stream": PEAKS.get("l2_stream_GBps")}
         r.pop("_spmm_geometry", None)
-    if peaks and main["roofline"] and main["roofline"]["kernel"] == "spmm":
-        main["roofline"]["measured_gather_peaks_GBps"] = peaks
-        main["roofline"]["frac_of_l2_gather_peak"] = main["roofline"]["achieved"] / peaks["l2_resident_64MB"]
-    for r in secondary.values():
-        if peaks and r["roofline"] and r["roofline"]["kernel"] == "spmm":
-            r["roofline"]["frac_of_l2_gather_peak"] = r["roofline"]["achieved"] / peaks["l2_resident_64MB"]
 
     if rank == 0:
         line = {

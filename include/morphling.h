@@ -313,6 +313,11 @@ int mph_profile_read(int32_t kind, int64_t* count_h, double* total_ms_h, double*
  * the L2-resident and HBM-resident random-row gather peaks the SpMM is compared with. */
 int mph_probe_gather(const float* table_d, int64_t n_rows, int32_t w, const int32_t* idx_d, int64_t n_idx,
                      float* out_d, void* stream);
+/* L2 delivery ceiling: a coalesced streaming read (ld.global.cg, no L1) of an L2-resident buffer
+ * buf_d [n_floats] repeated `passes` times by 2 x SMs blocks of 512 threads (n_floats a multiple
+ * of 8 x SMs; out_d needs 2 x SMs x 2048 floats).  rate = passes * n_floats * 4 / time.  bench.py
+ * reports the aggregation's gathered bytes per second against max(this, the gather probe). */
+int mph_probe_l2_stream(const float* buf_d, int64_t n_floats, int32_t passes, float* out_d, void* stream);
 
 /* =====================================================================================
  * a10/a11 — distributed runtime (MPI backend analogue).

@@ -24,7 +24,7 @@ __all__ = [
     "connected_components", "partition_components", "partition_greedy", "partition_hierarchical", "relabel",
     "partition_stats",
     "OPTIMIZERS", "sgd_step", "adamw_step",
-    "partition_1d", "localize", "LocalPlan", "GOLDEN",
+    "partition_1d", "localize", "LocalPlan", "GOLDEN", "prepare", "threads_used", "csr_matmul",
 ]
 
 GOLDEN = 0x9E3779B97F4A7C15
@@ -106,6 +106,16 @@ def _a_hat_csr(g: Graph) -> sp.csr_matrix:
                           shape=(g.num_nodes, g.num_nodes))
         object.__setattr__(g, "_a_hat", A)
     return A
+
+
+def prepare(g: Graph) -> None:
+    """Build the graph's cached Â / Ã operators now (setup, the analogue of the CSR build)."""
+    _a_hat_csr(g)
+
+
+def threads_used() -> int:
+    """Host threads the sparse products use (ORACLE_THREADS, default: all cores)."""
+    return _threads()
 
 
 def _threads() -> int:

@@ -124,6 +124,7 @@ _SIGS = {
     "mph_gcn_set_labels": [P, P, P, i64],
     "mph_profile_enable": [i32],
     "mph_probe_gather": [P, i64, i32, P, i64, P, P],
+    "mph_probe_l2_stream": [P, i64, i32, P, P],
     "mph_profile_read": [i32, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)],
     "mph_gcn_forward": [P, i32, P],
     "mph_gcn_loss": [P, P, P],
