@@ -450,6 +450,20 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
         raise RuntimeError(f"rank {rank}: a peer-memory wait timed out (MPH_ETIMEOUT); the timings are invalid")
     if world > 1:
         ms = _max_over_ranks(torch, dist, ms)
+        # evidence of the transport: which GPUs reach each other, whether any peer
+        # wait timed out, and what one halo exchange moved and took on this rank
+        ndev = torch.cuda.device_count()
+        hk = kernels.get("halo")
+        extra["transport"] = {
+            "comm": args.comm,
+            "peer_access": [[bool(i == j or torch.cuda.can_device_access_peer(i, j)) for j in range(ndev)]
+                            for i in range(ndev)],
+            "p2p_status": m.p2p_status() if args.comm == "p2p" else None,
+            "halo_exchanges_per_epoch": hk["launches_per_epoch"] if hk else None,
+            "halo_bytes_per_exchange": hk["bytes_per_launch"] if hk else None,
+            "halo_ms_per_exchange": hk["avg_launch_ms"] if hk else None,
+            "halo_GBps": hk["algorithmic_GBps"] if hk else None,
+        }
 
     # ---------------- end-to-end through the public API with host buffers
     e2e = None

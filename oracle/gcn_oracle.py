@@ -471,11 +471,14 @@ def softmax_ce(Z, labels, mask=None, n_lab: int | None = None):
 
 def backward(g: Graph, cache, Ws, dZ):
     """B1-B4: returns (dWs, dbs).  The upstream gradient of every layer, dZ_l = ∂loss/∂Z_l, is
-    recorded in cache["dZ"][l-1] (an output for bounds in tests; no extra arithmetic)."""
+    recorded in cache["dZ"][l-1], and the gradient w.r.t. the hidden activation before the ReLU
+    mask, dH_l = ∂loss/∂H_l, in cache["dH"][l-1] for l < L (outputs for bounds in tests; no extra
+    arithmetic)."""
     L = len(Ws)
     dWs, dbs = [None] * L, [None] * L
     agg = cache.get("aggregator", "gcn")
     cache["dZ"] = [None] * L
+    cache["dH"] = [None] * L
     for l in range(L, 0, -1):
         cache["dZ"][l - 1] = dZ
         dbs[l - 1] = dZ.sum(axis=0)                                     # B1
@@ -493,6 +496,7 @@ def backward(g: Graph, cache, Ws, dZ):
             if l > 1:
                 dH = _operand(G, r) @ _operand(W, r).T                   # B4
         if l > 1:
+            cache["dH"][l - 2] = dH
             dZ = dH * (cache["Z"][l - 2] > 0.0)                          # ReLU'(0) := 0 (Q8)
             if cache["dropout_p"] > 0.0:
                 keep = dropout_keep(dZ.shape[0], dZ.shape[1], cache["dropout_p"], cache["seed"],
