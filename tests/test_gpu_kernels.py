@@ -402,27 +402,3 @@ def test_sparse_feature_kernels(P, name, fo):
     assert float((np.abs(dW.cpu().numpy() - ref_dW) / (1e-5 * bound_dW + 1e-30)).max()) <= 1.0
 
 
-
-@pytest.mark.parametrize("w", [48, 64, 128, 256])
-def test_spmm_l1_hints(P, w, monkeypatch):
-    """Deep graphs (mean degree >= 16) aggregate with L1 residency hints: each row's ids stored
-    hot-first (the most-gathered columns of its row panel) with hot loads kept in L1 and cold ones
-    not allocated.  The per-row summation order differs from the plain kernel, so the two agree
-    within the FP32 aggregation bound, each is bitwise deterministic, and the hub-block budget
-    still holds (a degree-3000 hub)."""
-    wk = make_small(6000, 150000, 4, 5, seed=41, alpha=2.1)      # mean degree ~51: a deep graph
-    src = np.concatenate([wk["src"], np.full(3000, 7, np.int32)])
-    dst = np.concatenate([wk["dst"], np.arange(8, 3008, dtype=np.int32)])
-    rng = np.random.default_rng(w)
-    ref = oracle.graph_build(src, dst, 6000)
-    T = rng.standard_normal((6000, w)).astype(np.float32)
-    tin = cuda((ref.dinv[:, None] * T).astype(np.float32))
-    Zref, bound = oracle.aggregate(ref, T), agg_bound(ref, T)
-    for k in ("0", "256"):
-        monkeypatch.setenv("MPH_SPMM_HOT", k)
-        g = P.Graph(src, dst, 6000)
-        o1, o2 = torch.zeros((6000, w), device="cuda"), torch.zeros((6000, w), device="cuda")
-        g.spmm(tin, o1, w=w)
-        g.spmm(tin, o2, w=w)
-        assert torch.equal(o1, o2)
-        assert_agg_close(o1.cpu().numpy(), Zref, bound, what=f"spmm w={w} hot={k}")
