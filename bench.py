@@ -315,11 +315,24 @@ PEAKS = {}   # filled by run_ours before any workload is timed (probes + MEASURE
 
 
 def _l2_ceiling(peaks):
-    """The L2 delivery ceiling measured in this run: the larger of the L2 streaming probe
-    (ld.global.cg over an L2-resident buffer) and the L2-resident random-row gather probe."""
+    """(GB/s, source) of the L2 delivery ceiling: the LTS byte peak ncu reports for this part
+    (profiles/l2_peak.json: lts__t_bytes.sum.peak_sustained x the L2 clock, 34.6 TB/s on B200), a
+    rate no kernel can exceed; without that file, the best of this run's probes (an L2-resident
+    streaming read and random-row gather), which the aggregation itself can beat."""
+    p = os.path.join(ROOT, "profiles", "l2_peak.json")
+    if os.path.exists(p):
+        try:
+            with open(p) as f:
+                v = float(json.load(f)["lts_bytes_peak_GBps"])
+            return v, ("ncu LTS byte peak of B200 (lts__t_bytes.sum.peak_sustained x L2 clock = "
+                       f"{v:.0f} GB/s, profiles/l2_peak.json)")
+        except (OSError, ValueError, KeyError, TypeError):
+            pass
     cands = [peaks.get("l2_stream_GBps"), (peaks.get("gather") or {}).get("l2_resident_64MB")]
     cands = [c for c in cands if c]
-    return max(cands) if cands else None
+    if not cands:
+        return None, None
+    return max(cands), "measured in this run: max(L2 streaming-read probe, L2-resident random-row gather probe)"
 
 
 def _roofline(kernels, ms, config, peaks):
@@ -345,14 +358,13 @@ def _roofline(kernels, ms, config, peaks):
             traffic = json.load(fh).get(dom, {}).get("dram_bytes_per_launch")
     hbm_src = ("MEASURED_PEAKS.json hbm_gbs (of measured)" if hbm_kind == "measured" else
                "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)")
-    l2 = _l2_ceiling(peaks)
+    l2, l2_src = _l2_ceiling(peaks)
     gathering = dom in ("spmm", "sparse_feat")
     if gathering and l2:
         r = {"bound": "l2", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": l2, "unit": "GB/s",
              "frac": kd["algorithmic_GBps"] / l2, "traffic": traffic,
-             "peak_source": ("measured in this run: max(L2 streaming-read probe over a 50 MB L2-resident buffer with "
-                             "ld.global.cg, L2-resident random 512-byte-row gather probe) = "
-                             f"{l2:.0f} GB/s; the gathered bytes reach the SMs from L2, not from DRAM")}
+             "peak_source": l2_src + "; every gathered byte reaches the SMs through L2 (or hits L1), DRAM only "
+                                     "sees the misses (traffic)"}
     else:
         r = {"bound": "hbm", "kernel": dom, "achieved": kd["algorithmic_GBps"], "peak": hbm, "unit": "GB/s",
              "frac": kd["algorithmic_GBps"] / hbm, "traffic": traffic, "peak_source": hbm_src}
@@ -663,7 +675,7 @@ def run_ours(args):
             r = _measure(P, L, torch, dist, C, sargs, cfgname, world, rank, local, comm, full=False)
             secondary[spec] = {k: r[k] for k in ("value", "config", "roofline", "kernels", "gpu_launches",
                                                  "final_loss", "clocks", "epoch_ms", "_spmm_geometry")}
-    l2g = _l2_ceiling(PEAKS)
+    l2g = (PEAKS.get("gather") or {}).get("l2_resident_64MB")   # d.4's E: the L2 random-row gather rate
     l2_bytes = int(getattr(torch.cuda.get_device_properties(local), "L2_cache_size", 126 * 2 ** 20))
     for r in [main] + list(secondary.values()):
         if r.get("roofline") is not None:

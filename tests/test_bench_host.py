@@ -61,10 +61,13 @@ def test_roofline_bounds(tmp_path, monkeypatch):
     k = {"spmm": {"ms_per_epoch": 8.0, "avg_launch_ms": 2.0, "algorithmic_GBps": 19000.0, "bytes_per_launch": 3.8e10},
          "gemm_nt": {"ms_per_epoch": 0.5, "avg_launch_ms": 0.1, "algorithmic_GBps": 5000.0, "bytes_per_launch": 5e8}}
     r = bench._roofline(k, 9.0, "reddit", peaks)
-    assert r["bound"] == "l2" and r["kernel"] == "spmm" and r["peak"] == 21000.0
+    assert r["bound"] == "l2" and r["kernel"] == "spmm" and r["peak"] == 21000.0   # no ncu peak: probes
     assert r["frac"] == pytest.approx(19000.0 / 21000.0)
     assert r["traffic"] is None and "dram_frac_of_hbm" not in r
     (tmp_path / "profiles").mkdir()
+    (tmp_path / "profiles" / "l2_peak.json").write_text('{"lts_bytes_peak_GBps": 34650.0}')
+    r = bench._roofline(k, 9.0, "reddit", peaks)
+    assert r["peak"] == 34650.0 and r["frac"] == pytest.approx(19000.0 / 34650.0) and "ncu" in r["peak_source"]
     (tmp_path / "profiles" / "ncu_traffic_reddit.json").write_text('{"spmm": {"dram_bytes_per_launch": 1.0e9}}')
     r = bench._roofline(k, 9.0, "reddit", peaks)
     assert r["dram_frac_of_hbm"] == pytest.approx(1.0e9 / 2.0e6 / 6500.0)

@@ -402,3 +402,4 @@ def test_sparse_feature_kernels(P, name, fo):
     assert float((np.abs(dW.cpu().numpy() - ref_dW) / (1e-5 * bound_dW + 1e-30)).max()) <= 1.0
 
 
+
