@@ -457,6 +457,14 @@ def _measure(P, L, torch, dist, C, args, config, world, rank, local, comm, full:
                              "avg_launch_ms": tms.value / cnt.value, "algorithmic_GBps": by.value / tms.value / 1e6,
                              "bytes_per_launch": by.value / cnt.value, "TFLOPs": fl.value / tms.value / 1e9}
     L.mph_profile_enable(0)
+    if "gemm_tn" in kernels:
+        # gcn.cu: the weight-gradient GEMMs leave the critical path for a side stream when every
+        # aggregation operand fits 512 MB (reddit, arxiv); their event span then includes the
+        # concurrent aggregation, so it is wall time on that stream, not kernel time
+        nc = w["cfg"].num_nodes
+        side = nc * max(P.pad_width(d) for d in w["cfg"].dims[1:]) * 4.0 <= 512.0 * (1 << 20)
+        kernels["gemm_tn"]["stream"] = ("side stream, overlapped with the next aggregation: ms is wall time on "
+                                        "that stream, not kernel time") if side else "compute stream (in line)"
     loss_last = m.loss_buf.item()
     if world > 1 and args.comm == "p2p" and m.p2p_status() != 0:
         raise RuntimeError(f"rank {rank}: a peer-memory wait timed out (MPH_ETIMEOUT); the timings are invalid")

@@ -36,7 +36,11 @@ Parity status of each function (pins live in tests/test_oracle_*.py):
                                   component cases, scipy connected components, the greedy's
                                   list-scheduling bound, brute-force recounts, permutation
                                   invariance of training under relabelling)
+  bounds.tf32_gradient_bounds ... a test tolerance, not an oracle result; pinned by an FP32
+                                  emulation of the GPU's arithmetic staying inside it while the
+                                  bound stays tight (tests/test_oracle_bounds.py)
   absolute model quality vs the paper ... parity unpinned (the paper prints no loss
                                            or accuracy value)
 """
 from .gcn_oracle import *  # noqa: F401,F403
+from .bounds import FLOOR_REL, tf32_gradient_bounds  # noqa: F401

@@ -417,14 +417,21 @@ def _operand(M, rounding):
 
 
 def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: int = 1, operand_rounding=None,
-            aggregator: str = "gcn"):
+            aggregator: str = "gcn", orders=None):
     # X may be a scipy CSR matrix (sparse features): X·W_1 and X^T·G are then sparse products.
     # operand_rounding="tf32" rounds both operands of every dense product H·W (R2); sparse products
     # (X_csr·W_1) and the aggregation stay exact.  It models transform-first layers.
     # aggregator: "gcn" (Â, the north star), "sum", "mean" (linear: Z = AGG(H·W) + b) or "max"
     # (Z = MAX(H)·W + b, R7); see aggregate_scheme / aggregate_max.
+    # orders: per layer "TF" (transform first, Z = AGG(H·W) + b, the default) or "AF" (aggregate
+    # first, Z = AGG(H)·W + b) — the same Z in exact arithmetic (AGG is linear, P:88 / reading Q7);
+    # the order only decides which operand a rounded product sees (operand_rounding: AF rounds
+    # Y = AGG(H), TF rounds H).
     if aggregator not in AGGREGATORS:
         raise ValueError(aggregator)
+    orders = tuple(orders) if orders is not None else ("TF",) * len(Ws)
+    if len(orders) != len(Ws) or any(o not in ("TF", "AF") for o in orders):
+        raise ValueError(orders)
     H = X.astype(np.float64).tocsr() if sp.issparse(X) else np.asarray(X, dtype=np.float64)
     hs, zs, ys, args = [H], [], [], []
     L = len(Ws)
@@ -438,7 +445,14 @@ def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: i
             ys.append(Y)
             args.append(arg)
             Z = _operand(Y, r) @ _operand(W, r) + np.asarray(bs[l - 1], dtype=np.float64)
+        elif orders[l - 1] == "AF":
+            if sp.issparse(H):
+                raise ValueError("aggregate-first needs dense features")
+            Y = aggregate_scheme(g, H, aggregator)                       # F2 before F1 (Q7)
+            ys.append(Y)
+            Z = _operand(Y, r) @ _operand(W, r) + np.asarray(bs[l - 1], dtype=np.float64)
         else:
+            ys.append(None)
             P = _operand(H, r) @ (W if sp.issparse(H) else _operand(W, r))   # F1
             Z = aggregate_scheme(g, P, aggregator) + np.asarray(bs[l - 1], dtype=np.float64)   # F2
         zs.append(Z)
@@ -449,7 +463,7 @@ def forward(g: Graph, X, Ws, bs, dropout_p: float = 0.0, seed: int = 0, epoch: i
                 H = H * keep / (1.0 - float(np.float32(dropout_p)))
             hs.append(H)
     return zs[-1], {"H": hs, "Z": zs, "dropout_p": dropout_p, "seed": seed, "epoch": epoch, "rounding": r,
-                    "aggregator": aggregator, "Y": ys, "arg": args}
+                    "aggregator": aggregator, "Y": ys, "arg": args, "orders": orders}
 
 
 def softmax_ce(Z, labels, mask=None, n_lab: int | None = None):
@@ -489,6 +503,10 @@ def backward(g: Graph, cache, Ws, dZ):
             if l > 1:
                 dY = _operand(dZ, r) @ _operand(W, r).T
                 dH = aggregate_max_backward(dY, cache["arg"][l - 1], g.num_nodes)
+        elif cache.get("orders", ("TF",) * L)[l - 1] == "AF":           # Z = Y·W + b, Y = AGG(H)
+            dWs[l - 1] = _operand(cache["Y"][l - 1], r).T @ _operand(dZ, r)
+            if l > 1:
+                dH = aggregate_scheme(g, _operand(dZ, r) @ _operand(W, r).T, agg, transpose=True)
         else:
             G = aggregate_scheme(g, dZ, agg, transpose=True)             # B2 (Âᵀ = Â)
             Hp = cache["H"][l - 1]
@@ -544,7 +562,7 @@ OPTIMIZERS = ("adam", "sgd", "adamw")
 def train(g: Graph, X, labels, dims, epochs: int, seed: int = 42, lr=0.01, beta1=0.9,
           beta2=0.999, eps=1e-8, mask=None, dropout_p: float = 0.0, dropout_seed: int = 0,
           init=None, operand_rounding=None, aggregator: str = "gcn", optimizer: str = "adam",
-          weight_decay: float = 0.0, momentum: float = 0.0):
+          weight_decay: float = 0.0, momentum: float = 0.0, orders=None):
     """Epoch loop (Listing 1): loss_t at θ_{t-1}, backward, optimizer -> θ_t
     (Adam by default; SGD / AdamW)."""
     if optimizer not in OPTIMIZERS:
@@ -559,7 +577,8 @@ def train(g: Graph, X, labels, dims, epochs: int, seed: int = 42, lr=0.01, beta1
     v = [np.zeros_like(p) for p in params]
     losses = []
     for t in range(1, epochs + 1):
-        Z, cache = forward(g, X, params[:L], params[L:], dropout_p, dropout_seed, t, operand_rounding, aggregator)
+        Z, cache = forward(g, X, params[:L], params[L:], dropout_p, dropout_seed, t, operand_rounding, aggregator,
+                           orders)
         loss, dZ = softmax_ce(Z, labels, mask)
         losses.append(loss)
         dWs, dbs = backward(g, cache, params[:L], dZ)

@@ -130,3 +130,75 @@ def test_bf16_trajectory_within_north_star():
     ex, bf = np.array(ex), np.array(bf)
     assert np.all(np.abs(bf - ex) <= 1e-3 * np.maximum(1.0, np.abs(ex))), np.abs(bf - ex).max()
     assert not np.array_equal(bf, ex)
+
+
+# ---------------------------------------------------------------- layer order (reading Q7)
+def test_aggregate_first_equals_transform_first_exact():
+    """orders=("AF", ...) computes Z = (Â·H)·W + b instead of Â·(H·W) + b: the same numbers in
+    exact arithmetic (associativity of the linear maps), so without operand rounding the
+    loss and every gradient agree to FP64 rounding, for the GCN and the linear schemes (mean is
+    not symmetric, so its AF backward needs the adjoint D̃⁻¹-on-the-right path to be right)."""
+    w = make_small(400, 3200, 12, 4, seed=8)
+    g = oracle.graph_build(w["src"], w["dst"], 400)
+    dims = (12, 20, 16, 4)
+    Ws, bs = oracle.xavier_init(dims, 42)
+    for agg in ("gcn", "sum", "mean"):
+        Zt, ct = oracle.forward(g, w["X"], Ws, bs, aggregator=agg)
+        Za, ca = oracle.forward(g, w["X"], Ws, bs, aggregator=agg, orders=("AF", "AF", "TF"))
+        assert np.allclose(Za, Zt, rtol=1e-12, atol=1e-12)
+        lt, dZt = oracle.softmax_ce(Zt, w["y"])
+        la, dZa = oracle.softmax_ce(Za, w["y"])
+        assert abs(lt - la) <= 1e-12 * abs(lt)
+        gt = oracle.backward(g, ct, Ws, dZt)
+        ga = oracle.backward(g, ca, Ws, dZa)
+        for a, b in zip(gt[0] + gt[1], ga[0] + ga[1]):
+            assert np.allclose(a, b, rtol=1e-10, atol=1e-14), agg
+
+
+def test_aggregate_first_gradient_by_finite_differences():
+    """An independent pin of the AF backward (not a re-derivation of it): central differences of
+    the loss in three entries of W_1 and b_1 of an aggregate-first layer 1."""
+    w = make_small(120, 700, 6, 3, seed=9)
+    g = oracle.graph_build(w["src"], w["dst"], 120)
+    dims = (6, 9, 3)
+    Ws, bs = [np.asarray(a, np.float64) for a in oracle.xavier_init(dims, 3)[0]], \
+        [np.asarray(b, np.float64) + 0.01 for b in oracle.xavier_init(dims, 3)[1]]
+    orders = ("AF", "TF")
+    Z, c = oracle.forward(g, w["X"], Ws, bs, orders=orders)
+    _, dZ = oracle.softmax_ce(Z, w["y"])
+    dW, db = oracle.backward(g, c, Ws, dZ)
+
+    def loss_at(Wm, bm):
+        return oracle.softmax_ce(oracle.forward(g, w["X"], Wm, bm, orders=orders)[0], w["y"])[0]
+    h = 1e-6
+    for (i, j) in ((0, 0), (3, 5), (5, 8)):
+        Wp = [a.copy() for a in Ws]
+        Wm = [a.copy() for a in Ws]
+        Wp[0][i, j] += h
+        Wm[0][i, j] -= h
+        fd = (loss_at(Wp, bs) - loss_at(Wm, bs)) / (2 * h)
+        assert abs(fd - dW[0][i, j]) <= 1e-6 * max(1.0, abs(fd)), (i, j, fd, dW[0][i, j])
+    bp = [b.copy() for b in bs]
+    bm = [b.copy() for b in bs]
+    bp[0][2] += h
+    bm[0][2] -= h
+    fd = (loss_at(Ws, bp) - loss_at(Ws, bm)) / (2 * h)
+    assert abs(fd - db[0][2]) <= 1e-6 * max(1.0, abs(fd))
+
+
+def test_tf32_aggregate_first_rounds_the_aggregate():
+    """With operand_rounding="tf32", an AF layer 1 rounds Y = Â·X (the kernel's stored operand)
+    and not X: Z_1 moves from the exact value by at most (2^-11 + 2^-11 + 2^-22)|Y||W| (the GEMM
+    bound of one rounded product), and differs from the TF-rounded Z_1."""
+    w = make_small(300, 2400, 24, 5, seed=5)
+    g = oracle.graph_build(w["src"], w["dst"], 300)
+    dims = (24, 40, 5)
+    Ws, bs = oracle.xavier_init(dims, 42)
+    _, c0 = oracle.forward(g, w["X"], Ws, bs)
+    _, ca = oracle.forward(g, w["X"], Ws, bs, operand_rounding="tf32", orders=("AF", "TF"))
+    _, ct = oracle.forward(g, w["X"], Ws, bs, operand_rounding="tf32")
+    Y = oracle.aggregate(g, w["X"].astype(np.float64))
+    e = 2.0 ** -11 * 2 + 2.0 ** -22
+    assert np.all(np.abs(ca["Z"][0] - c0["Z"][0]) <= e * np.abs(Y) @ np.abs(Ws[0].astype(np.float64)) + 1e-15)
+    assert not np.array_equal(ca["Z"][0], ct["Z"][0])
+    assert np.array_equal(ca["Y"][0], Y)

@@ -7,18 +7,21 @@ Per config (BASELINE.json's Reddit- and ogbn-products-shaped workloads, SURVEY Â
 
 * ``losses`` â€” loss_1..loss_E of the free-running FP64 trajectory (Listing 1: forward,
   softmax-CE, backward, Adam(0.01, 0.9, 0.999), Xavier seed 42; SURVEY c.5 / Q24).
-* ``g1_*`` â€” the epoch-1 gradients dW_l, db_l at Î¸_0 and their element-wise magnitude bounds
-  ``bW_l = |H_{l-1}|áµ€Â·(Ã‚Â·M_l)`` and ``bb_l = Î£_u M_l[u]`` (the GEMM bound of SURVEY c.5,
-  ``|C âˆ’ C*| â‰¤ 2e-3Â·(|A|Â·|B|)``, composed through the aggregation: Ã‚ â‰¥ 0 and Ã‚áµ€ = Ã‚ make
-  ``|H|áµ€Â·|Ã‚Â·dZ| â‰¤ |H|áµ€Â·Ã‚Â·|dZ| = (Ã‚Â·|H|)áµ€Â·|dZ|``, so one bound serves the transform-first product
-  ``Háµ€Â·(Ã‚Â·dZ)`` and the aggregate-first ``(Ã‚Â·H)áµ€Â·dZ``).  M_l = |dZ_l| on the output layer; on a
-  ReLU layer (reading Q8, ReLU'(0) := 0) the mask is a discontinuity: where the pre-activation
-  lies within the forward GEMM tolerance of zero, ``|Z_l| â‰¤ 2e-3Â·Ã‚Â·(|H_{l-1}|Â·|W_l|)``, either
-  side of the mask is a correct rounding of the same product, so there the bound takes the
-  unmasked gradient: ``M_l = |dZ_l| + [|Z_l| â‰¤ 2e-3Â·Ã‚Â·(|H_{l-1}|Â·|W_l|)]Â·|dH_l|``.
-* ``tf<t>_*`` â€” teacher-forced epochs: Î¸_{t-1} of the oracle's trajectory rounded to FP32 (what
-  the GPU can hold), and the oracle's loss_t and gradients at exactly that FP32 Î¸, with bounds.
-  These keep the check meaningful after the synthetic task's loss collapses.
+* ``g1_*`` â€” the epoch-1 gradients dW_l, db_l of the exact oracle at Î¸_0 (compared normwise,
+  reading R1).
+* ``g1t_*`` â€” the same gradients from the oracle with the kernel's operand rounding
+  (``operand_rounding="tf32"``, reading R2: both operands of every dense product rounded to TF32
+  as the GPU stores them, in the GPU's layer orders, reading Q7), with the element-wise bounds of
+  ``oracle.tf32_gradient_bounds`` (oracle/bounds.py): the GEMM bound of each weight-gradient
+  product, ``2e-3Â·|A_l|áµ€Â·|B_l|`` for ``dW_l = A_láµ€Â·B_l`` (SURVEY c.5 "gradients can be compared after
+  step 1 with the GEMM bound", the north star's 2e-3 applied to one product), plus the ReLU
+  decisions FP32 accumulation can flip.  With the operand rounding on both sides what remains
+  between GPU and oracle is FP32 accumulation order; against the EXACT oracle the TF32 error of
+  every upstream product feeds each dW through cancelling sums, which no single-product bound
+  covers (measured: 5-40x over it on products' layer 2), hence the two references.
+* ``tf<t>_*`` / ``tf<t>t_*`` â€” teacher-forced epochs: Î¸_{t-1} of the oracle's trajectory rounded
+  to FP32 (what the GPU can hold), and both oracles' loss_t and gradients at exactly that FP32 Î¸
+  (bounds as above).  These keep the check meaningful after the synthetic task's loss collapses.
 * ``input_sha256`` â€” a digest of the generated (src, dst, X, y), so a test can tell that it
   regenerated the same inputs.
 
@@ -54,36 +57,35 @@ def input_digest(w) -> str:
     return h.hexdigest()
 
 
-def grads_with_bounds(g, X, Ws, bs, labels):
-    """loss, dWs, dbs at (Ws, bs) and the element-wise magnitude bounds (module docstring).  The
-    bounds are magnitudes scaled by 2e-3 in the test, so they are formed in FP32 (relative error
-    ~1e-7), layer by layer from the top, releasing the oracle's activations as they are used
-    (products-sized caches are ~45 GB in FP64)."""
-    import scipy.sparse as sp
+def layer_orders(dims, dense_features=True):
+    """The GPU's layer orders (reading Q7, DESIGN Â§2): layer 1 aggregate-first iff its features are
+    dense and F_1 > F_0; every other layer transform-first."""
+    return tuple("AF" if (l == 0 and dense_features and dims[1] > dims[0]) else "TF" for l in range(len(dims) - 1))
+
+
+def exact_grads(g, X, Ws, bs, labels):
+    """loss, dWs, dbs of the exact FP64 oracle at (Ws, bs)."""
     Z, cache = oracle.forward(g, X, Ws, bs)
     loss, dZ = oracle.softmax_ce(Z, labels)
     dWs, dbs = oracle.backward(g, cache, Ws, dZ)
+    return loss, dWs, dbs
+
+
+def tf32_grads_with_bounds(g, X, Ws, bs, labels, orders):
+    """loss, dWs, dbs of the TF32-operand oracle and oracle.tf32_gradient_bounds, formed in FP32
+    (a tolerance), releasing the activations as they are used (products-sized FP64 caches are
+    ~45 GB)."""
+    Z, cache = oracle.forward(g, X, Ws, bs, operand_rounding="tf32", orders=orders)
+    loss, dZ = oracle.softmax_ce(Z, labels)
+    dWs, dbs = oracle.backward(g, cache, Ws, dZ)
     del Z, dZ
-    A32 = sp.csr_matrix((oracle.a_hat_values(g).astype(np.float32), g.col_idx, g.row_ptr),
-                        shape=(g.num_nodes, g.num_nodes))
-    L = len(Ws)
-    bWs, bbs = [None] * L, [None] * L
-    f32 = lambda a: np.abs(np.asarray(a.toarray() if sp.issparse(a) else a)).astype(np.float32)  # noqa: E731
-    for l in range(L - 1, -1, -1):
-        M = f32(cache["dZ"][l])
-        Hp = f32(cache["H"][l])
-        if l < L - 1:   # a ReLU layer: the mask is undecided within the forward tolerance
-            bz = oracle.csr_matmul(A32, Hp @ f32(Ws[l]))
-            amb = np.abs(cache["Z"][l]) <= 2e-3 * bz
-            del bz
-            M += amb * f32(cache["dH"][l])
-            del amb
-        bWs[l] = (Hp.T @ oracle.csr_matmul(A32, M)).astype(np.float64)
-        bbs[l] = M.sum(axis=0, dtype=np.float64)
-        del M, Hp
-        cache["dZ"][l] = cache["Z"][l] = cache["dH"][l] = None
-        if l + 1 < len(cache["H"]):
-            cache["H"][l + 1] = None
+    cache["Z"][-1] = None   # the output layer's Z is not needed by the bound (no ReLU)
+    for key in ("H", "Z", "Y", "dZ", "dH"):   # a tolerance needs no FP64: halve the ~45 GB cache
+        for i, a in enumerate(cache[key]):
+            if isinstance(a, np.ndarray) and a.dtype == np.float64:
+                cache[key][i] = a.astype(np.float32)
+                del a
+    bWs, bbs = oracle.tf32_gradient_bounds(g, cache, Ws, bs, release=True, dtype=np.float32)
     return loss, dWs, dbs, bWs, bbs
 
 
@@ -106,13 +108,20 @@ def main():
         out = {"input_sha256": np.array(digest), "dims": np.array(dims, np.int64), "seed": np.array(42),
                "adam": np.array([0.01, 0.9, 0.999, 1e-8])}
 
-        # epoch-1 gradients and bounds at Î¸_0
+        orders = layer_orders(dims)
+        out["orders"] = np.array(orders)
+
+        # epoch-1 gradients at Î¸_0: exact, and TF32-operand with bounds
         Ws, bs = oracle.xavier_init(dims, 42)
-        loss1, dWs, dbs, bWs, bbs = grads_with_bounds(g, X, Ws, bs, y)
+        loss1, dWs, dbs = exact_grads(g, X, Ws, bs, y)
         for l in range(L):
             out[f"g1_dW{l + 1}"], out[f"g1_db{l + 1}"] = dWs[l], dbs[l]
-            out[f"g1_bW{l + 1}"], out[f"g1_bb{l + 1}"] = bWs[l], bbs[l]
-        print(f"[{name}] epoch-1 gradients {time.time() - t0:.1f} s (loss1 {loss1:.9f})", flush=True)
+        lt1, dWs, dbs, bWs, bbs = tf32_grads_with_bounds(g, X, Ws, bs, y, orders)
+        for l in range(L):
+            out[f"g1t_dW{l + 1}"], out[f"g1t_db{l + 1}"] = dWs[l], dbs[l]
+            out[f"g1t_bW{l + 1}"], out[f"g1t_bb{l + 1}"] = bWs[l], bbs[l]
+        out["g1t_loss"] = np.array(lt1)
+        print(f"[{name}] epoch-1 gradients {time.time() - t0:.1f} s (loss1 {loss1:.9f}, tf32 {lt1:.9f})", flush=True)
 
         # free-running trajectory, keeping Î¸_{t-1} for the teacher-forced epochs
         params = [np.asarray(a, np.float64).copy() for a in Ws] + [np.asarray(b, np.float64).copy() for b in bs]
@@ -136,12 +145,16 @@ def main():
         for t, th in snaps.items():
             Wt = [a.astype(np.float64) for a in th[:L]]
             bt = [b.astype(np.float64) for b in th[L:]]
-            lt, dW, db, bW, bb = grads_with_bounds(g, X, Wt, bt, y)
+            lt, dW, db = exact_grads(g, X, Wt, bt, y)
             out[f"tf{t}_loss"] = np.array(lt)
             for l in range(L):
                 out[f"tf{t}_W{l + 1}"], out[f"tf{t}_b{l + 1}"] = th[l], th[L + l]
                 out[f"tf{t}_dW{l + 1}"], out[f"tf{t}_db{l + 1}"] = dW[l], db[l]
-                out[f"tf{t}_bW{l + 1}"], out[f"tf{t}_bb{l + 1}"] = bW[l], bb[l]
+            lr, dW, db, bW, bb = tf32_grads_with_bounds(g, X, Wt, bt, y, orders)
+            out[f"tf{t}t_loss"] = np.array(lr)
+            for l in range(L):
+                out[f"tf{t}t_dW{l + 1}"], out[f"tf{t}t_db{l + 1}"] = dW[l], db[l]
+                out[f"tf{t}t_bW{l + 1}"], out[f"tf{t}t_bb{l + 1}"] = bW[l], bb[l]
             print(f"[{name}] teacher-forced epoch {t}: loss {lt:.9f}", flush=True)
         out["tf_epochs"] = np.array(sorted(snaps), np.int64)
         path = os.path.join(GOLDEN, f"fullsize_{name}.npz")
