@@ -89,6 +89,25 @@ def tf32_grads_with_bounds(g, X, Ws, bs, labels, orders):
     return loss, dWs, dbs, bWs, bbs
 
 
+_CTX = {}   # (g, X, y, orders) of the current config, inherited by forked workers
+
+
+def _job(kind, Ws, bs):
+    g, X, y, orders = _CTX["g"], _CTX["X"], _CTX["y"], _CTX["orders"]
+    if kind == "exact":
+        return exact_grads(g, X, Ws, bs, y)
+    return tf32_grads_with_bounds(g, X, Ws, bs, y, orders)
+
+
+def _in_child(kind, Ws, bs):
+    """Run one gradient evaluation in a forked process: each returns only small arrays, and the
+    ~45 GB of FP64 activations of a products-sized evaluation are returned to the OS with the
+    child instead of fragmenting this process's heap (the host has 62 GB)."""
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(1) as pool:
+        return pool.apply(_job, (kind, Ws, bs))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
@@ -110,13 +129,14 @@ def main():
 
         orders = layer_orders(dims)
         out["orders"] = np.array(orders)
+        _CTX.update(g=g, X=X, y=y, orders=orders)
 
         # epoch-1 gradients at θ_0: exact, and TF32-operand with bounds
         Ws, bs = oracle.xavier_init(dims, 42)
-        loss1, dWs, dbs = exact_grads(g, X, Ws, bs, y)
+        loss1, dWs, dbs = _in_child("exact", Ws, bs)
         for l in range(L):
             out[f"g1_dW{l + 1}"], out[f"g1_db{l + 1}"] = dWs[l], dbs[l]
-        lt1, dWs, dbs, bWs, bbs = tf32_grads_with_bounds(g, X, Ws, bs, y, orders)
+        lt1, dWs, dbs, bWs, bbs = _in_child("tf32", Ws, bs)
         for l in range(L):
             out[f"g1t_dW{l + 1}"], out[f"g1t_db{l + 1}"] = dWs[l], dbs[l]
             out[f"g1t_bW{l + 1}"], out[f"g1t_bb{l + 1}"] = bWs[l], bbs[l]
@@ -145,12 +165,12 @@ def main():
         for t, th in snaps.items():
             Wt = [a.astype(np.float64) for a in th[:L]]
             bt = [b.astype(np.float64) for b in th[L:]]
-            lt, dW, db = exact_grads(g, X, Wt, bt, y)
+            lt, dW, db = _in_child("exact", Wt, bt)
             out[f"tf{t}_loss"] = np.array(lt)
             for l in range(L):
                 out[f"tf{t}_W{l + 1}"], out[f"tf{t}_b{l + 1}"] = th[l], th[L + l]
                 out[f"tf{t}_dW{l + 1}"], out[f"tf{t}_db{l + 1}"] = dW[l], db[l]
-            lr, dW, db, bW, bb = tf32_grads_with_bounds(g, X, Wt, bt, y, orders)
+            lr, dW, db, bW, bb = _in_child("tf32", Wt, bt)
             out[f"tf{t}t_loss"] = np.array(lr)
             for l in range(L):
                 out[f"tf{t}t_dW{l + 1}"], out[f"tf{t}t_db{l + 1}"] = dW[l], db[l]
