@@ -89,23 +89,84 @@ def tf32_grads_with_bounds(g, X, Ws, bs, labels, orders):
     return loss, dWs, dbs, bWs, bbs
 
 
-_CTX = {}   # (g, X, y, orders) of the current config, inherited by forked workers
-
-
-def _job(kind, Ws, bs):
-    g, X, y, orders = _CTX["g"], _CTX["X"], _CTX["y"], _CTX["orders"]
+def _eval_main(argv):
+    """--eval <config> <theta.npz> <out.npz> <exact|tf32>: one gradient evaluation in a fresh
+    process (regenerates the inputs), so the ~45 GB of FP64 activations of a products-sized
+    evaluation never share a heap with the trajectory (the host has 62 GB)."""
+    name, src, dst, kind = argv
+    w = make_workload(name)
+    g = oracle.graph_build(w["src"], w["dst"], w["cfg"].num_nodes)
+    th = dict(np.load(src))
+    L = len(w["cfg"].dims) - 1
+    Ws = [th[f"W{l}"] for l in range(L)]
+    bs = [th[f"b{l}"] for l in range(L)]
     if kind == "exact":
-        return exact_grads(g, X, Ws, bs, y)
-    return tf32_grads_with_bounds(g, X, Ws, bs, y, orders)
+        loss, dW, db = exact_grads(g, w["X"], Ws, bs, w["y"])
+        bW = bb = [np.zeros(0)] * L
+    else:
+        loss, dW, db, bW, bb = tf32_grads_with_bounds(g, w["X"], Ws, bs, w["y"], layer_orders(w["cfg"].dims))
+    out = {"loss": np.array(loss)}
+    for l in range(L):
+        out[f"dW{l}"], out[f"db{l}"], out[f"bW{l}"], out[f"bb{l}"] = dW[l], db[l], bW[l], bb[l]
+    np.savez(dst, **out)
 
 
-def _in_child(kind, Ws, bs):
-    """Run one gradient evaluation in a forked process: each returns only small arrays, and the
-    ~45 GB of FP64 activations of a products-sized evaluation are returned to the OS with the
-    child instead of fragmenting this process's heap (the host has 62 GB)."""
-    import multiprocessing as mp
-    with mp.get_context("fork").Pool(1) as pool:
-        return pool.apply(_job, (kind, Ws, bs))
+def _in_child(name, kind, Ws, bs):
+    import subprocess
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        src, dst = os.path.join(d, "theta.npz"), os.path.join(d, "out.npz")
+        np.savez(src, **{f"W{l}": np.asarray(W) for l, W in enumerate(Ws)},
+                 **{f"b{l}": np.asarray(b) for l, b in enumerate(bs)})
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--eval", name, src, dst, kind], check=True)
+        r = dict(np.load(dst))
+    L = len(Ws)
+    dW = [r[f"dW{l}"] for l in range(L)]
+    db = [r[f"db{l}"] for l in range(L)]
+    if kind == "exact":
+        return float(r["loss"]), dW, db
+    return float(r["loss"]), dW, db, [r[f"bW{l}"] for l in range(L)], [r[f"bb{l}"] for l in range(L)]
+
+
+def _traj_main(argv):
+    """--traj <config> <epochs> <t1,t2,..> <out.npz>: the free-running FP64 trajectory (Listing 1
+    P:159-173) in a fresh process; writes the losses and θ_{t-1} (FP32) for each teacher-forced t."""
+    name, epochs, tfs, dst = argv[0], int(argv[1]), [int(x) for x in argv[2].split(",") if x], argv[3]
+    w = make_workload(name)
+    g = oracle.graph_build(w["src"], w["dst"], w["cfg"].num_nodes)
+    X, y, dims = w["X"], w["y"], w["cfg"].dims
+    L = len(dims) - 1
+    Ws, bs = oracle.xavier_init(dims, 42)
+    params = [np.asarray(a, np.float64).copy() for a in Ws] + [np.asarray(b, np.float64).copy() for b in bs]
+    m = [np.zeros_like(p) for p in params]
+    v = [np.zeros_like(p) for p in params]
+    out = {}
+    losses = []
+    for t in range(1, epochs + 1):
+        if t in tfs:
+            for i, p in enumerate(params):
+                out[f"s{t}_{i}"] = p.astype(np.float32)
+        Z, cache = oracle.forward(g, X, params[:L], params[L:], epoch=t)
+        loss, dZ = oracle.softmax_ce(Z, y)
+        losses.append(loss)
+        gW, gb = oracle.backward(g, cache, params[:L], dZ)
+        oracle.adam_step(params, gW + gb, m, v, t)
+        del Z, cache, dZ
+        print(f"[{name}] epoch {t} loss {loss:.9f}", flush=True)
+    out["losses"] = np.array(losses)
+    np.savez(dst, **out)
+
+
+def _traj_in_child(name, epochs, tfs, L):
+    import subprocess
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        dst = os.path.join(d, "traj.npz")
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--traj", name, str(epochs),
+                        ",".join(str(t) for t in tfs), dst], check=True)
+        r = dict(np.load(dst))
+    snaps = {t: [r[f"s{t}_{i}"] for i in range(2 * L)] for t in tfs if f"s{t}_0" in r}
+    return [float(x) for x in r["losses"]], snaps
 
 
 def main():
@@ -120,23 +181,21 @@ def main():
         w = make_workload(name)
         cfg = w["cfg"]
         digest = input_digest(w)
-        g = oracle.graph_build(w["src"], w["dst"], cfg.num_nodes)
-        X, y, dims = w["X"], w["y"], cfg.dims
+        dims = cfg.dims
         L = len(dims) - 1
-        print(f"[{name}] inputs + CSR {time.time() - t0:.1f} s", flush=True)
+        del w   # every evaluation below runs in a fresh process (_in_child / _traj_in_child)
         out = {"input_sha256": np.array(digest), "dims": np.array(dims, np.int64), "seed": np.array(42),
                "adam": np.array([0.01, 0.9, 0.999, 1e-8])}
 
         orders = layer_orders(dims)
         out["orders"] = np.array(orders)
-        _CTX.update(g=g, X=X, y=y, orders=orders)
 
         # epoch-1 gradients at θ_0: exact, and TF32-operand with bounds
         Ws, bs = oracle.xavier_init(dims, 42)
-        loss1, dWs, dbs = _in_child("exact", Ws, bs)
+        loss1, dWs, dbs = _in_child(name, "exact", Ws, bs)
         for l in range(L):
             out[f"g1_dW{l + 1}"], out[f"g1_db{l + 1}"] = dWs[l], dbs[l]
-        lt1, dWs, dbs, bWs, bbs = _in_child("tf32", Ws, bs)
+        lt1, dWs, dbs, bWs, bbs = _in_child(name, "tf32", Ws, bs)
         for l in range(L):
             out[f"g1t_dW{l + 1}"], out[f"g1t_db{l + 1}"] = dWs[l], dbs[l]
             out[f"g1t_bW{l + 1}"], out[f"g1t_bb{l + 1}"] = bWs[l], bbs[l]
@@ -144,33 +203,21 @@ def main():
         print(f"[{name}] epoch-1 gradients {time.time() - t0:.1f} s (loss1 {loss1:.9f}, tf32 {lt1:.9f})", flush=True)
 
         # free-running trajectory, keeping θ_{t-1} for the teacher-forced epochs
-        params = [np.asarray(a, np.float64).copy() for a in Ws] + [np.asarray(b, np.float64).copy() for b in bs]
-        m = [np.zeros_like(p) for p in params]
-        v = [np.zeros_like(p) for p in params]
-        losses, snaps = [], {}
-        for t in range(1, args.epochs + 1):
-            if t in tf_epochs:
-                snaps[t] = [p.astype(np.float32) for p in params]
-            Z, cache = oracle.forward(g, X, params[:L], params[L:], epoch=t)
-            loss, dZ = oracle.softmax_ce(Z, y)
-            losses.append(loss)
-            gW, gb = oracle.backward(g, cache, params[:L], dZ)
-            oracle.adam_step(params, gW + gb, m, v, t)
-            del Z, cache, dZ
-            print(f"[{name}] epoch {t} loss {loss:.9f}  ({time.time() - t0:.1f} s)", flush=True)
+        losses, snaps = _traj_in_child(name, args.epochs, tf_epochs, L)
         out["losses"] = np.array(losses)
+        print(f"[{name}] trajectory {time.time() - t0:.1f} s: " + " ".join(f"{x:.6g}" for x in losses), flush=True)
         assert abs(losses[0] - loss1) <= 1e-12 * max(1.0, abs(loss1))
 
         # teacher-forced epochs at the FP32-rounded θ_{t-1}
         for t, th in snaps.items():
             Wt = [a.astype(np.float64) for a in th[:L]]
             bt = [b.astype(np.float64) for b in th[L:]]
-            lt, dW, db = _in_child("exact", Wt, bt)
+            lt, dW, db = _in_child(name, "exact", Wt, bt)
             out[f"tf{t}_loss"] = np.array(lt)
             for l in range(L):
                 out[f"tf{t}_W{l + 1}"], out[f"tf{t}_b{l + 1}"] = th[l], th[L + l]
                 out[f"tf{t}_dW{l + 1}"], out[f"tf{t}_db{l + 1}"] = dW[l], db[l]
-            lr, dW, db, bW, bb = _in_child("tf32", Wt, bt)
+            lr, dW, db, bW, bb = _in_child(name, "tf32", Wt, bt)
             out[f"tf{t}t_loss"] = np.array(lr)
             for l in range(L):
                 out[f"tf{t}t_dW{l + 1}"], out[f"tf{t}t_db{l + 1}"] = dW[l], db[l]
@@ -183,4 +230,9 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--eval":
+        _eval_main(sys.argv[2:])
+    elif len(sys.argv) > 1 and sys.argv[1] == "--traj":
+        _traj_main(sys.argv[2:])
+    else:
+        main()
