@@ -12,30 +12,35 @@ import paper_2512_01678_b200 as P  # noqa: E402
 from synth.generate import make_workload  # noqa: E402
 
 name = sys.argv[1]
-shapes = [tuple(int(x) for x in s.split(":")) for s in sys.argv[2].split(",")]
+shapes = [(int(s.split(":")[0]), int(s.split(":")[1].rstrip("b")), s.endswith("b")) for s in sys.argv[2].split(",")]
 knobs = [(a.split("=")[0], a.split("=")[1].split(",")) for a in sys.argv[3:]]
 wl = make_workload(name)
 n = wl["cfg"].num_nodes
 g = P.Graph(wl["src"], wl["dst"], n)
 nnz = g.nnz
 del wl
-for w, ld in shapes:
+from paper_2512_01678_b200._lib import Epilogue  # noqa: E402
+for w, ld, bf in shapes:
     T = torch.randn((n, ld), device="cuda")
+    if bf:   # a bfloat16 operand (MPH_EPI_IN_BF16); pass its storage as the input pointer
+        T = T.to(torch.bfloat16)
+    epi = Epilogue(flags=512) if bf else None
     out = torch.zeros((n, ld), device="cuda")
     for rep in range(2):
         for combo in itertools.product(*[v for _, v in knobs]) if knobs else [()]:
             for (k, _), v in zip(knobs, combo):
                 os.environ[k] = v
             for _ in range(5):
-                g.spmm(T, out, w=w)
+                g.spmm(T, out, w=w, epi=epi)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(20):
-                g.spmm(T, out, w=w)
+                g.spmm(T, out, w=w, epi=epi)
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 20
             tag = " ".join(f"{k}={v}" for (k, _), v in zip(knobs, combo))
-            print(f"{name} w={w} ld={ld} {tag}: {ms:.4f} ms  {nnz * (4 + 4 * w) / ms / 1e9:.0f} GB/s no-reuse",
+            print(f"{name} w={w} ld={ld}{' bf16' if bf else ''} {tag}: {ms:.4f} ms  "
+                  f"{nnz * (4 + (2 if bf else 4) * w) / ms / 1e9:.1f} TB/s no-reuse",
                   flush=True)
     del T, out
