@@ -22,9 +22,9 @@ del wl
 from paper_2512_01678_b200._lib import Epilogue  # noqa: E402
 for w, ld, bf in shapes:
     T = torch.randn((n, ld), device="cuda")
-    if bf:   # a bfloat16 operand (MPH_EPI_IN_BF16); pass its storage as the input pointer
-        T = T.to(torch.bfloat16)
-    epi = Epilogue(flags=512) if bf else None
+    if bf:   # round-2 experiment only: a bfloat16 operand needed the (reverted) MPH_EPI_IN_BF16 flag
+        raise SystemExit("bf16 operands were a round-2 experiment (profiles/r02_experiments/spmm_bf16_operand.txt)")
+    epi = None
     out = torch.zeros((n, ld), device="cuda")
     for rep in range(2):
         for combo in itertools.product(*[v for _, v in knobs]) if knobs else [()]:
