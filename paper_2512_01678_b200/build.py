@@ -62,6 +62,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     os.makedirs(OBJDIR, exist_ok=True)
     common = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", inc, "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+    common += os.environ.get("MPH_BUILD_DEFINES", "").split()  # A/B builds of compile-time switches (tools/)
 
     def compile_one(src):
         obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")

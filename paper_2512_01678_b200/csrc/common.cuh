@@ -94,6 +94,22 @@ __device__ __forceinline__ void st_f4_hint(float4* p, float4 v, uint64_t pol) {
                "f"(v.z), "f"(v.w), "l"(pol)
                : "memory");
 }
+// The same sums with Blackwell's packed FP32 adds (FADD2: add.rn.f32x2, two lanes of a float4 per
+// instruction): round-to-nearest on each element, bit-identical to f4_add, half the instructions.
+__device__ __forceinline__ float4 f4_add2(float4 a, float4 b) {
+#ifdef MPH_NO_FADD2
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+#endif
+  float4 r;
+  asm("{\n\t.reg .b64 a0, a1, b0, b1, d0, d1;\n\t"
+      "mov.b64 a0, {%4, %5};\n\tmov.b64 a1, {%6, %7};\n\t"
+      "mov.b64 b0, {%8, %9};\n\tmov.b64 b1, {%10, %11};\n\t"
+      "add.rn.f32x2 d0, a0, b0;\n\tadd.rn.f32x2 d1, a1, b1;\n\t"
+      "mov.b64 {%0, %1}, d0;\n\tmov.b64 {%2, %3}, d1;\n\t}"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+      : "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w));
+  return r;
+}
 __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
   return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }

@@ -186,8 +186,8 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
 #pragma unroll
         for (int w = 1; w < U; w <<= 1)
 #pragma unroll
-          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add(x[uu][j], x[uu + w][j]);
-        acc[j] = f4_add(acc[j], x[0][j]);
+          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add2(x[uu][j], x[uu + w][j]);
+        acc[j] = f4_add2(acc[j], x[0][j]);
       }
     }
   }
@@ -327,8 +327,8 @@ __global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
 #pragma unroll
         for (int w = 1; w < U; w <<= 1)
 #pragma unroll
-          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add(x[uu][j], x[uu + w][j]);
-        acc[j] = f4_add(acc[j], x[0][j]);
+          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add2(x[uu][j], x[uu + w][j]);
+        acc[j] = f4_add2(acc[j], x[0][j]);
       }
       // ---- a finished row is stored by its slot
       if (row >= 0 && want) {
