@@ -373,9 +373,13 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   // operand ring cut to 2 stages.  MPH_GEMM_EPI=4 restores 4 warps (experiments).
   p.n_epi = BN >= 64 ? 8 : 4;
   if (const char* ev = getenv("MPH_GEMM_EPI")) p.n_epi = (atoi(ev) == 8 && BN >= 64) ? 8 : 4;
-  const size_t epi_bytes = (size_t)p.n_epi * kEpiBufs * kEpiChunkBytes;
+  // a mask tile streams in ahead of each chunk (3-buffer ring); without one, a chunk only needs its
+  // staging buffer and the previous chunk's, still being stored: 2 buffers, and the 32 KB saved per
+  // 8 warps buys the operand ring another stage (N = 256: 2 -> 3 stages of A + B in flight)
+  p.nbufs = (flags & MPH_EPI_MASK) ? kEpiBufs : 2;
+  const size_t epi_bytes = (size_t)p.n_epi * p.nbufs * kEpiChunkBytes;
   const size_t fixed = 1024 + epi_bytes + (size_t)BN * sizeof(float) +
-                       (size_t)(2 * 8 + 4 + p.n_epi * kEpiBufs) * 8 + 16 + 4 * (size_t)BN * sizeof(float);
+                       (size_t)(2 * 8 + 4 + p.n_epi * p.nbufs) * 8 + 16 + 4 * (size_t)BN * sizeof(float);
   constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block on sm_100
   p.stages = (int)std::max<size_t>(2, std::min<size_t>(8, (kMaxSmem - fixed) / stage_bytes));
   p.idesc = bf16 ? tc::idesc_bf16(kBM, BN, 0, 0) : tc::idesc_tf32(kBM, BN, 0, 0);

@@ -48,9 +48,13 @@ for rep in range(2):
             m.train_epoch(t)
         ev1.record()
         torch.cuda.synchronize()
-        cnt, tms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
-        L.mph_profile_read(0, C.byref(cnt), C.byref(tms), C.byref(by), C.byref(fl))
+        per = {}
+        for kind, kname in ((0, "spmm"), (1, "gemm_nt"), (2, "gemm_tn")):
+            cnt, tms, by, fl = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            L.mph_profile_read(kind, C.byref(cnt), C.byref(tms), C.byref(by), C.byref(fl))
+            per[kname] = (tms.value / 10, cnt.value // 10)
         L.mph_profile_enable(0)
         name = " ".join(f"{k}={v}" for (k, _), v in zip(knobs, combo))
-        print(f"{cfgname} {prec} {name}: epoch {ev0.elapsed_time(ev1) / 10:.3f} ms  spmm {tms.value / 10:.3f} ms "
-              f"({cnt.value // 10} launches)", flush=True)
+        print(f"{cfgname} {prec} {name}: epoch {ev0.elapsed_time(ev1) / 10:.3f} ms  spmm {per['spmm'][0]:.3f} ms "
+              f"({per['spmm'][1]} launches)  gemm_nt {per['gemm_nt'][0]:.3f}  gemm_tn {per['gemm_tn'][0]:.3f}",
+              flush=True)
