@@ -156,6 +156,12 @@ int mph_features_destroy(mph_features* f);
                                 holds bf16, ld in elements): outputs that only feed BF16 GEMMs.
                                 mph_gemm_nt and mph_spmm (whole rows, part -1) */
 #define MPH_EPI_MASK_BF16 256u /* mask_src holds bfloat16 values (ld_mask in elements); mph_gemm_nt */
+#define MPH_EPI_SIGNBITS 1024u /* also write the signs of the stored output as "sign bytes": bit t of byte
+                                  bits_out[r * ld_bits + c / 4] = (stored value at column c > 0), t = c % 4
+                                  (ld_bits in bytes).  A ReLU (+ dropout) layer's mask in 1/16 of its
+                                  FP32 bytes.  mph_gemm_nt (ld_bits % 8 == 0); mph_spmm (part -1 or 1) */
+#define MPH_EPI_MASK_BITS 2048u /* MASK with mask_src holding such sign bytes (ld_mask in bytes, % 8 == 0,
+                                   8-byte aligned): the same decisions as the value mask; mph_gemm_nt */
 
 typedef struct {
   uint32_t flags;
@@ -170,6 +176,8 @@ typedef struct {
   int32_t dropout_layer, dropout_epoch;
   int64_t row0;            /* global id of row 0 (Philox counter; distributed ranks) */
   const int32_t* dropout_epoch_d; /* nullable: device epoch counter overriding dropout_epoch (graph replay) */
+  uint32_t* bits_out;      /* [rows][ld_bits] sign bytes (SIGNBITS) */
+  int32_t ld_bits;
 } mph_epilogue;
 
 /* a3/a6 — aggregation SpMM (Alg. 3, fused per P:361/P:735):
@@ -179,6 +187,9 @@ typedef struct {
  * Deterministic, atomic-free; no O(|E|·F) buffer.  `in` has n_cols rows. */
 int mph_spmm(const mph_graph* g, const float* in_d, int32_t w, int32_t ld_in, float* out_d, int32_t ld_out,
              const mph_epilogue* epi, void* stream);
+/* *ok_h = 1 if mph_spmm of width w on g can write MPH_EPI_SIGNBITS (any width that is a multiple of
+ * 4, <= 512), else 0.  Host only, no device work.  MPH_EINVAL on null arguments. */
+int mph_spmm_signbits_ok(const mph_graph* g, int32_t w, int32_t* ok_h);
 /* Same, restricted to one part of each row of a localized graph: part 0 = owned columns,
  * part 1 = ghost columns accumulated onto out (which must hold part 0's raw sums);
  * the epilogue runs with part 1 only.  part -1 = whole row (== mph_spmm). */

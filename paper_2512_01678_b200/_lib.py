@@ -19,7 +19,7 @@ STATUS = {0: "MPH_OK", -1: "MPH_EINVAL", -2: "MPH_ERANGE", -3: "MPH_EDEGENERATE"
           -10: "MPH_ETIMEOUT"}
 
 EPI_BIAS, EPI_RELU, EPI_ROWSCALE, EPI_MASK, EPI_DROPOUT, EPI_COLSUM, EPI_TF32 = 1, 2, 4, 8, 16, 32, 64
-EPI_BF16, EPI_MASK_BF16 = 128, 256
+EPI_BF16, EPI_MASK_BF16, EPI_SIGNBITS, EPI_MASK_BITS = 128, 256, 1024, 2048
 AGG = {"gcn": 0, "sum": 1, "mean": 2, "max": 3}            # MPH_AGG_*
 TAU_PAPER_BP, TAU_B200_BP = 8000, 9500                     # MPH_TAU_PAPER_BP, MPH_TAU_B200_BP
 OPT = {"adam": 0, "sgd": 1, "adamw": 2}                    # MPH_OPT_*
@@ -36,7 +36,8 @@ class Epilogue(C.Structure):
     _fields_ = [("flags", C.c_uint32), ("row_scale", C.c_void_p), ("bias", C.c_void_p), ("mask_src", C.c_void_p),
                 ("ld_mask", C.c_int32), ("mask_scale", C.c_float), ("colsum_out", C.c_void_p),
                 ("dropout_p", C.c_float), ("dropout_seed", C.c_uint64), ("dropout_layer", C.c_int32),
-                ("dropout_epoch", C.c_int32), ("row0", C.c_int64), ("dropout_epoch_d", C.c_void_p)]
+                ("dropout_epoch", C.c_int32), ("row0", C.c_int64), ("dropout_epoch_d", C.c_void_p),
+                ("bits_out", C.c_void_p), ("ld_bits", C.c_int32)]
 
 
 class AdamCfg(C.Structure):
@@ -81,6 +82,7 @@ _SIGS = {
     "mph_features_dense": [P, PP, C.POINTER(i32)],
     "mph_features_destroy": [P],
     "mph_spmm": [P, P, i32, i32, P, i32, C.POINTER(Epilogue), P],
+    "mph_spmm_signbits_ok": [P, i32, C.POINTER(i32)],
     "mph_spmm_part": [P, i32, P, i32, i32, P, i32, C.POINTER(Epilogue), P],
     "mph_graph_agg_scales": [P, i32, i32, PP, PP],
     "mph_aggregate": [P, i32, i32, P, i32, i32, P, i32, C.POINTER(Epilogue), P],

@@ -35,6 +35,11 @@ struct Layer {
   float* colsum = nullptr;
   int32_t* arg = nullptr;  // max aggregation: argmax of Y (layers > 1)
   float* dY = nullptr;     // max aggregation: dZ·Wᵀ, the gradient routed back through arg
+  // hidden layers: the signs of out (= the ReLU + dropout mask of the backward dH GEMM) as sign
+  // bytes, written by the producing SpMM / GEMM epilogue (MPH_EPI_SIGNBITS): the dH GEMM reads
+  // 1/16 of out's bytes for the same decisions (MPH_EPI_MASK_BITS)
+  uint8_t* sb = nullptr;
+  int ld_sb = 0;
 };
 
 }  // namespace
@@ -104,6 +109,7 @@ static void gcn_free(mph_gcn* m) {
   for (auto& l : m->layers) {
     if (!in_arena(m, l.T)) dev_free(l.T);
     dev_free(l.out);
+    dev_free(l.sb);
     if (!in_arena(m, l.dZ)) dev_free(l.dZ);
     dev_free(l.G);
     dev_free(l.Y);
@@ -256,7 +262,10 @@ static int gemm_nt_p(int M, int N, int K, const float* A, int lda, const float* 
                      const mph_epilogue* e, cudaStream_t s, int colsum_fill = 1, bool bf16 = false) {
   const uint32_t f = e ? e->flags : 0u;
   const double in_b = bf16 ? 2.0 : 4.0, out_b = (f & MPH_EPI_BF16) ? 2.0 : 4.0;
-  const double extra = (f & MPH_EPI_MASK) ? ((f & MPH_EPI_MASK_BF16) ? 2.0 : 4.0) * M * N : 0.0;
+  // mask read (4 B / 2 B per element, a sign byte per 4 with MASK_BITS) + sign bytes written
+  const double extra = ((f & MPH_EPI_MASK) ? ((f & MPH_EPI_MASK_BITS) ? 0.25 : (f & MPH_EPI_MASK_BF16) ? 2.0 : 4.0)
+                                           : 0.0) * M * N +
+                       ((f & MPH_EPI_SIGNBITS) ? 0.25 * M * N : 0.0);
   prof::Scope sc(MPH_PROF_GEMM_NT, s, in_b * ((double)M * K + (double)N * K) + out_b * M * N + extra,
                  2.0 * M * N * K);
   return gemm_nt_launch_ex(M, N, K, A, lda, Bt, ldb, C, ldc, e, s, colsum_fill, bf16);
@@ -306,6 +315,11 @@ static int layer_forward(mph_gcn* m, int li, cudaStream_t s) {
   // hidden outputs only feed tensor-core GEMMs (and the ReLU-mask sign test): store them as TF32
   eo.flags = MPH_EPI_BIAS | (hidden ? (MPH_EPI_RELU | gemm_operand_flag(m)) : 0u);
   eo.bias = m->params + l.off_b;
+  if (hidden && l.sb) {
+    eo.flags |= MPH_EPI_SIGNBITS;
+    eo.bits_out = reinterpret_cast<uint32_t*>(l.sb);
+    eo.ld_bits = l.ld_sb;
+  }
   if (hidden && m->dropout_p > 0.0f) {
     eo.flags |= MPH_EPI_DROPOUT;
     eo.dropout_p = m->dropout_p;
@@ -446,10 +460,11 @@ static int do_backward(mph_gcn* m, cudaStream_t s) {
       Layer& pl = m->layers[li - 1];
       mph_epilogue ed = epi_none();
       // TF: dZ' feeds the FP32 SpMM (keep FP32); AF: dZ_1 feeds only the dW GEMM (TF32)
-      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM | (m->bf16 ? MPH_EPI_MASK_BF16 : 0u) |
+      ed.flags = MPH_EPI_MASK | MPH_EPI_COLSUM |
+                 (pl.sb ? MPH_EPI_MASK_BITS : (m->bf16 ? MPH_EPI_MASK_BF16 : 0u)) |
                  (pl.order == 0 ? (m->bpre ? MPH_EPI_ROWSCALE : 0u) : gemm_operand_flag(m));
-      ed.mask_src = pl.out;
-      ed.ld_mask = pl.pout;
+      ed.mask_src = pl.sb ? reinterpret_cast<const float*>(pl.sb) : pl.out;
+      ed.ld_mask = pl.sb ? pl.ld_sb : pl.pout;
       ed.mask_scale = dropout_scale(m->dropout_p);
       ed.colsum_out = pl.colsum;
       ed.row_scale = m->bpre;
@@ -598,6 +613,12 @@ extern "C" int mph_gcn_create(const mph_graph* g, const mph_features* f, const m
     else if ((rc = dev_alloc(&l.dZ, (size_t)(l.order == 0 ? nc : nr) * l.pout)))
       return bail(rc);
     if ((rc = dev_alloc(&l.colsum, (size_t)ceil_div(nr, 128) * l.pout))) return bail(rc);
+#ifndef MPH_NO_SIGNBYTES
+    if (!max_agg && li + 1 < m->L) {
+      l.ld_sb = (int)round_up((int)ceil_div(l.pout, 4), 8);
+      if ((rc = dev_alloc(&l.sb, (size_t)nr * l.ld_sb))) return bail(rc);
+    }
+#endif
     if (max_agg) {
       if ((rc = dev_alloc(&l.Y, (size_t)nr * l.pin))) return bail(rc);
       if (li > 0 && ((rc = dev_alloc(&l.arg, (size_t)nr * l.pin)) || (rc = dev_alloc(&l.dY, (size_t)nr * l.pin))))

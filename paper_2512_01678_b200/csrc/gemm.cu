@@ -36,8 +36,10 @@ struct EpiG {
   uint32_t flags;
   const float* row_scale;
   const float* bias;
-  const float* mask_src;
+  const float* mask_src;  // MASK_BITS: uint32 sign-bit words
   int ld_mask;
+  uint32_t* bits_out;     // SIGNBITS
+  int ld_bits;
   float mask_scale;
   float* colsum_out;
   Dropout drop;
@@ -350,10 +352,17 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   const uint32_t flags = epi ? epi->flags : 0u;
   if ((flags & MPH_EPI_BIAS) && !epi->bias) return fail(MPH_EINVAL, "gemm_nt: null bias");
   if ((flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "gemm_nt: null row_scale");
-  if ((flags & MPH_EPI_MASK) && (!epi->mask_src || epi->ld_mask % 4 || epi->ld_mask < N ||
+  if ((flags & MPH_EPI_MASK) && !(flags & MPH_EPI_MASK_BITS) && (!epi->mask_src || epi->ld_mask % 4 || epi->ld_mask < N ||
                                  (reinterpret_cast<uintptr_t>(epi->mask_src) & 15)))
     return fail(MPH_EINVAL, "gemm_nt: mask_src must be 16-byte aligned with ld_mask %% 4 == 0, >= N");
   if ((flags & MPH_EPI_COLSUM) && !epi->colsum_out) return fail(MPH_EINVAL, "gemm_nt: null colsum_out");
+  if ((flags & MPH_EPI_MASK_BITS) && (!(flags & MPH_EPI_MASK) || (flags & MPH_EPI_MASK_BF16) ||
+                                      epi->ld_mask < (N + 3) / 4 || epi->ld_mask % 8 ||
+                                      (reinterpret_cast<uintptr_t>(epi->mask_src) & 7)))
+    return fail(MPH_EINVAL, "gemm_nt: MASK_BITS needs MASK, 8-byte aligned sign bytes, ld_mask %% 8 == 0 and >= ceil(N/4)");
+  if ((flags & MPH_EPI_SIGNBITS) && (!epi->bits_out || epi->ld_bits < (N + 3) / 4 || epi->ld_bits % 8 ||
+                                     (reinterpret_cast<uintptr_t>(epi->bits_out) & 7)))
+    return fail(MPH_EINVAL, "gemm_nt: SIGNBITS needs 8-byte aligned bits_out, ld_bits %% 8 == 0 and >= ceil(N/4)");
   if (M == 0) return MPH_OK;
   const int sms = sm_count();
   const int BN = round_up(N, 32);
@@ -376,7 +385,7 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   // a mask tile streams in ahead of each chunk (3-buffer ring); without one, a chunk only needs its
   // staging buffer and the previous chunk's, still being stored: 2 buffers, and the 32 KB saved per
   // 8 warps buys the operand ring another stage (N = 256: 2 -> 3 stages of A + B in flight)
-  p.nbufs = (flags & MPH_EPI_MASK) ? kEpiBufs : 2;
+  p.nbufs = ((flags & MPH_EPI_MASK) && !(flags & MPH_EPI_MASK_BITS)) ? kEpiBufs : 2;
   const size_t epi_bytes = (size_t)p.n_epi * p.nbufs * kEpiChunkBytes;
   const size_t fixed = 1024 + epi_bytes + (size_t)BN * sizeof(float) +
                        (size_t)(2 * 8 + 4 + p.n_epi * p.nbufs) * 8 + 16 + 4 * (size_t)BN * sizeof(float);
@@ -389,6 +398,8 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   p.epi.bias = epi ? epi->bias : nullptr;
   p.epi.mask_src = epi ? epi->mask_src : nullptr;
   p.epi.ld_mask = epi ? epi->ld_mask : 0;
+  p.epi.bits_out = (epi && (flags & MPH_EPI_SIGNBITS)) ? epi->bits_out : nullptr;
+  p.epi.ld_bits = epi ? epi->ld_bits : 0;
   p.epi.mask_scale = epi ? epi->mask_scale : 1.0f;
   p.epi.colsum_out = epi ? epi->colsum_out : nullptr;
   p.epi.drop = make_dropout(epi);
@@ -401,27 +412,27 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   const bool out_bf = (flags & MPH_EPI_BF16) != 0, mask_bf = (flags & MPH_EPI_MASK_BF16) != 0;
   // BF16 output in 64-column units (full 128-byte smem rows, half the TMA stores), when the width
   // allows and a mask, if any, is BF16 too
-  p.wide = (out_bf && BN % 64 == 0 && (!(flags & MPH_EPI_MASK) || mask_bf)) ? 1 : 0;
+  p.wide = (out_bf && BN % 64 == 0 && (!(flags & MPH_EPI_MASK) || mask_bf || (flags & MPH_EPI_MASK_BITS))) ? 1 : 0;
   const uint32_t cw = p.wide ? 64 : 32;
   MPH_TRY(make_tmap(&tcm, C, (uint64_t)N, (uint64_t)M, (uint64_t)ldc, cw, 32,
                     (out_bf && !p.wide) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, out_bf));
-  if (flags & MPH_EPI_MASK)
+  if ((flags & MPH_EPI_MASK) && !(flags & MPH_EPI_MASK_BITS))
     MPH_TRY(make_tmap(&tm, epi->mask_src, (uint64_t)N, (uint64_t)M, (uint64_t)epi->ld_mask, cw, 32,
                       (mask_bf && !p.wide) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, mask_bf));
   else
     tm = tcm;
   const size_t smem = fixed + (size_t)p.stages * stage_bytes;
-  static size_t configured[2] = {0, 0};
-  if (smem > configured[bf16]) {
-    MPH_CUDA_TRY(cudaFuncSetAttribute(bf16 ? k_gemm_nt<true> : k_gemm_nt<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[bf16] = smem;
+  const bool sb = (flags & (MPH_EPI_SIGNBITS | MPH_EPI_MASK_BITS)) != 0;
+  auto kern = bf16 ? (sb ? k_gemm_nt<true, true> : k_gemm_nt<true, false>)
+                   : (sb ? k_gemm_nt<false, true> : k_gemm_nt<false, false>);
+  static size_t configured[4] = {0, 0, 0, 0};
+  const int ki = (bf16 ? 2 : 0) + (sb ? 1 : 0);
+  if (smem > configured[ki]) {
+    MPH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured[ki] = smem;
   }
   const int grid = std::min(p.n_tiles, sms);
-  if (bf16)
-    k_gemm_nt<true><<<grid, 64 + 32 * p.n_epi, smem, s>>>(ta, tb, tcm, tm, p);
-  else
-    k_gemm_nt<false><<<grid, 64 + 32 * p.n_epi, smem, s>>>(ta, tb, tcm, tm, p);
+  kern<<<grid, 64 + 32 * p.n_epi, smem, s>>>(ta, tb, tcm, tm, p);
   count_launch();
   return launch_check("gemm_nt");
 }

@@ -139,6 +139,8 @@ int launch_dinv(const int32_t* deg, float* dinv, float* dinv1, int64_t n, cudaSt
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
                 const mph_epilogue* epi, const float* post, cudaStream_t s, const float* partial = nullptr);
 int ensure_graph_items(const mph_graph* g, cudaStream_t s);
+// MPH_EPI_SIGNBITS is available for whole-row aggregations of width w on g
+bool spmm_signbits_ok(const mph_graph* g, int w);
 // aggregate.cu (NEXT-4): scheme scales, max aggregation and its adjoint, chunked column sums
 int agg_scales(const mph_graph* g, int scheme, int transpose, const float** pre, const float** post);
 int aggregate_max_launch(const mph_graph* g, const float* in, int w, int ld_in, float* out, int ld_out, int32_t* arg,

@@ -52,6 +52,8 @@ struct SpmmArgs {
   int row_slots;   // 1: narrow rows of a low-degree graph -> k_spmm_rows
   int mid_degree;  // 1: mean degree in [16, 64) (dispatch of 48-wide rows)
   const float* partial;  // part 1 with a BF16 output: part 0's FP32 sums (row stride nv4·4), else nullptr
+  uint32_t* bits_out;    // SIGNBITS: sign nibbles, one byte per float4 column, [rows][ld_bits] bytes
+  int ld_bits;
   EpiDev epi;
 };
 
@@ -70,7 +72,7 @@ __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int6
 // ReLU, dropout, row scale, TF32 (Q1, Q6, Q8, Q10).
 constexpr int64_t kRowSlotMaxDegree = 16;  // mean degree (incl. self loop) below which k_spmm_rows serves w <= 64 (arxiv -7 %; products at 26 is 5 % slower with it)
 
-template <int LPR, int VPL>
+template <int LPR, int VPL, bool SGN = false>
 __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, const float4 (&acc)[VPL], float du,
                                           float rs, uint64_t pol) {
   float4* orow = reinterpret_cast<float4*>(a.out + (int64_t)row * a.ld_out);
@@ -81,40 +83,53 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, c
     return;
   }
   const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
+  constexpr bool sign_out = SGN;
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
     const int c4 = sub + j * LPR;
     if (c4 >= a.nv4) continue;
-    float4 v = acc[j];
-    if (a.part == 1)
-      v = f4_add(v, a.partial ? reinterpret_cast<const float4*>(a.partial + (int64_t)row * a.nv4 * 4)[c4] : orow[c4]);
-    v.x *= du;
-    v.y *= du;
-    v.z *= du;
-    v.w *= du;
-    if (a.epi.flags & MPH_EPI_BIAS) {
-      float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
-      v = f4_add(v, b);
+    uint32_t nib = 0u;  // SIGNBITS: stored value > 0, 4 bits per float4
+    if (c4 < a.nv4) {
+      float4 v = acc[j];
+      if (a.part == 1)
+        v = f4_add(v, a.partial ? reinterpret_cast<const float4*>(a.partial + (int64_t)row * a.nv4 * 4)[c4] : orow[c4]);
+      v.x *= du;
+      v.y *= du;
+      v.z *= du;
+      v.w *= du;
+      if (a.epi.flags & MPH_EPI_BIAS) {
+        float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
+        v = f4_add(v, b);
+      }
+      if (a.epi.flags & MPH_EPI_RELU) {
+        v.x = fmaxf(v.x, 0.0f);
+        v.y = fmaxf(v.y, 0.0f);
+        v.z = fmaxf(v.z, 0.0f);
+        v.w = fmaxf(v.w, 0.0f);
+      }
+      if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, a.epi.c4_0 + c4);
+      if (a.epi.flags & MPH_EPI_ROWSCALE) {
+        v.x *= rs;
+        v.y *= rs;
+        v.z *= rs;
+        v.w *= rs;
+      }
+      if (a.epi.flags & MPH_EPI_BF16) {  // BF16 row (only feeds BF16 GEMMs); out/ld_out in bf16 elements
+        uint2* o16 = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + (int64_t)row * a.ld_out);
+        const uint2 q = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+        o16[c4] = q;
+        if (sign_out)
+          nib = (uint32_t)bf16_positive(q.x & 0xFFFFu) | ((uint32_t)bf16_positive(q.x >> 16) << 1) |
+                ((uint32_t)bf16_positive(q.y & 0xFFFFu) << 2) | ((uint32_t)bf16_positive(q.y >> 16) << 3);
+      } else {
+        const float4 st = to_tf32 ? f4_tf32(v) : v;
+        st_f4_hint(orow + c4, st, pol);
+        nib = (uint32_t)(st.x > 0.0f) | ((uint32_t)(st.y > 0.0f) << 1) | ((uint32_t)(st.z > 0.0f) << 2) |
+              ((uint32_t)(st.w > 0.0f) << 3);
+      }
     }
-    if (a.epi.flags & MPH_EPI_RELU) {
-      v.x = fmaxf(v.x, 0.0f);
-      v.y = fmaxf(v.y, 0.0f);
-      v.z = fmaxf(v.z, 0.0f);
-      v.w = fmaxf(v.w, 0.0f);
-    }
-    if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, a.epi.c4_0 + c4);
-    if (a.epi.flags & MPH_EPI_ROWSCALE) {
-      v.x *= rs;
-      v.y *= rs;
-      v.z *= rs;
-      v.w *= rs;
-    }
-    if (a.epi.flags & MPH_EPI_BF16) {  // BF16 row (only feeds BF16 GEMMs); out/ld_out in bf16 elements
-      uint2* o16 = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + (int64_t)row * a.ld_out);
-      o16[c4] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
-    } else {
-      st_f4_hint(orow + c4, to_tf32 ? f4_tf32(v) : v, pol);
-    }
+    if (sign_out && c4 < a.nv4)  // one byte per float4: its 4 sign bits (MPH_EPI_SIGNBITS layout)
+      reinterpret_cast<uint8_t*>(a.bits_out)[(int64_t)row * a.ld_bits + a.epi.c4_0 + c4] = (uint8_t)nib;
   }
 }
 
@@ -127,7 +142,7 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, c
 // edges keep the plain single-block sum.  Alg. 3 P:373-384 (the per-row sum), P:357 (skew).
 constexpr int64_t kHubBlock = 256;
 
-template <int LPR, int VPL, bool HAS_VAL, int UOV>
+template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false, bool PK = true>
 __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   constexpr int ES = 32 / LPR;
   // U gathers per slot in flight; U*VPL float4 loads per lane before the first use
@@ -186,8 +201,8 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
 #pragma unroll
         for (int w = 1; w < U; w <<= 1)
 #pragma unroll
-          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add2(x[uu][j], x[uu + w][j]);
-        acc[j] = f4_add2(acc[j], x[0][j]);
+          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = PK ? f4_add2(x[uu][j], x[uu + w][j]) : f4_add(x[uu][j], x[uu + w][j]);
+        acc[j] = PK ? f4_add2(acc[j], x[0][j]) : f4_add(acc[j], x[0][j]);
       }
     }
   }
@@ -207,12 +222,12 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
   if (slot != 0) return;
   const float du = (a.part != 0 && a.dinv) ? a.dinv[row] : 1.0f;
   const float rs = (a.part != 0 && (a.epi.flags & MPH_EPI_ROWSCALE)) ? a.epi.row_scale[row] : 1.0f;
-  store_row<LPR, VPL>(a, row, sub, acc, du, rs, pol);
+  store_row<LPR, VPL, SGN>(a, row, sub, acc, du, rs, pol);
 }
 
 // 4 blocks (32 warps) per SM within the 64-register budget for the one-float4-per-lane shapes
 // (the hub-block partials would otherwise cost a block per SM); 3 for the wider register tiles
-template <int LPR, int VPL, bool HAS_VAL, int UOV>
+template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false>
 __global__ void __launch_bounds__(256, ((VPL == 1 || LPR == 4) ? 4 : 3)) k_spmm(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   while (true) {
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(256, ((VPL == 1 || LPR == 4) ? 4 : 3)) k_spmm(
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
-    for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL, HAS_VAL, UOV>(a, row, lane);
+    for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL, HAS_VAL, UOV, SGN>(a, row, lane);
   }
 }
 
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(256, ((VPL == 1 || LPR == 4) ? 4 : 3)) k_spmm(
 // its next step gathers immediately.  Per step a slot gathers U neighbours (U·VPL independent
 // 16-byte loads per lane) whose ids were loaded one step earlier.  Every row is summed by one
 // slot in edge order (pairwise tree per group of U): deterministic whatever the claim order.
-template <int LPR, int VPL, int U>
+template <int LPR, int VPL, int U, bool SGN = false>
 __global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
   constexpr int ES = 32 / LPR;
   constexpr int NID = (U + LPR - 1) / LPR;  // id registers per lane
@@ -251,7 +266,7 @@ __global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
     if (rr.y - rr.x == 1) {  // a long row (> E edges) is an item of its own: all slots on it
-      spmm_row<LPR, VPL, false, 0>(a, rr.x, lane);
+      spmm_row<LPR, VPL, false, 0, SGN, false>(a, rr.x, lane);  // scalar adds: packed ones spill here
       continue;
     }
     int w0 = rr.x;  // row bounds window: lane i holds [ws, we) of row w0 + i
@@ -327,12 +342,12 @@ __global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
 #pragma unroll
         for (int w = 1; w < U; w <<= 1)
 #pragma unroll
-          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add2(x[uu][j], x[uu + w][j]);
-        acc[j] = f4_add2(acc[j], x[0][j]);
+          for (int uu = 0; uu + w < U; uu += 2 * w) x[uu][j] = f4_add(x[uu][j], x[uu + w][j]);
+        acc[j] = f4_add(acc[j], x[0][j]);
       }
       // ---- a finished row is stored by its slot
       if (row >= 0 && want) {
-        store_row<LPR, VPL>(a, row, sub, acc, du, rs, pol);
+        store_row<LPR, VPL, SGN>(a, row, sub, acc, du, rs, pol);
 #pragma unroll
         for (int j = 0; j < VPL; ++j) acc[j] = f4_zero();
       }
@@ -439,12 +454,12 @@ int ensure_graph_items(const mph_graph* gc, cudaStream_t s) {
   return MPH_OK;
 }
 
-template <int LPR, int VPL, bool HAS_VAL, int UOV = 0>
+template <int LPR, int VPL, bool HAS_VAL, int UOV = 0, bool SGN = false>
 static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
   static int blocks_per_sm = 0;
   static int sms = 0;
   if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<LPR, VPL, HAS_VAL, UOV>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<LPR, VPL, HAS_VAL, UOV, SGN>, 256, 0);
     blocks_per_sm = std::max(1, blocks_per_sm);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -452,18 +467,18 @@ static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
   }
   const int64_t grid = std::min<int64_t>((int64_t)sms * blocks_per_sm, ceil_div(a.n_items, 8));
   MPH_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
-  k_spmm<LPR, VPL, HAS_VAL, UOV><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
+  k_spmm<LPR, VPL, HAS_VAL, UOV, SGN><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
   count_launch();
   return launch_check("spmm");
 }
 
 
-template <int LPR, int VPL, int U>
+template <int LPR, int VPL, int U, bool SGN = false>
 static int launch_spmm_rows(const SpmmArgs& a, cudaStream_t s) {
   static int blocks_per_sm = 0;
   static int sms = 0;
   if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm_rows<LPR, VPL, U>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm_rows<LPR, VPL, U, SGN>, 256, 0);
     blocks_per_sm = std::max(1, blocks_per_sm);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -471,7 +486,7 @@ static int launch_spmm_rows(const SpmmArgs& a, cudaStream_t s) {
   }
   const int64_t grid = std::min<int64_t>((int64_t)sms * blocks_per_sm, ceil_div(a.n_items, 8));
   MPH_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
-  k_spmm_rows<LPR, VPL, U><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
+  k_spmm_rows<LPR, VPL, U, SGN><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
   count_launch();
   return launch_check("spmm (row slots)");
 }
@@ -484,40 +499,46 @@ static int env_int(const char* name) {
 // Per-shape unroll: 256-wide rows (32 lanes x 2 float4) gain from 8 gathers in flight per slot
 // (measured with the round-1 unroll sweep, arxiv SpMM -8 %); every other shape is best at the
 // default U.
-template <int LPR, int VPL, bool HAS_VAL>
+template <int LPR, int VPL, bool HAS_VAL, bool SGN = false>
 static int launch_spmm_u(const SpmmArgs& a, cudaStream_t s) {
-  if constexpr (LPR == 32 && VPL == 2) return launch_spmm<LPR, VPL, HAS_VAL, 8>(a, s);
-  else return launch_spmm<LPR, VPL, HAS_VAL>(a, s);
+  if constexpr (LPR == 32 && VPL == 2) return launch_spmm<LPR, VPL, HAS_VAL, 8, SGN>(a, s);
+  else return launch_spmm<LPR, VPL, HAS_VAL, 0, SGN>(a, s);
 }
 
-template <bool HAS_VAL>
+template <bool HAS_VAL, bool SGN = false>
 static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
   const int nv4 = a.nv4;
-  if (!HAS_VAL && a.row_slots && nv4 <= 16) {  // narrow rows, low degree: several rows per warp
-    if (nv4 <= 1) return launch_spmm_rows<1, 1, 4>(a, s);
-    if (nv4 <= 2) return launch_spmm_rows<2, 1, 4>(a, s);
-    if (nv4 <= 4) return launch_spmm_rows<4, 1, 4>(a, s);
-    if (nv4 <= 8) return launch_spmm_rows<8, 1, 8>(a, s);
-    if (nv4 <= 12) return launch_spmm_rows<4, 3, 4>(a, s);
-    return launch_spmm_rows<16, 1, 8>(a, s);
+  if constexpr (!HAS_VAL && !SGN) {
+    if (a.bits_out) return dispatch_spmm<false, true>(a, s);  // SIGNBITS: same maps, sign-byte store
   }
-  if (nv4 <= 1) return launch_spmm<1, 1, HAS_VAL>(a, s);
-  if (nv4 <= 2) return launch_spmm<2, 1, HAS_VAL>(a, s);
-  if (nv4 <= 4) return launch_spmm<4, 1, HAS_VAL>(a, s);
-  if (nv4 <= 8) return launch_spmm<8, 1, HAS_VAL>(a, s);
+  if (!HAS_VAL && a.row_slots && nv4 <= 16) {  // narrow rows, low degree: several rows per warp
+    if (nv4 <= 1) return launch_spmm_rows<1, 1, 4, SGN>(a, s);
+    if (nv4 <= 2) return launch_spmm_rows<2, 1, 4, SGN>(a, s);
+    if (nv4 <= 4) return launch_spmm_rows<4, 1, 4, SGN>(a, s);
+    if (nv4 <= 8) return launch_spmm_rows<8, 1, 8, SGN>(a, s);
+    if (nv4 <= 12) return launch_spmm_rows<4, 3, 4, SGN>(a, s);
+    return launch_spmm_rows<16, 1, 8, SGN>(a, s);
+  }
+  if (nv4 <= 1) return launch_spmm<1, 1, HAS_VAL, 0, SGN>(a, s);
+  if (nv4 <= 2) return launch_spmm<2, 1, HAS_VAL, 0, SGN>(a, s);
+  if (nv4 <= 4) return launch_spmm<4, 1, HAS_VAL, 0, SGN>(a, s);
+  if (nv4 <= 8) return launch_spmm<8, 1, HAS_VAL, 0, SGN>(a, s);
   if (nv4 <= 12) {
     // 48-wide rows: 4 lanes x 3 float4 (8 edge slots) where rows are long (reddit: the shuffle
     // reduction is amortised), 16 lanes x 1 float4 with 12 active (2 slots, a third of the
     // cross-slot reduction) at moderate degree (products, mean 26: -1.7 % epoch)
-    if (a.mid_degree) return launch_spmm_u<16, 1, HAS_VAL>(a, s);
-    return launch_spmm_u<4, 3, HAS_VAL>(a, s);
+    if (a.mid_degree) return launch_spmm_u<16, 1, HAS_VAL, SGN>(a, s);
+    return launch_spmm_u<4, 3, HAS_VAL, SGN>(a, s);
   }
-  if (nv4 <= 16) return launch_spmm_u<16, 1, HAS_VAL>(a, s);
-  if (nv4 <= 32) return launch_spmm_u<32, 1, HAS_VAL>(a, s);
-  if (nv4 <= 64) return launch_spmm_u<32, 2, HAS_VAL>(a, s);
-  if (nv4 <= 96) return launch_spmm<32, 3, HAS_VAL>(a, s);
-  return launch_spmm<32, 4, HAS_VAL>(a, s);
+  if (nv4 <= 16) return launch_spmm_u<16, 1, HAS_VAL, SGN>(a, s);
+  if (nv4 <= 32) return launch_spmm_u<32, 1, HAS_VAL, SGN>(a, s);
+  if (nv4 <= 64) return launch_spmm_u<32, 2, HAS_VAL, SGN>(a, s);
+  if (nv4 <= 96) return launch_spmm<32, 3, HAS_VAL, 0, SGN>(a, s);
+  return launch_spmm<32, 4, HAS_VAL, 0, SGN>(a, s);
 }
+
+// MPH_EPI_SIGNBITS on mph_spmm: every lane map stores one sign byte per float4 column it owns.
+bool spmm_signbits_ok(const mph_graph* g, int w) { return g && w > 0 && w % 4 == 0 && w <= 512; }
 
 int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in, float* out, int ld_out,
                 const mph_epilogue* epi, const float* post, cudaStream_t s, const float* partial) {
@@ -528,17 +549,23 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   if ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15)
     return fail(MPH_EINVAL, "spmm: operands must be 16-byte aligned");
   if (part != -1 && !g->local) return fail(MPH_EINVAL, "spmm: row parts need a localized graph");
-  const uint32_t allowed =
-      MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE | MPH_EPI_TF32 | MPH_EPI_BF16;
+  const uint32_t allowed = MPH_EPI_BIAS | MPH_EPI_RELU | MPH_EPI_DROPOUT | MPH_EPI_ROWSCALE | MPH_EPI_TF32 |
+                           MPH_EPI_BF16 | MPH_EPI_SIGNBITS;
   if (epi && (epi->flags & ~allowed)) return fail(MPH_EINVAL, "spmm: unsupported epilogue flags 0x%x", epi->flags);
   if (epi && (epi->flags & MPH_EPI_BF16) && part != -1 && !(part == 1 && partial))
     return fail(MPH_ENOTSUP, "spmm: BF16 output needs whole rows (part -1), or part 1 over FP32 partial sums");
   if (epi && (epi->flags & MPH_EPI_BIAS) && (!epi->bias || (reinterpret_cast<uintptr_t>(epi->bias) & 15)))
     return fail(MPH_EINVAL, "spmm: bias must be non-null and 16-byte aligned");
   if (epi && (epi->flags & MPH_EPI_ROWSCALE) && !epi->row_scale) return fail(MPH_EINVAL, "spmm: null row_scale");
+  if (epi && (epi->flags & MPH_EPI_SIGNBITS)) {
+    if (!epi->bits_out || epi->ld_bits < w / 4) return fail(MPH_EINVAL, "spmm: SIGNBITS needs bits_out, ld_bits >= w/4");
+    if (part == 0) return fail(MPH_EINVAL, "spmm: SIGNBITS on part 1 (or whole rows), not part 0");
+  }
   if (g->n_rows == 0) return MPH_OK;
   MPH_TRY(ensure_graph_items(g, s));
   SpmmArgs a{};
+  a.bits_out = (epi && (epi->flags & MPH_EPI_SIGNBITS)) ? epi->bits_out : nullptr;
+  a.ld_bits = epi ? epi->ld_bits : 0;
   a.val = nullptr;
   a.row_ptr = g->row_ptr;
   a.split = g->split;
@@ -555,7 +582,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.nv4 = w / 4;
   a.part = part;
   a.partial = part == 1 ? partial : nullptr;
-  a.epi.flags = epi ? epi->flags : 0u;
+  a.epi.flags = epi ? (epi->flags & ~MPH_EPI_SIGNBITS) : 0u;
   a.epi.bias = epi ? epi->bias : nullptr;
   a.epi.row_scale = epi ? epi->row_scale : nullptr;
   a.epi.drop = make_dropout(epi);
@@ -653,4 +680,10 @@ extern "C" int mph_spmm_part(const mph_graph* g, int32_t part, const float* in_d
   if (part < -1 || part > 1) return mph::fail(MPH_EINVAL, "spmm_part: part must be -1, 0 or 1");
   if (!g) return mph::fail(MPH_EINVAL, "spmm: null argument");
   return mph::spmm_launch(g, part, in_d, w, ld_in, out_d, ld_out, epi, g->dinv, (cudaStream_t)stream);
+}
+
+extern "C" int mph_spmm_signbits_ok(const mph_graph* g, int32_t w, int32_t* ok_h) {
+  if (!g || !ok_h) return mph::fail(MPH_EINVAL, "spmm_signbits_ok: null argument");
+  *ok_h = mph::spmm_signbits_ok(g, w) ? 1 : 0;
+  return MPH_OK;
 }

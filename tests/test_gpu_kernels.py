@@ -403,3 +403,84 @@ def test_sparse_feature_kernels(P, name, fo):
 
 
 
+
+
+# ---------------------------------------------------------------- sign bytes (MPH_EPI_SIGNBITS / MASK_BITS)
+def _sign_bytes(x: np.ndarray, ld: int) -> np.ndarray:
+    """The SIGNBITS layout written out: bit t of byte [r, c // 4] = (x[r, c] > 0), t = c % 4."""
+    M, N = x.shape
+    out = np.zeros((M, ld), dtype=np.uint8)
+    pos = (x > 0).astype(np.uint8)
+    for c in range(N):
+        out[:, c // 4] |= pos[:, c] << (c % 4)
+    return out
+
+
+@pytest.mark.parametrize("N,bf16_out", [(48, False), (256, False), (128, True)])
+def test_gemm_nt_sign_bytes_and_bit_mask(P, N, bf16_out):
+    """SIGNBITS writes the signs of exactly the values the GEMM stores (ReLU output, TF32 or BF16
+    rounded), and a dH-style GEMM masked by those sign bytes (MASK_BITS) is bit-identical to the same
+    GEMM masked by the stored values (MASK) — the decisions are the same, 1/16 of the bytes."""
+    from paper_2512_01678_b200._lib import (EPI_BF16, EPI_COLSUM, EPI_MASK, EPI_MASK_BF16, EPI_MASK_BITS, EPI_RELU,
+                                            EPI_ROWSCALE, EPI_SIGNBITS, EPI_TF32, Epilogue, mph_gemm_nt)
+    M, K = 1300, 64
+    rng = np.random.default_rng(N)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    Bt = rng.standard_normal((N, K)).astype(np.float32)
+    s = torch.cuda.current_stream().cuda_stream
+    ld_sb = ((N + 3) // 4 + 7) // 8 * 8
+    sb = torch.full((M, ld_sb), 0xAA, dtype=torch.uint8, device="cuda")
+    e = Epilogue()
+    e.flags = EPI_RELU | EPI_SIGNBITS | (EPI_BF16 if bf16_out else EPI_TF32)
+    e.mask_scale, e.bits_out, e.ld_bits = 1.0, sb.data_ptr(), ld_sb
+    h = torch.zeros((M, N), dtype=torch.bfloat16 if bf16_out else torch.float32, device="cuda")
+    mph_gemm_nt(M, N, K, cuda(A).data_ptr(), K, cuda(Bt).data_ptr(), K, h.data_ptr(), N, C.byref(e), s)
+    torch.cuda.synchronize()
+    hv = h.float().cpu().numpy()
+    assert np.array_equal(sb.cpu().numpy()[:, :(N + 3) // 4], _sign_bytes(hv, ld_sb)[:, :(N + 3) // 4])
+    # dH-style GEMM: G (M x K2) times W (N x K2)^T masked by H's signs, 1.5 = dropout scale
+    K2 = 32
+    G = rng.standard_normal((M, K2)).astype(np.float32)
+    W = rng.standard_normal((N, K2)).astype(np.float32)
+    rs = cuda(rng.random(M).astype(np.float32) + 0.5)
+    outs = []
+    for bits in (False, True):
+        cs = torch.zeros(((M + 127) // 128, N), device="cuda")
+        d = Epilogue()
+        d.flags = EPI_MASK | EPI_COLSUM | EPI_ROWSCALE | (EPI_MASK_BITS if bits else (EPI_MASK_BF16 if bf16_out else 0))
+        d.mask_src = sb.data_ptr() if bits else h.data_ptr()
+        d.ld_mask = ld_sb if bits else N
+        d.mask_scale, d.row_scale, d.colsum_out = 1.5, rs.data_ptr(), cs.data_ptr()
+        o = torch.zeros((M, N), device="cuda")
+        mph_gemm_nt(M, N, K2, cuda(G).data_ptr(), K2, cuda(W).data_ptr(), K2, o.data_ptr(), N, C.byref(d), s)
+        outs.append((o, cs))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    assert int((outs[1][0] != 0).sum()) > 0
+
+
+@pytest.mark.parametrize("w", [16, 48, 64, 128, 256])
+def test_spmm_sign_bytes(P, spmm_graph, w):
+    """mph_spmm with SIGNBITS: the sign bytes of exactly the stored (ReLU, TF32-rounded) output, for
+    every lane map the widths select (incl. the column slabs of 128 / 256 on a dense graph)."""
+    from paper_2512_01678_b200._lib import EPI_BIAS, EPI_RELU, EPI_SIGNBITS, EPI_TF32, Epilogue
+    from paper_2512_01678_b200._lib import mph_spmm_signbits_ok
+    g, ref = spmm_graph
+    n = ref.num_nodes
+    ok = C.c_int32()
+    mph_spmm_signbits_ok(g.h, w, C.byref(ok))
+    assert ok.value == 1
+    rng = np.random.default_rng(w)
+    T = cuda(rng.standard_normal((n, w)).astype(np.float32))
+    bias = cuda(rng.standard_normal(w).astype(np.float32) * 0.1)
+    ld_sb = (w // 4 + 7) // 8 * 8
+    sb = torch.full((n, ld_sb), 0x55, dtype=torch.uint8, device="cuda")
+    e = Epilogue()
+    e.flags = EPI_BIAS | EPI_RELU | EPI_TF32 | EPI_SIGNBITS
+    e.bias, e.mask_scale, e.bits_out, e.ld_bits = bias.data_ptr(), 1.0, sb.data_ptr(), ld_sb
+    out = torch.zeros((n, w), device="cuda")
+    g.spmm(T, out, w=w, epi=e)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert np.array_equal(sb.cpu().numpy()[:, :w // 4], _sign_bytes(o, ld_sb)[:, :w // 4])
+    assert 0 < int((o > 0).sum()) < o.size
