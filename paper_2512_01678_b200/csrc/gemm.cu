@@ -422,11 +422,13 @@ int gemm_nt_launch_ex(int M, int N, int K, const void* A, int lda, const void* B
   else
     tm = tcm;
   const size_t smem = fixed + (size_t)p.stages * stage_bytes;
-  const bool sb = (flags & (MPH_EPI_SIGNBITS | MPH_EPI_MASK_BITS)) != 0;
-  auto kern = bf16 ? (sb ? k_gemm_nt<true, true> : k_gemm_nt<true, false>)
-                   : (sb ? k_gemm_nt<false, true> : k_gemm_nt<false, false>);
-  static size_t configured[4] = {0, 0, 0, 0};
-  const int ki = (bf16 ? 2 : 0) + (sb ? 1 : 0);
+  if ((flags & MPH_EPI_SIGNBITS) && (flags & MPH_EPI_MASK_BITS))
+    return fail(MPH_ENOTSUP, "gemm_nt: SIGNBITS and MASK_BITS in one launch");
+  const int sb = (flags & MPH_EPI_SIGNBITS) ? 1 : (flags & MPH_EPI_MASK_BITS) ? 2 : 0;
+  auto kern = bf16 ? (sb == 1 ? k_gemm_nt<true, 1> : sb == 2 ? k_gemm_nt<true, 2> : k_gemm_nt<true, 0>)
+                   : (sb == 1 ? k_gemm_nt<false, 1> : sb == 2 ? k_gemm_nt<false, 2> : k_gemm_nt<false, 0>);
+  static size_t configured[6] = {0, 0, 0, 0, 0, 0};
+  const int ki = (bf16 ? 3 : 0) + sb;
   if (smem > configured[ki]) {
     MPH_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured[ki] = smem;
