@@ -83,53 +83,48 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, c
     return;
   }
   const bool to_tf32 = (a.epi.flags & MPH_EPI_TF32) != 0;
-  constexpr bool sign_out = SGN;
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
     const int c4 = sub + j * LPR;
     if (c4 >= a.nv4) continue;
-    uint32_t nib = 0u;  // SIGNBITS: stored value > 0, 4 bits per float4
-    if (c4 < a.nv4) {
-      float4 v = acc[j];
-      if (a.part == 1)
-        v = f4_add(v, a.partial ? reinterpret_cast<const float4*>(a.partial + (int64_t)row * a.nv4 * 4)[c4] : orow[c4]);
-      v.x *= du;
-      v.y *= du;
-      v.z *= du;
-      v.w *= du;
-      if (a.epi.flags & MPH_EPI_BIAS) {
-        float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
-        v = f4_add(v, b);
-      }
-      if (a.epi.flags & MPH_EPI_RELU) {
-        v.x = fmaxf(v.x, 0.0f);
-        v.y = fmaxf(v.y, 0.0f);
-        v.z = fmaxf(v.z, 0.0f);
-        v.w = fmaxf(v.w, 0.0f);
-      }
-      if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, a.epi.c4_0 + c4);
-      if (a.epi.flags & MPH_EPI_ROWSCALE) {
-        v.x *= rs;
-        v.y *= rs;
-        v.z *= rs;
-        v.w *= rs;
-      }
-      if (a.epi.flags & MPH_EPI_BF16) {  // BF16 row (only feeds BF16 GEMMs); out/ld_out in bf16 elements
-        uint2* o16 = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + (int64_t)row * a.ld_out);
-        const uint2 q = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
-        o16[c4] = q;
-        if (sign_out)
-          nib = (uint32_t)bf16_positive(q.x & 0xFFFFu) | ((uint32_t)bf16_positive(q.x >> 16) << 1) |
-                ((uint32_t)bf16_positive(q.y & 0xFFFFu) << 2) | ((uint32_t)bf16_positive(q.y >> 16) << 3);
-      } else {
-        const float4 st = to_tf32 ? f4_tf32(v) : v;
-        st_f4_hint(orow + c4, st, pol);
-        nib = (uint32_t)(st.x > 0.0f) | ((uint32_t)(st.y > 0.0f) << 1) | ((uint32_t)(st.z > 0.0f) << 2) |
-              ((uint32_t)(st.w > 0.0f) << 3);
-      }
+    float4 v = acc[j];
+    if (a.part == 1)
+      v = f4_add(v, a.partial ? reinterpret_cast<const float4*>(a.partial + (int64_t)row * a.nv4 * 4)[c4] : orow[c4]);
+    v.x *= du;
+    v.y *= du;
+    v.z *= du;
+    v.w *= du;
+    if (a.epi.flags & MPH_EPI_BIAS) {
+      float4 b = reinterpret_cast<const float4*>(a.epi.bias)[c4];
+      v = f4_add(v, b);
     }
-    if (sign_out && c4 < a.nv4)  // one byte per float4: its 4 sign bits (MPH_EPI_SIGNBITS layout)
-      reinterpret_cast<uint8_t*>(a.bits_out)[(int64_t)row * a.ld_bits + a.epi.c4_0 + c4] = (uint8_t)nib;
+    if (a.epi.flags & MPH_EPI_RELU) {
+      v.x = fmaxf(v.x, 0.0f);
+      v.y = fmaxf(v.y, 0.0f);
+      v.z = fmaxf(v.z, 0.0f);
+      v.w = fmaxf(v.w, 0.0f);
+    }
+    if (a.epi.flags & MPH_EPI_DROPOUT) v = apply_dropout(v, a.epi.drop, a.epi.row0 + row, a.epi.c4_0 + c4);
+    if (a.epi.flags & MPH_EPI_ROWSCALE) {
+      v.x *= rs;
+      v.y *= rs;
+      v.z *= rs;
+      v.w *= rs;
+    }
+    uint32_t nib;  // SGN: the 4 sign bits of the stored values, one byte per float4 (MPH_EPI_SIGNBITS)
+    if (a.epi.flags & MPH_EPI_BF16) {  // BF16 row (only feeds BF16 GEMMs); out/ld_out in bf16 elements
+      uint2* o16 = reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + (int64_t)row * a.ld_out);
+      const uint2 q = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+      o16[c4] = q;
+      nib = (uint32_t)bf16_positive(q.x & 0xFFFFu) | ((uint32_t)bf16_positive(q.x >> 16) << 1) |
+            ((uint32_t)bf16_positive(q.y & 0xFFFFu) << 2) | ((uint32_t)bf16_positive(q.y >> 16) << 3);
+    } else {
+      const float4 st = to_tf32 ? f4_tf32(v) : v;
+      st_f4_hint(orow + c4, st, pol);
+      nib = (uint32_t)(st.x > 0.0f) | ((uint32_t)(st.y > 0.0f) << 1) | ((uint32_t)(st.z > 0.0f) << 2) |
+            ((uint32_t)(st.w > 0.0f) << 3);
+    }
+    if (SGN) reinterpret_cast<uint8_t*>(a.bits_out)[(int64_t)row * a.ld_bits + a.epi.c4_0 + c4] = (uint8_t)nib;
   }
 }
 
