@@ -99,6 +99,11 @@ static void graph_free(mph_graph* g) {
   dev_free(g->send_ids);
   dev_free(g->send_buf);
   dev_free(g->items);
+  dev_free(g->sitems);
+  dev_free(g->vrow_ptr);
+  dev_free(g->vmap);
+  dev_free(g->chunk_part);
+  dev_free(g->srows);
   dev_free(g->item_counter);
   delete g;
 }

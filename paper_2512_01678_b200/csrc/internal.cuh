@@ -30,6 +30,21 @@ struct mph_graph {
   int2* items = nullptr;
   int n_items = 0;
   int* item_counter = nullptr;
+  // whole-row launches (part -1) over an operand larger than L2/2 walk the chunked virtual CSR
+  // (spmm.cu, build_split_items): rows longer than chunk_edges cut into virtual rows of <=
+  // chunk_edges entries; vrow_ptr [n_v + 1] into col_idx, vmap[v] = row or -1 - chunk, sitems runs
+  // of virtual rows; chunk partials in chunk_part (kChunkPartF4 float4 each); srows = {row, first
+  // chunk, n chunks} of every cut row, for the combine kernel
+  int split_mode = 0;  // MPH_SPMM_SPLIT at item build: 0 off, 1 operand > L2/2, 2 always
+  int64_t* vrow_ptr = nullptr;
+  int* vmap = nullptr;
+  int2* sitems = nullptr;
+  int n_sitems = 0;
+  int64_t n_chunks = 0;
+  int chunk_edges = 0;
+  float4* chunk_part = nullptr;
+  int4* srows = nullptr;
+  int n_srows = 0;
 };
 
 struct mph_features {

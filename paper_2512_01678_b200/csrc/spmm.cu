@@ -12,9 +12,13 @@
 //  * persistent warps pull work items from a global counter.  A work item is a run of
 //    consecutive rows holding about the same number of edges (built once per graph), so the
 //    power-law degree skew (Reddit hubs have 20x the mean degree) never idles a warp the way
-//    a block-per-row grid does; items holding a hub row are served first, so the longest
-//    rows start at t = 0 instead of forming the tail; rows are never split, so the summation
-//    order of every row is fixed (deterministic).
+//    a block-per-row grid does.  Two item lists: hub-first whole rows (items holding a hub row
+//    are served first, so the longest rows start at t = 0 instead of forming the tail), and,
+//    for whole-row launches whose gathered operand exceeds L2/2 (products), a chunked virtual
+//    CSR walked in row order: rows longer than S = 256 edges cut into chunks, their partial rows
+//    added in chunk order by k_spmm_combine, so the rows gathered at any moment stay a narrow
+//    window of the graph and its L2 hits are kept.  Either way the summation order
+//    of every row is fixed (deterministic).
 //  * per-edge values are pre-scaled by dinv at the producer (T' = dinv ⊙ T), so the kernel
 //    reads no per-edge weight: out[u] = dinv[u] · Σ_v T'[v]  ==  (Â·T)[u]  (Q1).
 //  * partial sums: a pairwise tree over each group of U gathers, a running sum per slot,
@@ -45,7 +49,7 @@ struct SpmmArgs {
   const float* dinv;  // output row scale (nullptr: 1)
   const float* in;
   float* out;
-  const int2* items;  // [first_row, end_row) per work item, hubs first
+  const int2* items;  // [first_row, end_row) per work item (hubs first), or {-1 - chunk, 0} (split items)
   int* counter;
   int n_items;
   int ld_in, ld_out, n_rows, nv4, part;
@@ -54,8 +58,14 @@ struct SpmmArgs {
   const float* partial;  // part 1 with a BF16 output: part 0's FP32 sums (row stride nv4·4), else nullptr
   uint32_t* bits_out;    // SIGNBITS: sign nibbles, one byte per float4 column, [rows][ld_bits] bytes
   int ld_bits;
+  // whole-row launches over the chunked virtual CSR (build_split_items): row_ptr is the virtual
+  // row_ptr, vmap[v] the output row of virtual row v, or -1 - chunk for a chunk of a cut row
+  const int* vmap;
+  float4* chunk_part;    // [chunk][kChunkPartF4] partial row sums
   EpiDev epi;
 };
+
+constexpr int kChunkPartF4 = 128;  // float4 per chunk partial: the widest launch (512 columns)
 
 __device__ __forceinline__ float4 apply_dropout(float4 v, const Dropout& d, int64_t grow, int c4) {
   const uint32_t ep = d.epoch_dev ? (uint32_t)*d.epoch_dev : d.epoch;
@@ -137,18 +147,17 @@ __device__ __forceinline__ void store_row(const SpmmArgs& a, int row, int sub, c
 // edges keep the plain single-block sum.  Alg. 3 P:373-384 (the per-row sum), P:357 (skew).
 constexpr int64_t kHubBlock = 256;
 
-template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false, bool PK = true>
-__device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
+// Sum of the gathered rows of CSR entries [s, e) (one row, or one chunk of a long row): on return
+// every lane holds the total of its columns sub + j·LPR (slot partials met in the xor tree).
+template <int LPR, int VPL, bool HAS_VAL, int UOV, bool PK>
+__device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e, int lane, float4 (&acc)[VPL]) {
   constexpr int ES = 32 / LPR;
   // U gathers per slot in flight; U*VPL float4 loads per lane before the first use
   constexpr int U0 = (32 / ES) < 8 ? (32 / ES) : 8;
   constexpr int U = UOV > 0 ? UOV : ((U0 * VPL > 8) ? ((8 / VPL) < 2 ? 2 : (8 / VPL)) : U0);
   const int slot = lane / LPR, sub = lane % LPR;
-  int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
-  if (a.part == 0) e = a.split[row];
-  if (a.part == 1) s = a.split[row];
   // acc sums the current block of kHubBlock edges; tot the finished blocks, in block order
-  float4 acc[VPL], tot[VPL];
+  float4 tot[VPL];
 #pragma unroll
   for (int j = 0; j < VPL; ++j) acc[j] = tot[j] = f4_zero();
   const uint64_t pol = l2_policy_evict_first();
@@ -214,10 +223,35 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
       acc[j].z += __shfl_xor_sync(0xffffffffu, acc[j].z, off);
       acc[j].w += __shfl_xor_sync(0xffffffffu, acc[j].w, off);
     }
-  if (slot != 0) return;
-  const float du = (a.part != 0 && a.dinv) ? a.dinv[row] : 1.0f;
-  const float rs = (a.part != 0 && (a.epi.flags & MPH_EPI_ROWSCALE)) ? a.epi.row_scale[row] : 1.0f;
-  store_row<LPR, VPL, SGN>(a, row, sub, acc, du, rs, pol);
+}
+
+// One (virtual) row: its sum, then the fused epilogue by the slot-0 lanes.  Over the chunked
+// virtual CSR of a whole-row launch (vmap != nullptr) a virtual row is either a whole row of the
+// graph or chunk c of a long row (vmap = -1 - c: the sum of ≤ S consecutive CSR entries of it),
+// whose partial row goes to chunk_part[c]; k_spmm_combine adds a row's chunk partials in chunk
+// order after the launch and runs the epilogue, so every row's sum is fixed whatever order the
+// chunks ran in (deterministic, no atomics, no fences).  Walking rows in row order with long rows
+// cut this way keeps the rows gathered at any moment a narrow window of the graph;
+// the per-row code is the same for both (a second copy of the gather loop costs its registers).
+template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false, bool PK = true>
+__device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
+  int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
+  if (a.part == 0) e = a.split[row];
+  if (a.part == 1) s = a.split[row];
+  float4 acc[VPL];
+  spmm_sum<LPR, VPL, HAS_VAL, UOV, PK>(a, s, e, lane, acc);
+  if (lane >= LPR) return;
+  const int orow = (!HAS_VAL && a.vmap) ? a.vmap[row] : row;
+  if (!HAS_VAL && orow < 0) {
+    float4* part = a.chunk_part + (int64_t)(-1 - orow) * kChunkPartF4;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+      if (lane + j * LPR < a.nv4) part[lane + j * LPR] = acc[j];
+    return;
+  }
+  const float du = (a.part != 0 && a.dinv) ? a.dinv[orow] : 1.0f;
+  const float rs = (a.part != 0 && (a.epi.flags & MPH_EPI_ROWSCALE)) ? a.epi.row_scale[orow] : 1.0f;
+  store_row<LPR, VPL, SGN>(a, orow, lane, acc, du, rs, l2_policy_evict_first());
 }
 
 // 4 blocks (32 warps) per SM within the 64-register budget for the one-float4-per-lane shapes
@@ -362,6 +396,28 @@ __global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
   }
 }
 
+// The rows cut into chunks: one warp per row adds the row's chunk partials in chunk order (float4
+// columns lane + 32·j) and runs the fused epilogue (store_row) exactly as an unsplit row would.
+template <bool SGN>
+__global__ void __launch_bounds__(256) k_spmm_combine(SpmmArgs a, const int4* srows, int n_srows) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int r = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r < n_srows; r += nwarps) {
+    const int4 sr = srows[r];  // {row, first chunk, n chunks, -}
+    float4 acc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] = f4_zero();
+    const float4* p = a.chunk_part + (int64_t)sr.y * kChunkPartF4;
+    for (int q = 0; q < sr.z; ++q, p += kChunkPartF4)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lane + 32 * j < a.nv4) acc[j] = f4_add(acc[j], p[lane + 32 * j]);
+    const float du = a.dinv ? a.dinv[sr.x] : 1.0f;
+    const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[sr.x] : 1.0f;
+    store_row<32, 4, SGN>(a, sr.x, lane, acc, du, rs, l2_policy_evict_first());
+  }
+}
+
 Dropout make_dropout(const mph_epilogue* e) {
   Dropout d{};
   if (!e || !(e->flags & MPH_EPI_DROPOUT) || e->dropout_p <= 0.0f) {
@@ -389,7 +445,8 @@ int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** i
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, nnz / ((int64_t)sms * 24 * 32)));
+  int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, nnz / ((int64_t)sms * 24 * 32)));
+  if (const char* ie = getenv("MPH_SPMM_ITEM_EDGES")) kItemEdges = std::max<int64_t>(8, atoll(ie));  // experiments
   std::vector<int64_t> rp((size_t)n_rows + 1);
   MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), row_ptr_d, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   MPH_CUDA_TRY(cudaStreamSynchronize(s));
@@ -441,10 +498,96 @@ int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** i
   return MPH_OK;
 }
 
+// The chunked virtual CSR of whole-row launches (part -1): every row longer than S edges is cut
+// into ⌈deg/S⌉ virtual rows of ≤ S consecutive CSR entries (vrow_ptr indexes the graph's col_idx;
+// vmap[v] = -1 - chunk), the other rows stay whole (vmap[v] = row), and the work items are runs of
+// consecutive virtual rows of about S edges, all in row order.  Walking the graph in row order
+// keeps the rows gathered at any moment a narrow window (a community of the planted partition, the
+// co-purchase clusters of products): with long rows as whole items, served first, the one warp on
+// a hub keeps gathering long after the rest of the grid has moved on, and its hits become misses
+// (LRU replay tools/sim/lru_items.c: 29 % of products' 128-wide gathers miss an 85 MB
+// L2 with hub rows first, 16 % with chunks of 256; ncu: 10.8 -> 6.9 GB DRAM per launch).
+// S = MPH_SPMM_CHUNK_EDGES, default min(E, 256) (E as in build_work_items).
+static int build_split_items(mph_graph* g, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t E = std::max<int64_t>(64, std::min<int64_t>(2048, g->nnz / ((int64_t)sms * 24 * 32)));
+  // graphs with fewer than 256 edges per item (E < 256: arxiv, 1.2 M edges) keep the hub-first
+  // items: their SpMM measured 3 % slower on the chunked CSR
+  if (E < 256 && g->split_mode != 2) return MPH_OK;
+  int64_t S = std::min<int64_t>(E, 256);
+  if (const char* ce = getenv("MPH_SPMM_CHUNK_EDGES")) S = std::max<int64_t>(32, atoll(ce));  // experiments
+  std::vector<int64_t> rp((size_t)g->n_rows + 1);
+  MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), g->row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  MPH_CUDA_TRY(cudaStreamSynchronize(s));
+  std::vector<int64_t> vrp;
+  std::vector<int> vmap;
+  std::vector<int2> items;
+  std::vector<int4> srows;  // {row, first chunk, n chunks, -}
+  vrp.reserve((size_t)g->n_rows + 1);
+  vmap.reserve((size_t)g->n_rows);
+  int64_t n_chunks = 0;
+  for (int r = 0; r < g->n_rows; ++r) {
+    const int64_t d = rp[r + 1] - rp[r];
+    if (d > S) {
+      const int nc = (int)((d + S - 1) / S);
+      srows.push_back(make_int4(r, (int)n_chunks, nc, 0));
+      for (int k = 0; k < nc; ++k) {
+        vrp.push_back(rp[r] + (int64_t)k * S);
+        vmap.push_back((int)(-1 - n_chunks));
+        ++n_chunks;
+      }
+    } else {
+      vrp.push_back(rp[r]);
+      vmap.push_back(r);
+    }
+  }
+  vrp.push_back(rp[g->n_rows]);
+  if (vmap.size() > (size_t)INT32_MAX / 2) return fail(MPH_ENOTSUP, "spmm: %zu virtual rows", vmap.size());
+  const int n_v = (int)vmap.size();
+  int v0 = 0;
+  int64_t acc = 0;
+  for (int v = 0; v < n_v; ++v) {
+    acc += vrp[v + 1] - vrp[v];
+    if (acc >= S) {
+      items.push_back(make_int2(v0, v + 1));
+      v0 = v + 1;
+      acc = 0;
+    }
+  }
+  if (v0 < n_v) items.push_back(make_int2(v0, n_v));
+  if (!n_chunks) return MPH_OK;  // no row longer than S: the whole-row items serve as they are
+  MPH_TRY(dev_alloc(&g->vrow_ptr, vrp.size()));
+  MPH_TRY(dev_alloc(&g->vmap, vmap.size()));
+  MPH_TRY(dev_alloc(&g->sitems, std::max<size_t>(items.size(), 1)));
+  MPH_TRY(dev_alloc(&g->chunk_part, (size_t)n_chunks * kChunkPartF4));
+  MPH_TRY(dev_alloc(&g->srows, srows.size()));
+  MPH_CUDA_TRY(cudaMemcpyAsync(g->vrow_ptr, vrp.data(), vrp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  MPH_CUDA_TRY(cudaMemcpyAsync(g->vmap, vmap.data(), vmap.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+  MPH_CUDA_TRY(cudaMemcpyAsync(g->sitems, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+  MPH_CUDA_TRY(cudaMemcpyAsync(g->srows, srows.data(), srows.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+  MPH_CUDA_TRY(cudaStreamSynchronize(s));
+  g->n_sitems = (int)items.size();
+  g->n_chunks = n_chunks;
+  g->n_srows = (int)srows.size();
+  g->chunk_edges = (int)S;
+  return MPH_OK;
+}
+
+// MPH_SPMM_SPLIT, read when a graph's items are built (setup): 0 off, 1 (default) when the gathered
+// operand exceeds L2/2, 2 for every warp-per-row whole-row launch (tests)
+static int split_mode_env() {
+  const char* e = getenv("MPH_SPMM_SPLIT");
+  return e ? atoi(e) : 1;
+}
+
 int ensure_graph_items(const mph_graph* gc, cudaStream_t s) {
   mph_graph* g = const_cast<mph_graph*>(gc);
   if (g->items) return MPH_OK;
   MPH_TRY(build_work_items(g->row_ptr, g->n_rows, g->nnz, &g->items, &g->n_items, s));
+  g->split_mode = split_mode_env();
+  if (g->split_mode) MPH_TRY(build_split_items(g, s));
   MPH_TRY(dev_alloc(&g->item_counter, 1));
   return MPH_OK;
 }
@@ -532,6 +675,35 @@ static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
   return launch_spmm<32, 4, HAS_VAL, 0, SGN>(a, s);
 }
 
+// One whole-row launch: over the chunked virtual CSR when the gathered operand exceeds half of L2
+// (what the window of concurrently walked rows buys is L2 hits; an L2-resident operand - reddit's
+// 64-wide slabs, 60 MB - gains nothing and would pay for the chunk partials) and the launch is a
+// warp-per-row one, then the combine of the cut rows; otherwise over the hub-first whole-row items.
+static int run_spmm(SpmmArgs a, const mph_graph* g, cudaStream_t s) {
+  static int64_t l2_bytes = -1;
+  if (l2_bytes < 0) {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+    l2_bytes = v;
+  }
+  const bool rows_kernel = a.row_slots && a.nv4 <= 16;
+  const bool big = g->split_mode == 2 || (int64_t)g->n_cols * a.nv4 * 16 > l2_bytes / 2;
+  const bool use_split = a.part == -1 && g->sitems && !rows_kernel && big;
+  if (!use_split) return dispatch_spmm<false>(a, s);
+  a.row_ptr = g->vrow_ptr;
+  a.vmap = g->vmap;
+  a.items = g->sitems;
+  a.n_items = g->n_sitems;
+  a.chunk_part = g->chunk_part;
+  MPH_TRY(dispatch_spmm<false>(a, s));
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(g->n_srows, 8), 148 * 8);
+  if (a.bits_out) k_spmm_combine<true><<<grid, 256, 0, s>>>(a, g->srows, g->n_srows);
+  else k_spmm_combine<false><<<grid, 256, 0, s>>>(a, g->srows, g->n_srows);
+  count_launch();
+  return launch_check("spmm combine");
+}
+
 // MPH_EPI_SIGNBITS on mph_spmm: every lane map stores one sign byte per float4 column it owns.
 bool spmm_signbits_ok(const mph_graph* g, int w) { return g && w > 0 && w % 4 == 0 && w <= 512; }
 
@@ -607,11 +779,11 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
       b.nv4 = std::min(slab, w - c0) / 4;
       if (b.epi.bias) b.epi.bias = a.epi.bias + c0;
       b.epi.c4_0 = c0 / 4;
-      MPH_TRY(dispatch_spmm<false>(b, s));
+      MPH_TRY(run_spmm(b, g, s));
     }
     return MPH_OK;
   }
-  return dispatch_spmm<false>(a, s);
+  return run_spmm(a, g, s);
 }
 
 int spmm_csr_launch(const int64_t* row_ptr, const int32_t* col, const float* val, int n_rows, const int2* items,

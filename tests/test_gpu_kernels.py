@@ -484,3 +484,63 @@ def test_spmm_sign_bytes(P, spmm_graph, w):
     o = out.cpu().numpy()
     assert np.array_equal(sb.cpu().numpy()[:, :w // 4], _sign_bytes(o, ld_sb)[:, :w // 4])
     assert 0 < int((o > 0).sum()) < o.size
+
+
+@pytest.mark.parametrize("chunk", ["32", "100", ""])
+def test_spmm_chunked_long_rows(P, chunk, monkeypatch):
+    """Whole-row launches over the chunked virtual CSR (rows longer than S edges cut into chunks of
+    S, MPH_SPMM_CHUNK_EDGES; default min(E, 256); MPH_SPMM_SPLIT=2 uses it at every operand size,
+    the default only above L2/2): the combine kernel adds a row's chunk partials in chunk order.
+    Every width within the FP32 aggregation bound, bitwise deterministic over repeated launches,
+    the fused epilogue intact, and the same bound with the hub-first whole-row items (SPLIT=0)."""
+    from paper_2512_01678_b200._lib import EPI_BIAS, EPI_RELU, EPI_SIGNBITS, Epilogue
+    if chunk:
+        monkeypatch.setenv("MPH_SPMM_CHUNK_EDGES", chunk)
+    monkeypatch.setenv("MPH_SPMM_SPLIT", "2")
+    w0 = make_small(4001, 90000, 4, 5, seed=71, alpha=2.1)
+    hubs = [0, 17, 4000]                                          # degree 3000, 1001, 257 + ragged chunks
+    src = np.concatenate([w0["src"]] + [np.full(k, h, np.int32) for h, k in zip(hubs, (3000, 1001, 257))])
+    dst = np.concatenate([w0["dst"]] + [np.arange(1, k + 1, dtype=np.int32) * 3 % 4001 for k in (3000, 1001, 257)])
+    ref = oracle.graph_build(src, dst, 4001)
+    # work items are built at a graph's first SpMM, under the environment of that moment
+    probe_in, probe_out = torch.zeros((4001, 4), device="cuda"), torch.zeros((4001, 4), device="cuda")
+    g = P.Graph(src, dst, 4001)
+    g.spmm(probe_in, probe_out, w=4)
+    monkeypatch.setenv("MPH_SPMM_SPLIT", "0")
+    g_whole = P.Graph(src, dst, 4001)
+    g_whole.spmm(probe_in, probe_out, w=4)
+    monkeypatch.setenv("MPH_SPMM_SPLIT", "2")
+    for w in (4, 48, 64, 128, 256, 512):
+        rng = np.random.default_rng(w + 7)
+        T = rng.standard_normal((ref.num_nodes, w)).astype(np.float32)
+        tin = cuda((ref.dinv[:, None] * T).astype(np.float32))
+        want, bound = oracle.aggregate(ref, T), agg_bound(ref, T)
+        outs = []
+        for _ in range(3):
+            out = torch.zeros((ref.num_nodes, w), device="cuda")
+            g.spmm(tin, out, w=w)
+            outs.append(out)
+        torch.cuda.synchronize()
+        assert all(torch.equal(outs[0], o) for o in outs[1:]), f"w={w}: not deterministic"
+        assert_agg_close(outs[0].cpu().numpy(), want, bound, what=f"chunked spmm w={w} S={chunk or 'default'}")
+        ow = torch.zeros((ref.num_nodes, w), device="cuda")
+        g_whole.spmm(tin, ow, w=w)
+        assert_agg_close(ow.cpu().numpy(), want, bound, what=f"whole-row spmm w={w}")
+    # fused bias + ReLU + sign bytes through the chunk path
+    w = 64
+    rng = np.random.default_rng(3)
+    T = rng.standard_normal((ref.num_nodes, w)).astype(np.float32)
+    b = rng.standard_normal(w).astype(np.float32)
+    tin, bias = cuda((ref.dinv[:, None] * T).astype(np.float32)), cuda(b)
+    bits = torch.zeros((ref.num_nodes, 16), dtype=torch.uint8, device="cuda")
+    e = Epilogue()
+    e.flags = EPI_BIAS | EPI_RELU | EPI_SIGNBITS
+    e.bias = bias.data_ptr()
+    e.mask_scale = 1.0
+    e.bits_out = bits.data_ptr()
+    e.ld_bits = 16
+    out = torch.zeros((ref.num_nodes, w), device="cuda")
+    g.spmm(tin, out, w=w, epi=e)
+    Z = out.cpu().numpy()
+    assert_agg_close(Z, np.maximum(oracle.aggregate(ref, T) + b, 0), agg_bound(ref, T) + np.abs(b), what="chunked epilogue")
+    assert np.array_equal(bits.cpu().numpy(), _sign_bytes(Z, 16))
