@@ -11,7 +11,7 @@ cap() {  # name regex skip count config [agg] [precision]
     python tools/profile_step.py --config $5 --epochs 2 --agg ${6:-gcn} --precision ${7:-tf32} > /dev/null 2>&1; echo "$1 rc=$?"
 }
 cap spmm_reddit k_spmm 6 6 reddit
-cap spmm_products k_spmm 7 7 products
+cap spmm_products k_spmm 12 12 products   # 7 k_spmm + 5 k_spmm_combine per epoch (chunked CSR)
 cap gemm_products k_gemm 8 8 products
 cap gemm_reddit k_gemm 5 5 reddit
 cap sparse_nell "k_spmm|k_sparse" 9 9 nell
