@@ -408,10 +408,24 @@ __global__ void __launch_bounds__(256) k_spmm_combine(SpmmArgs a, const int4* sr
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = f4_zero();
     const float4* p = a.chunk_part + (int64_t)sr.y * kChunkPartF4;
-    for (int q = 0; q < sr.z; ++q, p += kChunkPartF4)
+    if (a.nv4 <= 32) {  // one float4 per lane: four chunks' loads in flight, added in chunk order
+      float4 v = f4_zero();
+      int q = 0;
+      for (; q + 4 <= sr.z; q += 4) {
+        float4 x[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (lane + 32 * j < a.nv4) acc[j] = f4_add(acc[j], p[lane + 32 * j]);
+        for (int t = 0; t < 4; ++t) x[t] = lane < a.nv4 ? p[(int64_t)(q + t) * kChunkPartF4 + lane] : f4_zero();
+#pragma unroll
+        for (int t = 0; t < 4; ++t) v = f4_add(v, x[t]);
+      }
+      for (; q < sr.z; ++q) v = f4_add(v, lane < a.nv4 ? p[(int64_t)q * kChunkPartF4 + lane] : f4_zero());
+      acc[0] = v;
+    } else {
+      for (int q = 0; q < sr.z; ++q, p += kChunkPartF4)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (lane + 32 * j < a.nv4) acc[j] = f4_add(acc[j], p[lane + 32 * j]);
+    }
     const float du = a.dinv ? a.dinv[sr.x] : 1.0f;
     const float rs = (a.epi.flags & MPH_EPI_ROWSCALE) ? a.epi.row_scale[sr.x] : 1.0f;
     store_row<32, 4, SGN>(a, sr.x, lane, acc, du, rs, l2_policy_evict_first());
