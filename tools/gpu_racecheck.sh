@@ -7,7 +7,7 @@ CS=/usr/local/cuda/bin/compute-sanitizer
 for tool in ${TOOLS:-racecheck synccheck}; do
   timeout 1500 $CS --tool $tool --print-limit 20 --log-file gpurun_out/${tool}_%p.log \
     python -m pytest tests/test_gpu_kernels.py -m gpu -q -p no:cacheprovider --timeout 1400 \
-    -k "${1:-gemm or softmax or spmm_widths or row_slots}" > gpurun_out/${tool}_pytest.log 2>&1
+    -k "${1:-gemm or softmax or spmm_widths or row_slots or chunked}" > gpurun_out/${tool}_pytest.log 2>&1
   echo "$tool rc=$?"; tail -1 gpurun_out/${tool}_pytest.log
   grep -h "ERROR SUMMARY\|RACECHECK SUMMARY\|hazard" gpurun_out/${tool}_*.log | sort | uniq -c | head -10
 done
