@@ -99,11 +99,13 @@ static void graph_free(mph_graph* g) {
   dev_free(g->send_ids);
   dev_free(g->send_buf);
   dev_free(g->items);
-  dev_free(g->sitems);
-  dev_free(g->vrow_ptr);
-  dev_free(g->vmap);
+  for (auto& c : g->scsr) {
+    dev_free(c.vrow_ptr);
+    dev_free(c.vmap);
+    dev_free(c.items);
+    dev_free(c.srows);
+  }
   dev_free(g->chunk_part);
-  dev_free(g->srows);
   dev_free(g->item_counter);
   delete g;
 }

@@ -30,21 +30,26 @@ struct mph_graph {
   int2* items = nullptr;
   int n_items = 0;
   int* item_counter = nullptr;
-  // whole-row launches (part -1) over an operand larger than L2/2 walk the chunked virtual CSR
-  // (spmm.cu, build_split_items): rows longer than chunk_edges cut into virtual rows of <=
-  // chunk_edges entries; vrow_ptr [n_v + 1] into col_idx, vmap[v] = row or -1 - chunk, sitems runs
-  // of virtual rows; chunk partials in chunk_part (kChunkPartF4 float4 each); srows = {row, first
-  // chunk, n chunks} of every cut row, for the combine kernel
+  // launches over an operand larger than L2/2 walk a chunked virtual CSR (spmm.cu,
+  // build_split_items), one per row range: whole rows (part -1), owned edges (part 0), ghost
+  // edges (part 1) of a localized graph.  Rows longer than chunk_edges entries are cut into
+  // virtual rows of <= chunk_edges; vrow_ptr [n_v + 1] indexes col_idx, vmap[v] = row or -1 -
+  // chunk, items = runs of virtual rows; srows = {row, first chunk, n chunks} of every cut row for
+  // the combine kernel.  chunk_part (kChunkPartF4 float4 per chunk) is shared by the three.
+  struct SplitCsr {
+    int64_t* vrow_ptr = nullptr;
+    int* vmap = nullptr;
+    int2* items = nullptr;
+    int n_items = 0;
+    int4* srows = nullptr;
+    int n_srows = 0;
+    int64_t n_chunks = 0;
+    int n_vrows = 0;
+  };
   int split_mode = 0;  // MPH_SPMM_SPLIT at item build: 0 off, 1 operand > L2/2, 2 always
-  int64_t* vrow_ptr = nullptr;
-  int* vmap = nullptr;
-  int2* sitems = nullptr;
-  int n_sitems = 0;
-  int64_t n_chunks = 0;
+  SplitCsr scsr[3];    // [part + 1]
   int chunk_edges = 0;
   float4* chunk_part = nullptr;
-  int4* srows = nullptr;
-  int n_srows = 0;
 };
 
 struct mph_features {

@@ -43,6 +43,7 @@ struct EpiDev {
 
 struct SpmmArgs {
   const int64_t* row_ptr;
+  const int64_t* row_end;  // row r's entries end at row_end[r] (row_ptr + 1, or a part's virtual row ends)
   const int64_t* split;
   const int32_t* col;
   const float* val;   // per-edge values (HAS_VAL kernels only)
@@ -235,9 +236,11 @@ __device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e
 // the per-row code is the same for both (a second copy of the gather loop costs its registers).
 template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false, bool PK = true>
 __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
-  int64_t s = a.row_ptr[row], e = a.row_ptr[row + 1];
-  if (a.part == 0) e = a.split[row];
-  if (a.part == 1) s = a.split[row];
+  int64_t s = a.row_ptr[row], e = a.row_end[row];
+  if (!a.vmap) {  // (a virtual CSR has its part's ranges built in)
+    if (a.part == 0) e = a.split[row];
+    if (a.part == 1) s = a.split[row];
+  }
   float4 acc[VPL];
   spmm_sum<LPR, VPL, HAS_VAL, UOV, PK>(a, s, e, lane, acc);
   if (lane >= LPR) return;
@@ -532,59 +535,96 @@ static int build_split_items(mph_graph* g, cudaStream_t s) {
   if (E < 256 && g->split_mode != 2) return MPH_OK;
   int64_t S = std::min<int64_t>(E, 256);
   if (const char* ce = getenv("MPH_SPMM_CHUNK_EDGES")) S = std::max<int64_t>(32, atoll(ce));  // experiments
-  std::vector<int64_t> rp((size_t)g->n_rows + 1);
+  std::vector<int64_t> rp((size_t)g->n_rows + 1), sp;
   MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), g->row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  if (g->local && g->split) {
+    sp.resize((size_t)g->n_rows);
+    MPH_CUDA_TRY(cudaMemcpyAsync(sp.data(), g->split, sp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  }
   MPH_CUDA_TRY(cudaStreamSynchronize(s));
-  std::vector<int64_t> vrp;
-  std::vector<int> vmap;
-  std::vector<int2> items;
-  std::vector<int4> srows;  // {row, first chunk, n chunks, -}
-  vrp.reserve((size_t)g->n_rows + 1);
-  vmap.reserve((size_t)g->n_rows);
-  int64_t n_chunks = 0;
-  for (int r = 0; r < g->n_rows; ++r) {
-    const int64_t d = rp[r + 1] - rp[r];
-    if (d > S) {
-      const int nc = (int)((d + S - 1) / S);
-      srows.push_back(make_int4(r, (int)n_chunks, nc, 0));
-      for (int k = 0; k < nc; ++k) {
-        vrp.push_back(rp[r] + (int64_t)k * S);
-        vmap.push_back((int)(-1 - n_chunks));
-        ++n_chunks;
+  int64_t max_chunks = 0;
+  for (int part = -1; part <= (sp.empty() ? -1 : 1); ++part) {
+    // the row range of this launch kind: whole rows, owned-column edges, ghost-column edges
+    auto lo = [&](int r) { return part == 1 ? sp[r] : rp[r]; };
+    auto hi = [&](int r) { return part == 0 ? sp[r] : rp[r + 1]; };
+    std::vector<int64_t> vrp;
+    std::vector<int> vmap;
+    std::vector<int2> items;
+    std::vector<int4> srows;  // {row, first chunk, n chunks, -}
+    vrp.reserve((size_t)g->n_rows + 1);
+    vmap.reserve((size_t)g->n_rows);
+    int64_t n_chunks = 0;
+    for (int r = 0; r < g->n_rows; ++r) {
+      const int64_t d = hi(r) - lo(r);
+      if (d > S) {
+        const int nc = (int)((d + S - 1) / S);
+        srows.push_back(make_int4(r, (int)n_chunks, nc, 0));
+        for (int k = 0; k < nc; ++k) {
+          vrp.push_back(lo(r) + (int64_t)k * S);
+          vmap.push_back((int)(-1 - n_chunks));
+          ++n_chunks;
+        }
+      } else {
+        vrp.push_back(lo(r));
+        vmap.push_back(r);
       }
+    }
+    // a virtual row ends where the next begins: the last one at the row range's end
+    vrp.push_back(g->n_rows ? hi(g->n_rows - 1) : 0);
+    if (vmap.size() > (size_t)INT32_MAX / 2) return fail(MPH_ENOTSUP, "spmm: %zu virtual rows", vmap.size());
+    if (!n_chunks) continue;  // no row longer than S: the whole-row items serve as they are
+    // part 0/1 ranges are not contiguous across rows (row r's range ends at split[r], row r+1's
+    // starts at row_ptr[r+1]): their virtual rows keep explicit ends, so vrp holds begin/end pairs
+    const int n_v = (int)vmap.size();
+    std::vector<int64_t> vend((size_t)n_v);
+    {
+      int v = 0;
+      for (int r = 0; r < g->n_rows; ++r) {
+        const int64_t d = hi(r) - lo(r);
+        if (d > S) {
+          for (int64_t c = lo(r); c < hi(r); c += S) vend[v++] = std::min(c + S, hi(r));
+        } else {
+          vend[v++] = hi(r);
+        }
+      }
+    }
+    int v0 = 0;
+    int64_t acc = 0;
+    for (int v = 0; v < n_v; ++v) {
+      acc += vend[v] - vrp[v];
+      if (acc >= S) {
+        items.push_back(make_int2(v0, v + 1));
+        v0 = v + 1;
+        acc = 0;
+      }
+    }
+    if (v0 < n_v) items.push_back(make_int2(v0, n_v));
+    // device layout: vrow_ptr = [begin_0 .. begin_{n_v-1}, end_0 .. end_{n_v-1}] for parts 0/1;
+    // for whole rows (part -1) begin_{v+1} == end_v, so the plain n_v + 1 offsets suffice
+    std::vector<int64_t> dev_vrp;
+    if (part == -1) {
+      dev_vrp = vrp;
     } else {
-      vrp.push_back(rp[r]);
-      vmap.push_back(r);
+      dev_vrp.assign(vrp.begin(), vrp.begin() + n_v);
+      dev_vrp.insert(dev_vrp.end(), vend.begin(), vend.end());
     }
+    mph_graph::SplitCsr& c = g->scsr[part + 1];
+    MPH_TRY(dev_alloc(&c.vrow_ptr, dev_vrp.size()));
+    MPH_TRY(dev_alloc(&c.vmap, vmap.size()));
+    MPH_TRY(dev_alloc(&c.items, std::max<size_t>(items.size(), 1)));
+    MPH_TRY(dev_alloc(&c.srows, srows.size()));
+    MPH_CUDA_TRY(cudaMemcpyAsync(c.vrow_ptr, dev_vrp.data(), dev_vrp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    MPH_CUDA_TRY(cudaMemcpyAsync(c.vmap, vmap.data(), vmap.size() * sizeof(int), cudaMemcpyHostToDevice, s));
+    MPH_CUDA_TRY(cudaMemcpyAsync(c.items, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    MPH_CUDA_TRY(cudaMemcpyAsync(c.srows, srows.data(), srows.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+    MPH_CUDA_TRY(cudaStreamSynchronize(s));
+    c.n_items = (int)items.size();
+    c.n_srows = (int)srows.size();
+    c.n_chunks = n_chunks;
+    c.n_vrows = n_v;
+    max_chunks = std::max(max_chunks, n_chunks);
   }
-  vrp.push_back(rp[g->n_rows]);
-  if (vmap.size() > (size_t)INT32_MAX / 2) return fail(MPH_ENOTSUP, "spmm: %zu virtual rows", vmap.size());
-  const int n_v = (int)vmap.size();
-  int v0 = 0;
-  int64_t acc = 0;
-  for (int v = 0; v < n_v; ++v) {
-    acc += vrp[v + 1] - vrp[v];
-    if (acc >= S) {
-      items.push_back(make_int2(v0, v + 1));
-      v0 = v + 1;
-      acc = 0;
-    }
-  }
-  if (v0 < n_v) items.push_back(make_int2(v0, n_v));
-  if (!n_chunks) return MPH_OK;  // no row longer than S: the whole-row items serve as they are
-  MPH_TRY(dev_alloc(&g->vrow_ptr, vrp.size()));
-  MPH_TRY(dev_alloc(&g->vmap, vmap.size()));
-  MPH_TRY(dev_alloc(&g->sitems, std::max<size_t>(items.size(), 1)));
-  MPH_TRY(dev_alloc(&g->chunk_part, (size_t)n_chunks * kChunkPartF4));
-  MPH_TRY(dev_alloc(&g->srows, srows.size()));
-  MPH_CUDA_TRY(cudaMemcpyAsync(g->vrow_ptr, vrp.data(), vrp.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s));
-  MPH_CUDA_TRY(cudaMemcpyAsync(g->vmap, vmap.data(), vmap.size() * sizeof(int), cudaMemcpyHostToDevice, s));
-  MPH_CUDA_TRY(cudaMemcpyAsync(g->sitems, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
-  MPH_CUDA_TRY(cudaMemcpyAsync(g->srows, srows.data(), srows.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
-  MPH_CUDA_TRY(cudaStreamSynchronize(s));
-  g->n_sitems = (int)items.size();
-  g->n_chunks = n_chunks;
-  g->n_srows = (int)srows.size();
+  if (max_chunks) MPH_TRY(dev_alloc(&g->chunk_part, (size_t)max_chunks * kChunkPartF4));
   g->chunk_edges = (int)S;
   return MPH_OK;
 }
@@ -706,17 +746,20 @@ static int run_spmm(SpmmArgs a, const mph_graph* g, cudaStream_t s) {
   // rows narrower than 64 columns keep the hub-first items: products' 48-wide launch, issue-bound
   // rather than DRAM-bound, measured 2.6 % slower on the chunked CSR (1.489 vs 1.451 ms)
   const bool big = g->split_mode == 2 || ((int64_t)g->n_cols * a.nv4 * 16 > l2_bytes / 2 && a.nv4 >= 16);
-  const bool use_split = a.part == -1 && g->sitems && !rows_kernel && big;
+  const mph_graph::SplitCsr& c = g->scsr[a.part + 1];
+  const bool use_split = c.items && !rows_kernel && big;
   if (!use_split) return dispatch_spmm<false>(a, s);
-  a.row_ptr = g->vrow_ptr;
-  a.vmap = g->vmap;
-  a.items = g->sitems;
-  a.n_items = g->n_sitems;
+  a.row_ptr = c.vrow_ptr;
+  // whole rows: virtual row v ends where v + 1 begins; parts: explicit ends after the n_v begins
+  a.row_end = a.part == -1 ? c.vrow_ptr + 1 : c.vrow_ptr + c.n_vrows;
+  a.vmap = c.vmap;
+  a.items = c.items;
+  a.n_items = c.n_items;
   a.chunk_part = g->chunk_part;
   MPH_TRY(dispatch_spmm<false>(a, s));
-  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(g->n_srows, 8), 148 * 8);
-  if (a.bits_out) k_spmm_combine<true><<<grid, 256, 0, s>>>(a, g->srows, g->n_srows);
-  else k_spmm_combine<false><<<grid, 256, 0, s>>>(a, g->srows, g->n_srows);
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(c.n_srows, 8), 148 * 8);
+  if (a.bits_out) k_spmm_combine<true><<<grid, 256, 0, s>>>(a, c.srows, c.n_srows);
+  else k_spmm_combine<false><<<grid, 256, 0, s>>>(a, c.srows, c.n_srows);
   count_launch();
   return launch_check("spmm combine");
 }
@@ -752,6 +795,7 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.ld_bits = epi ? epi->ld_bits : 0;
   a.val = nullptr;
   a.row_ptr = g->row_ptr;
+  a.row_end = g->row_ptr + 1;
   a.split = g->split;
   a.col = g->col_idx;
   a.dinv = post;
@@ -814,6 +858,7 @@ int spmm_csr_launch(const int64_t* row_ptr, const int32_t* col, const float* val
   if (n_rows == 0 || n_items == 0) return MPH_OK;
   SpmmArgs a{};
   a.row_ptr = row_ptr;
+  a.row_end = row_ptr + 1;
   a.split = nullptr;
   a.col = col;
   a.val = val;

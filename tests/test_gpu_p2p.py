@@ -152,6 +152,20 @@ def _unpack(flat, offsets, ld_w, dims):
 
 @pytest.mark.parametrize("case", list(CASES))
 def test_p2p_epochs_match_oracle(case):
+    _check_p2p_case(case)
+
+
+@pytest.mark.parametrize("case", ["dense_tf_w2", "af_layer1_w3", "bf16_tf_w3"])
+def test_p2p_chunked_parts_match_oracle(case, monkeypatch):
+    """The owned-edge / ghost-edge launches (parts 0 and 1) over their chunked virtual CSRs
+    (MPH_SPMM_SPLIT=2 forces them at this size, chunks of 32 edges), ranks spawned with that
+    environment: the same bars as the whole-row-items run."""
+    monkeypatch.setenv("MPH_SPMM_SPLIT", "2")
+    monkeypatch.setenv("MPH_SPMM_CHUNK_EDGES", "32")
+    _check_p2p_case(case)
+
+
+def _check_p2p_case(case):
     world, kw, dims, force_mode, p_drop, epochs, prec = _case(case)
     res = _run(case)
     for r in res:
