@@ -149,6 +149,45 @@ def test_reddit_hub_rows_spmm(P, reddit_graphs, w):
     assert ratio <= 1.0
 
 
+@pytest.fixture(scope="module")
+def products_graphs(P):
+    w = make_workload("products")
+    n = w["cfg"].num_nodes
+    return P.Graph(w["src"], w["dst"], n), oracle.graph_build(w["src"], w["dst"], n)
+
+
+@pytest.mark.parametrize("w", [48, 104, 128, 256])
+def test_products_hub_rows_spmm(P, products_graphs, w):
+    """The FP32 aggregation bar 1e-5·(|Â|·|T|) on the full products-shaped graph's 64 largest hubs
+    (degrees up to ~7.5K) plus 64 random rows, in the launch configuration the epoch uses: w = 104
+    and 128 walk the chunked virtual CSR (hub rows cut into chunks of 256 edges whose partial rows
+    k_spmm_combine adds in chunk order), w = 256 as two such 128-wide slabs, w = 48
+    the hub-first whole-row items.  Expected values: the oracle's one-row-at-a-time Â·T."""
+    g, ref = products_graphs
+    n = ref.num_nodes
+    deg = np.diff(ref.row_ptr)
+    hubs = np.argsort(deg, kind="stable")[-64:]
+    rng = np.random.default_rng(2000 + w)
+    rows = np.concatenate([hubs, rng.choice(n, 64, replace=False)])
+    assert deg[hubs].max() > 5000 and deg[hubs].min() > 256   # every hub is cut into chunks
+    T = rng.standard_normal((n, w)).astype(np.float32)
+    Tp = (ref.dinv[:, None] * T).astype(np.float32)
+    out = torch.zeros((n, w), device="cuda")
+    tin = torch.from_numpy(Tp).cuda()
+    g.spmm(tin, out, w=w)
+    out2 = torch.zeros_like(out)
+    g.spmm(tin, out2, w=w)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)   # deterministic whatever order the chunks ran in
+    Z = out.cpu().numpy()[rows]
+    Zref = oracle.aggregate_rows(ref, T, rows)
+    bound = oracle.aggregate_rows(ref, np.abs(T), rows)
+    err = np.abs(Z.astype(np.float64) - Zref)
+    ratio = float((err / (1e-5 * bound + 1e-30)).max())
+    print(f"w={w}: max |err|/(1e-5·|Â||T|) = {ratio:.3g} (hubs {float((err[:64] / (1e-5 * bound[:64])).max()):.3g})")
+    assert ratio <= 1.0
+
+
 def test_products_forward_loss(P):
     w = make_workload("products")
     n = w["cfg"].num_nodes
