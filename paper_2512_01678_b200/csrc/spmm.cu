@@ -411,15 +411,23 @@ __global__ void __launch_bounds__(256) k_spmm_combine(SpmmArgs a, const int4* sr
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[j] = f4_zero();
     const float4* p = a.chunk_part + (int64_t)sr.y * kChunkPartF4;
-    if (a.nv4 <= 32) {  // one float4 per lane: four chunks' loads in flight, added in chunk order
+    if (a.nv4 <= 32) {  // one float4 per lane: eight chunks' loads in flight, added in chunk order
       float4 v = f4_zero();
       int q = 0;
-      for (; q + 4 <= sr.z; q += 4) {
+      for (; q + 8 <= sr.z; q += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) x[t] = lane < a.nv4 ? p[(int64_t)(q + t) * kChunkPartF4 + lane] : f4_zero();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v = f4_add(v, x[t]);
+      }
+      if (q + 4 <= sr.z) {
         float4 x[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) x[t] = lane < a.nv4 ? p[(int64_t)(q + t) * kChunkPartF4 + lane] : f4_zero();
 #pragma unroll
         for (int t = 0; t < 4; ++t) v = f4_add(v, x[t]);
+        q += 4;
       }
       for (; q < sr.z; ++q) v = f4_add(v, lane < a.nv4 ? p[(int64_t)q * kChunkPartF4 + lane] : f4_zero());
       acc[0] = v;
@@ -757,7 +765,7 @@ static int run_spmm(SpmmArgs a, const mph_graph* g, cudaStream_t s) {
   a.n_items = c.n_items;
   a.chunk_part = g->chunk_part;
   MPH_TRY(dispatch_spmm<false>(a, s));
-  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(c.n_srows, 8), 148 * 8);
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(c.n_srows, 8), 148 * 16);
   if (a.bits_out) k_spmm_combine<true><<<grid, 256, 0, s>>>(a, c.srows, c.n_srows);
   else k_spmm_combine<false><<<grid, 256, 0, s>>>(a, c.srows, c.n_srows);
   count_launch();
