@@ -44,6 +44,8 @@ struct EpiDev {
 struct SpmmArgs {
   const int64_t* row_ptr;
   const int64_t* row_end;  // row r's entries end at row_end[r] (row_ptr + 1, or a part's virtual row ends)
+  int64_t col_len;         // entries in col (the id prefetch never reads past it)
+  int contig;              // 1: whole-row launch over the graph's CSR (rows run contiguously through col)
   const int64_t* split;
   const int32_t* col;
   const float* val;   // per-edge values (HAS_VAL kernels only)
@@ -150,8 +152,9 @@ constexpr int64_t kHubBlock = 256;
 
 // Sum of the gathered rows of CSR entries [s, e) (one row, or one chunk of a long row): on return
 // every lane holds the total of its columns sub + j·LPR (slot partials met in the xor tree).
-template <int LPR, int VPL, bool HAS_VAL, int UOV, bool PK>
-__device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e, int lane, float4 (&acc)[VPL]) {
+template <int LPR, int VPL, bool HAS_VAL, int UOV, bool PK, bool CARRY = false>
+__device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e, int lane, float4 (&acc)[VPL],
+                                         int& carry, bool have) {
   constexpr int ES = 32 / LPR;
   // U gathers per slot in flight; U*VPL float4 loads per lane before the first use
   constexpr int U0 = (32 / ES) < 8 ? (32 / ES) : 8;
@@ -163,7 +166,9 @@ __device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e
   for (int j = 0; j < VPL; ++j) acc[j] = tot[j] = f4_zero();
   const uint64_t pol = l2_policy_evict_first();
   const int* vbits = reinterpret_cast<const int*>(a.val);
-  int nxt = (s + lane < e) ? ldg_stream_i32_hint(a.col + s + lane, pol) : 0;
+  // the row's first 32 ids: carried over from the previous row of a contiguous run (its last block
+  // prefetched them), else loaded now
+  int nxt = (CARRY && have) ? carry : ((s + lane < e) ? ldg_stream_i32_hint(a.col + s + lane, pol) : 0);
   int nxv = (HAS_VAL && s + lane < e) ? ldg_stream_i32_hint(vbits + s + lane, pol) : 0;
   int64_t blk_end = s + kHubBlock;
   for (int64_t base = s; base < e; base += 32) {
@@ -178,7 +183,14 @@ __device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e
     const int nb = (int)min((int64_t)32, e - base);
     const int my_c = nxt;
     const float my_v = __int_as_float(nxv);
-    nxt = (base + 32 + lane < e) ? ldg_stream_i32_hint(a.col + base + 32 + lane, pol) : 0;  // prefetch next ids
+    // prefetch the next 32 ids: the rest of this row, or (last block) the next row's first ids when
+    // rows run contiguously through col_idx (whole-row launches: a run of rows, or the chunked CSR)
+    if constexpr (CARRY) {
+      const int64_t pb = base + 32 < e ? base + 32 : e;
+      nxt = (pb + lane < a.col_len) ? ldg_stream_i32_hint(a.col + pb + lane, pol) : 0;
+    } else {
+      nxt = (base + 32 + lane < e) ? ldg_stream_i32_hint(a.col + base + 32 + lane, pol) : 0;
+    }
     if (HAS_VAL) nxv = (base + 32 + lane < e) ? ldg_stream_i32_hint(vbits + base + 32 + lane, pol) : 0;
     for (int k0 = 0; k0 < nb; k0 += ES * U) {
       float4 x[U][VPL];
@@ -211,6 +223,7 @@ __device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e
       }
     }
   }
+  if (CARRY) carry = nxt;  // the ids from position e on (the next row's first block in a contiguous run)
   if (e - s > kHubBlock) {
 #pragma unroll
     for (int j = 0; j < VPL; ++j) acc[j] = f4_add(tot[j], acc[j]);
@@ -234,15 +247,15 @@ __device__ __forceinline__ void spmm_sum(const SpmmArgs& a, int64_t s, int64_t e
 // chunks ran in (deterministic, no atomics, no fences).  Walking rows in row order with long rows
 // cut this way keeps the rows gathered at any moment a narrow window of the graph;
 // the per-row code is the same for both (a second copy of the gather loop costs its registers).
-template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false, bool PK = true>
-__device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
+template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false, bool PK = true, bool CARRY = false>
+__device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane, int& carry, bool have) {
   int64_t s = a.row_ptr[row], e = a.row_end[row];
   if (!a.vmap) {  // (a virtual CSR has its part's ranges built in)
     if (a.part == 0) e = a.split[row];
     if (a.part == 1) s = a.split[row];
   }
   float4 acc[VPL];
-  spmm_sum<LPR, VPL, HAS_VAL, UOV, PK>(a, s, e, lane, acc);
+  spmm_sum<LPR, VPL, HAS_VAL, UOV, PK, CARRY>(a, s, e, lane, acc, carry, have);
   if (lane >= LPR) return;
   const int orow = (!HAS_VAL && a.vmap) ? a.vmap[row] : row;
   if (!HAS_VAL && orow < 0) {
@@ -259,7 +272,7 @@ __device__ __forceinline__ void spmm_row(const SpmmArgs& a, int row, int lane) {
 
 // 4 blocks (32 warps) per SM within the 64-register budget for the one-float4-per-lane shapes
 // (the hub-block partials would otherwise cost a block per SM); 3 for the wider register tiles
-template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false>
+template <int LPR, int VPL, bool HAS_VAL, int UOV, bool SGN = false, bool CARRY = false>
 __global__ void __launch_bounds__(256, ((VPL == 1 || LPR == 4) ? 4 : 3)) k_spmm(SpmmArgs a) {
   const int lane = threadIdx.x & 31;
   while (true) {
@@ -268,7 +281,9 @@ __global__ void __launch_bounds__(256, ((VPL == 1 || LPR == 4) ? 4 : 3)) k_spmm(
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
-    for (int row = rr.x; row < rr.y; ++row) spmm_row<LPR, VPL, HAS_VAL, UOV, SGN>(a, row, lane);
+    int carry = 0;  // CARRY: row r + 1's entries start where row r's end (whole-row launch)
+    for (int row = rr.x; row < rr.y; ++row)
+      spmm_row<LPR, VPL, HAS_VAL, UOV, SGN, true, CARRY>(a, row, lane, carry, row > rr.x);
   }
 }
 
@@ -298,7 +313,8 @@ __global__ void __launch_bounds__(256, 3) k_spmm_rows(SpmmArgs a) {
     if (it >= a.n_items) break;
     const int2 rr = a.items[it];
     if (rr.y - rr.x == 1) {  // a long row (> E edges) is an item of its own: all slots on it
-      spmm_row<LPR, VPL, false, 0, SGN, false>(a, rr.x, lane);  // scalar adds: packed ones spill here
+      int carry = 0;
+      spmm_row<LPR, VPL, false, 0, SGN, false>(a, rr.x, lane, carry, false);  // scalar adds: packed ones spill here
       continue;
     }
     int w0 = rr.x;  // row bounds window: lane i holds [ws, we) of row w0 + i
@@ -654,12 +670,12 @@ int ensure_graph_items(const mph_graph* gc, cudaStream_t s) {
   return MPH_OK;
 }
 
-template <int LPR, int VPL, bool HAS_VAL, int UOV = 0, bool SGN = false>
+template <int LPR, int VPL, bool HAS_VAL, int UOV = 0, bool SGN = false, bool CARRY = false>
 static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
   static int blocks_per_sm = 0;
   static int sms = 0;
   if (!blocks_per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<LPR, VPL, HAS_VAL, UOV, SGN>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_spmm<LPR, VPL, HAS_VAL, UOV, SGN, CARRY>, 256, 0);
     blocks_per_sm = std::max(1, blocks_per_sm);
     int dev = 0;
     cudaGetDevice(&dev);
@@ -667,7 +683,7 @@ static int launch_spmm(const SpmmArgs& a, cudaStream_t s) {
   }
   const int64_t grid = std::min<int64_t>((int64_t)sms * blocks_per_sm, ceil_div(a.n_items, 8));
   MPH_CUDA_TRY(cudaMemsetAsync(a.counter, 0, sizeof(int), s));
-  k_spmm<LPR, VPL, HAS_VAL, UOV, SGN><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
+  k_spmm<LPR, VPL, HAS_VAL, UOV, SGN, CARRY><<<(unsigned)std::max<int64_t>(1, grid), 256, 0, s>>>(a);
   count_launch();
   return launch_check("spmm");
 }
@@ -727,7 +743,12 @@ static int dispatch_spmm(const SpmmArgs& a, cudaStream_t s) {
     // 48-wide rows: 4 lanes x 3 float4 (8 edge slots) where rows are long (reddit: the shuffle
     // reduction is amortised), 16 lanes x 1 float4 with 12 active (2 slots, a third of the
     // cross-slot reduction) at moderate degree (products, mean 26: -1.7 % epoch)
-    if (a.mid_degree) return launch_spmm_u<16, 1, HAS_VAL, SGN>(a, s);
+    if (a.mid_degree) {
+      if constexpr (!HAS_VAL) {
+        if (a.contig) return launch_spmm<16, 1, false, 0, SGN, true>(a, s);  // ids carried across rows
+      }
+      return launch_spmm_u<16, 1, HAS_VAL, SGN>(a, s);
+    }
     return launch_spmm_u<4, 3, HAS_VAL, SGN>(a, s);
   }
   if (nv4 <= 16) return launch_spmm_u<16, 1, HAS_VAL, SGN>(a, s);
@@ -756,7 +777,13 @@ static int run_spmm(SpmmArgs a, const mph_graph* g, cudaStream_t s) {
   const bool big = g->split_mode == 2 || ((int64_t)g->n_cols * a.nv4 * 16 > l2_bytes / 2 && a.nv4 >= 16);
   const mph_graph::SplitCsr& c = g->scsr[a.part + 1];
   const bool use_split = c.items && !rows_kernel && big;
-  if (!use_split) return dispatch_spmm<false>(a, s);
+  if (!use_split) {
+    // carry each row's first ids over from the previous row's last block on graphs of moderate
+    // degree (products' 48-wide rows, 26 edges each: 1.65 -> 1.52 ms); on reddit's long rows and
+    // on the chunked CSR it measured 1-8 % slower
+    a.contig = (a.part == -1 && a.mid_degree) ? 1 : 0;
+    return dispatch_spmm<false>(a, s);
+  }
   a.row_ptr = c.vrow_ptr;
   // whole rows: virtual row v ends where v + 1 begins; parts: explicit ends after the n_v begins
   a.row_end = a.part == -1 ? c.vrow_ptr + 1 : c.vrow_ptr + c.n_vrows;
@@ -804,6 +831,8 @@ int spmm_launch(const mph_graph* g, int part, const float* in, int w, int ld_in,
   a.val = nullptr;
   a.row_ptr = g->row_ptr;
   a.row_end = g->row_ptr + 1;
+  a.col_len = g->nnz;
+  a.contig = 0;  // set per launch in run_spmm
   a.split = g->split;
   a.col = g->col_idx;
   a.dinv = post;
@@ -867,6 +896,8 @@ int spmm_csr_launch(const int64_t* row_ptr, const int32_t* col, const float* val
   SpmmArgs a{};
   a.row_ptr = row_ptr;
   a.row_end = row_ptr + 1;
+  a.col_len = 0;
+  a.contig = 0;  // (X_csr / X_csc-segment launches: no cross-row id prefetch)
   a.split = nullptr;
   a.col = col;
   a.val = val;
