@@ -542,7 +542,7 @@ int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** i
 // The chunked virtual CSR of whole-row launches (part -1): every row longer than S edges is cut
 // into ⌈deg/S⌉ virtual rows of ≤ S consecutive CSR entries (vrow_ptr indexes the graph's col_idx;
 // vmap[v] = -1 - chunk), the other rows stay whole (vmap[v] = row), and the work items are runs of
-// consecutive virtual rows of about S edges, all in row order.  Walking the graph in row order
+// consecutive virtual rows of about S/2 edges, all in row order.  Walking the graph in row order
 // keeps the rows gathered at any moment a narrow window (a community of the planted partition, the
 // co-purchase clusters of products): with long rows as whole items, served first, the one warp on
 // a hub keeps gathering long after the rest of the grid has moved on, and its hits become misses
@@ -614,9 +614,14 @@ static int build_split_items(mph_graph* g, cudaStream_t s) {
     }
     int v0 = 0;
     int64_t acc = 0;
+    // edges per work item: half a chunk — a narrower window of rows in flight than items of S
+    // (products per call: S/2 = 128 edges 4.62-4.64 ms vs 4.68-4.73 at 256, 5.0 at 512;
+    // profiles/r02_experiments/spmm_chunked_csr.txt); MPH_SPMM_RUN_EDGES overrides (experiments)
+    static const int64_t run_env = getenv("MPH_SPMM_RUN_EDGES") ? atoll(getenv("MPH_SPMM_RUN_EDGES")) : 0;
+    const int64_t R = run_env > 0 ? run_env : std::max<int64_t>(32, S / 2);
     for (int v = 0; v < n_v; ++v) {
       acc += vend[v] - vrp[v];
-      if (acc >= S) {
+      if (acc >= R) {
         items.push_back(make_int2(v0, v + 1));
         v0 = v + 1;
         acc = 0;
