@@ -478,7 +478,7 @@ Dropout make_dropout(const mph_epilogue* e) {
 }
 
 // Work items (built once per graph, on the host from row_ptr): runs of consecutive rows of
-// about E edges, E = nnz / (32 items per resident warp) clamped to [64, 2048]; a row longer
+// about E edges, E = nnz / (32 items per resident warp) clamped to [64, 512]; a row longer
 // than E is an item of its own.  Items holding a row longer than 4E ("hubs") come first,
 // longest first.
 int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** items_out, int* n_items,
@@ -486,7 +486,9 @@ int build_work_items(const int64_t* row_ptr_d, int n_rows, int64_t nnz, int2** i
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(2048, nnz / ((int64_t)sms * 24 * 32)));
+  // clamped to [64, 512]: reddit's E = 1010 -> 512 measured 0.8-2.3 % faster per call (a narrower
+  // window of rows in flight; profiles/r02_experiments/spmm_item_edges_sweep.txt)
+  int64_t kItemEdges = std::max<int64_t>(64, std::min<int64_t>(512, nnz / ((int64_t)sms * 24 * 32)));
   if (const char* ie = getenv("MPH_SPMM_ITEM_EDGES")) kItemEdges = std::max<int64_t>(8, atoll(ie));  // experiments
   std::vector<int64_t> rp((size_t)n_rows + 1);
   MPH_CUDA_TRY(cudaMemcpyAsync(rp.data(), row_ptr_d, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
